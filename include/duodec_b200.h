@@ -1,0 +1,226 @@
+/*
+ * duodec_b200.h — C ABI of the B200-native DuoDecoding target path.
+ *
+ * This is the drop-in seam below the reference's model/verifier contract
+ * (reference = DuoDecoding C++ library under proj/ of arxiv 2503.00784).
+ * Every entry point names the reference interface it replaces:
+ *
+ *   dd_prefill / dd_score   <- ModelSpec::forward / forward_scored
+ *                              (proj/include/duodec/model.hpp:57-65) as used by
+ *                              scored_with_next + target_step
+ *                              (proj/src/engine.cpp:36-43, 145-157)
+ *   dd_verify               <- verify_prefix / verify_bundle / sps_verify
+ *                              (proj/include/duodec/verify.hpp:43-44, 53-54, 66-68;
+ *                              proj/src/verify.cpp:41-107) plus the per-draw
+ *                              RandomStream schedule (proj/include/duodec/random.hpp:16-26)
+ *   dd_kv_truncate          <- the verified-prefix commit/truncate of
+ *                              apply_verification (proj/src/engine.cpp:62-106)
+ *   dd_time_pass            <- the target half of calibrate (proj/src/engine.cpp:534-578)
+ *   dd_engine_run           <- run_vanilla / run_sps / run_duo
+ *                              (proj/include/duodec/engine.hpp:102-116)
+ *   dd_calibrate            <- calibrate + choose_budget (engine.hpp:118-126)
+ *
+ * Conventions: no exceptions cross this boundary; every int-returning call
+ * returns 0 on success and a negative DD_E* code otherwise, with a message
+ * available from dd_last_error().  A dd_ctx owns one CUDA stream on one GPU
+ * and is not thread-safe: it is driven only from the target-role thread, as
+ * the reference drives ModelSpec::forward only from the engine thread
+ * (engine.cpp:458-478).  There is no CPU fallback: creating a context on a
+ * machine without a Blackwell (sm_100) GPU fails with DD_E_CUDA.
+ */
+#ifndef DUODEC_B200_H
+#define DUODEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DD_OK 0
+#define DD_E_ARG (-1)      /* ConfigError / invalid argument            */
+#define DD_E_CUDA (-2)     /* CUDA / driver failure (includes "no GPU") */
+#define DD_E_STATE (-3)    /* call sequence violated (e.g. no pass yet) */
+#define DD_E_CAPACITY (-4) /* KV cache or pass width exceeded           */
+
+typedef struct dd_ctx dd_ctx;
+typedef struct dd_draft dd_draft;
+
+/* Llama-family shape (the target; the CPU draft uses the same struct). */
+typedef struct dd_model_desc {
+    int n_layers;
+    int d_model;
+    int n_heads;
+    int n_kv_heads;
+    int head_dim;
+    int ffn_dim;
+    int vocab;
+    float rms_eps;    /* 1e-5 for Llama-2 */
+    float rope_theta; /* 1e4 for Llama-2  */
+    int max_seq;      /* KV capacity in tokens */
+    int page_size;    /* tokens per KV page (0 -> 16) */
+} dd_model_desc;
+
+/* Synthetic random-init weights with an optional planted shared bigram
+ * (SURVEY.md §7 hard part 1): a fraction `alpha` of tokens t get the LM-head
+ * row of pi(t) aligned with their embedding, in target and draft alike. */
+typedef struct dd_plant_desc {
+    uint64_t plant_seed; /* permutation pi and planted set                   */
+    double alpha;        /* fraction of planted tokens (0 = pure random init) */
+    float gain;          /* planted logit gain                                */
+    float emb_std;       /* embedding std (0 -> 0.02)                         */
+} dd_plant_desc;
+
+/* ------------------------------------------------------------ target ctx */
+int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out);
+void dd_ctx_destroy(dd_ctx* ctx);
+const char* dd_last_error(const dd_ctx* ctx); /* ctx may be NULL: global error */
+
+/* Generate all weights on the device from (weight_seed, plant); bit-identical
+ * to the CPU oracle's generator (oracle/llama_ref.c). plant may be NULL. */
+int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plant);
+
+/* Append n tokens to the KV cache without producing logits (chunked). */
+int dd_prefill(dd_ctx* ctx, const int32_t* tokens, int n);
+
+/* One scored pass: append w (<= 256) tokens at positions n_cached.. and
+ * compute fp32 logits for all w rows (kept on the device).  Row i is the
+ * target's next-token logits after tokens[i], i.e. forward_scored rows plus
+ * the trailing p_next row of scored_with_next. */
+int dd_score(dd_ctx* ctx, const int32_t* tokens, int w);
+
+int dd_kv_len(const dd_ctx* ctx, int* n_cached);
+/* Roll the cache back to n_valid tokens (KV rollback after a rejection). */
+int dd_kv_truncate(dd_ctx* ctx, int n_valid);
+/* In-place compaction: move cache slots src_pos[i] -> dst_pos[i] (i < n),
+ * in order; used to keep an accepted non-chain branch contiguous. */
+int dd_kv_compact(dd_ctx* ctx, const int32_t* src_pos, const int32_t* dst_pos, int n);
+
+/* Copy logits rows [row0, row0+rows) of the last pass to host memory. */
+int dd_read_logits(dd_ctx* ctx, float* host, int row0, int rows);
+
+/* Draft next-token distributions for the tail rows (fp32, rows x vocab). The
+ * copy runs on a side stream and overlaps the next dd_score. */
+int dd_upload_q(dd_ctx* ctx, const float* q_rows, int rows, int vocab);
+
+#define DD_MODE_DUO 0     /* verify_prefix (tail) then verify_bundle          */
+#define DD_MODE_SPS 1     /* sps_verify                                        */
+#define DD_MODE_VANILLA 2 /* sample(p, next_uniform) — run_vanilla step        */
+
+typedef struct dd_verify_args {
+    int mode;
+    int tail_len;       /* L: rows of the last pass tested against the tail  */
+    int n_firsts;       /* s: bundle first tokens (duo)                      */
+    int32_t firsts[16]; /* bundle first tokens in bundle order               */
+    uint64_t seed;      /* verify RandomStream seed                          */
+    uint64_t counter;   /* draws already consumed on entry                   */
+    double temperature; /* > 0, used unless greedy                           */
+    int greedy;         /* one-hot target at argmax (lowest id on ties)      */
+    int q_onehot;       /* draft q rows are one-hot on the drafted tokens     */
+} dd_verify_args;
+
+typedef struct dd_verify_out {
+    int prefix_all_accepted; /* duo: tail fully accepted (or empty)           */
+    int reject_index;        /* duo/sps: first rejected position, -1 if none  */
+    int resample;            /* duo: residual resample token                  */
+    int bundle_accepted;     /* duo                                           */
+    int seq_index;           /* duo: accepted bundle sequence                 */
+    int fallback;            /* duo: token drawn when every sequence rejected */
+    int sps_accepted;        /* sps: accepted draft length                    */
+    int next_token;          /* sps: resample or bonus; vanilla: sampled token*/
+    int n_draws;             /* uniforms consumed                              */
+    int pad;
+    uint64_t counter_out;    /* counter + n_draws                              */
+} dd_verify_out;
+
+/* Fused logits -> softmax -> speculative-sampling acceptance on the last
+ * L+1 rows of the last pass (tail tokens = last L tokens of that pass). */
+int dd_verify(dd_ctx* ctx, const dd_verify_args* args, dd_verify_out* out);
+
+/* Same acceptance kernel fed with host fp64 probability rows (L+1 x vocab) and
+ * explicit tail tokens instead of logits — the path used to run the
+ * reference's Markov-table models through the GPU verifier. */
+int dd_verify_probs(dd_ctx* ctx, const double* p_rows, const int32_t* tail_tokens,
+                    int vocab, const dd_verify_args* args, dd_verify_out* out);
+
+/* Median device time (CUDA events) of a scored pass of width w. */
+int dd_time_pass(dd_ctx* ctx, int w, int trials, float* median_ms);
+
+/* Per-kernel device time breakdown of one pass of width w (ms, by class:
+ * 0 gemm, 1 attention, 2 epilogues/norms, 3 total). */
+int dd_profile_pass(dd_ctx* ctx, int w, float* ms4);
+
+/* Algorithmic weight bytes streamed by one pass (excludes the gathered
+ * embedding), for the roofline. */
+uint64_t dd_pass_weight_bytes(const dd_ctx* ctx);
+
+/* ------------------------------------------------------------ CPU draft */
+int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_plant_desc* plant,
+                    int n_threads, const int* cpus, int n_cpus, dd_draft** out);
+void dd_draft_destroy(dd_draft* d);
+/* Next-token logits (fp32, vocab) after the given context (KV reused). */
+int dd_draft_logits(dd_draft* d, const int32_t* ctx_tokens, int n, float* logits);
+/* Median wall time of one single-token draft forward (calibrate denominator). */
+int dd_draft_time_token(dd_draft* d, int trials, float* median_ms);
+
+/* ------------------------------------------------------------ engine */
+#define DD_BUDGET_FIXED 0
+#define DD_BUDGET_CALIBRATED 1
+
+typedef struct dd_engine_config { /* EngineConfig (engine.hpp:43-60) */
+    int mode;           /* DD_MODE_*                                           */
+    int budget;         /* gamma                                               */
+    int max_sequences;  /* s_max                                               */
+    int max_new_tokens; /* L                                                   */
+    double temperature; /* > 0; ignored when greedy                            */
+    int greedy;         /* one-hot target and draft (argmax, lowest-id ties)   */
+    uint64_t draft_seed;
+    uint64_t verify_seed;
+    int budget_policy;  /* DD_BUDGET_*                                         */
+    int budget_hard_cap;
+    int calib_probe_len;
+    int calib_trials;
+    int threaded;       /* DuoExecution::threaded (1) / sequential (0)         */
+} dd_engine_config;
+
+typedef struct dd_iteration_record { /* IterationRecord (engine.hpp:62-70) */
+    double draft_ms;
+    double target_ms;
+    double verify_ms;
+    double comm_ms;
+    int tokens_processed;
+    int sequence_count;
+    int accepted;
+    int width; /* scored-pass width W = 1 + tail */
+} dd_iteration_record;
+
+typedef struct dd_generation_result { /* GenerationResult (engine.hpp:72-78) */
+    int32_t* tokens;    /* caller buffer, capacity max_tokens              */
+    int max_tokens;
+    int n_tokens;
+    dd_iteration_record* iterations; /* caller buffer, capacity max_iterations */
+    int max_iterations;
+    int n_iterations;
+    double ttft_ms;
+    double total_ms;
+    double tps;
+    double prefill_ms;
+    int budget_used;
+} dd_generation_result;
+
+/* Run one generation: target on the GPU (ctx), draft on host cores (draft,
+ * may be NULL for vanilla).  prompt is a host buffer. */
+int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
+                  const int32_t* prompt, int n_prompt, dd_generation_result* out);
+
+/* calibrate(): median GPU scored pass at probe_len over median CPU draft
+ * token; *budget = choose_budget(c) capped at hard_cap. */
+int dd_calibrate(dd_ctx* ctx, dd_draft* draft, int probe_len, int trials, int hard_cap,
+                 double* cost_coefficient, int* budget);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DUODEC_B200_H */

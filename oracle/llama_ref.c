@@ -1,0 +1,438 @@
+/*
+ * oracle/llama_ref.c — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+ *
+ * CPU restatement of the target forward contract that the reference leaves
+ * abstract: ModelSpec::forward / forward_scored (reference
+ * proj/include/duodec/model.hpp:57-65, proj/src/model.cpp:286-320) and
+ * scored_with_next (proj/src/engine.cpp:36-43): row i of a pass is the
+ * next-token distribution after tokens[0..i].  The reference's model is a
+ * Markov table; the north star replaces it by a Llama-2-shape transformer with
+ * seeded random-init weights, so this file is the logit-level oracle.  Its
+ * Llama math is cross-checked against transformers' LlamaForCausalLM
+ * (tests/test_oracle_llama.py); PARITY NOTE: the forward itself has no
+ * reference arithmetic to pin against.
+ *
+ * Numerics mirror the GPU pass (paper_2503_00784_b200/csrc/model.cu): fp32
+ * residual stream, bf16 rounding of every GEMM input (h, o, a) and of cached
+ * K/V, fp32 accumulation, q kept fp32, RoPE from a double-precision table.
+ * Only tests/, bench.py's cpu_baseline leg and __graft_entry__.smoke() load it.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <pthread.h>
+#include <string.h>
+
+/* ------------------------------------------------------------ threads */
+typedef void (*range_fn)(void* arg, int64_t lo, int64_t hi);
+typedef struct {
+    range_fn fn;
+    void* arg;
+    int64_t lo, hi;
+} par_job;
+static int g_threads = 1;
+static void* par_entry(void* p) {
+    par_job* j = (par_job*)p;
+    j->fn(j->arg, j->lo, j->hi);
+    return NULL;
+}
+/* static partition of [0, n) over g_threads pthreads */
+static void par_range(int64_t n, range_fn fn, void* arg) {
+    int nt = g_threads;
+    if (nt > n) nt = (int)n;
+    if (nt <= 1) {
+        fn(arg, 0, n);
+        return;
+    }
+    pthread_t th[256];
+    par_job jobs[256];
+    for (int i = 0; i < nt; ++i) {
+        jobs[i].fn = fn;
+        jobs[i].arg = arg;
+        jobs[i].lo = n * i / nt;
+        jobs[i].hi = n * (i + 1) / nt;
+        if (i > 0) pthread_create(&th[i], NULL, par_entry, &jobs[i]);
+    }
+    par_entry(&jobs[0]);
+    for (int i = 1; i < nt; ++i) pthread_join(th[i], NULL);
+}
+
+/* ------------------------------------------------------------ generator */
+static inline uint64_t mix(uint64_t seed, uint64_t m) { /* random.hpp:16-21 */
+    uint64_t z = seed + m * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+static inline uint64_t derive(uint64_t base, uint64_t index) { /* random.hpp:38-43 */
+    uint64_t z = base + (index + 1) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 30)) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+static inline float unit(uint64_t seed, uint64_t e) {
+    const uint64_t x = mix(seed, e + 1);
+    return (float)(int32_t)(x >> 40) * 0x1.0p-23f - 1.0f;
+}
+static inline uint16_t f2bf(float f) { /* round to nearest even (finite inputs) */
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+static inline float bf2f(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+static inline float bfr(float f) { return bf2f(f2bf(f)); }
+
+enum { T_WQ = 0, T_WK = 1, T_WV = 2, T_WO = 3, T_WG = 4, T_WU = 5, T_WD = 6 };
+static uint64_t tensor_id(int layer, int kind) { return 2 + (uint64_t)layer * 8 + (uint64_t)kind; }
+
+typedef struct {
+    uint16_t* dst;
+    uint64_t seed;
+    float amp;
+} gen_arg;
+static void gen_range(void* p, int64_t lo, int64_t hi) {
+    gen_arg* a = (gen_arg*)p;
+    for (int64_t e = lo; e < hi; ++e) a->dst[e] = f2bf(unit(a->seed, (uint64_t)e) * a->amp);
+}
+static void gen_matrix(uint16_t* dst, uint64_t n, uint64_t seed, float amp) {
+    gen_arg a = {dst, seed, amp};
+    par_range((int64_t)n, gen_range, &a);
+}
+
+/* plant table: identical recipe to paper_2503_00784_b200/csrc/plant.cpp */
+static int make_plant(int vocab, int d, uint64_t plant_seed, double alpha, float gain,
+                      float emb_std, int32_t* src, float* coef) {
+    int any = 0;
+    int32_t* perm = (int32_t*)malloc(sizeof(int32_t) * vocab);
+    for (int i = 0; i < vocab; ++i) {
+        perm[i] = i;
+        src[i] = -1;
+    }
+    *coef = 0.0f;
+    if (alpha > 0.0) {
+        uint64_t counter = 0;
+        for (int i = vocab - 1; i >= 1; --i) {
+            const uint64_t j = mix(plant_seed, ++counter) % (uint64_t)(i + 1);
+            const int32_t t = perm[i];
+            perm[i] = perm[j];
+            perm[j] = t;
+        }
+        const uint64_t sel = derive(plant_seed, 1);
+        for (int tok = 0; tok < vocab; ++tok) {
+            const double u = (double)(mix(sel, (uint64_t)tok + 1) >> 11) * 0x1.0p-53;
+            if (u < alpha) {
+                src[perm[tok]] = tok;
+                any = 1;
+            }
+        }
+        *coef = (float)((double)gain / ((double)emb_std * sqrt((double)d)));
+    }
+    free(perm);
+    return any;
+}
+
+/* ------------------------------------------------------------ model */
+typedef struct {
+    uint16_t *qkv, *o, *gu, *dn;
+} orc_layer;
+
+typedef struct orc_llama {
+    int L, d, H, Hkv, hd, F, V, max_seq, n_cached, n_threads;
+    float eps, theta;
+    uint16_t *emb, *head;
+    orc_layer* layers;
+    uint16_t* kv; /* [L][2][Hkv][max_seq][hd] */
+    float *rope_cos, *rope_sin;
+    int32_t* plant_src;
+    int32_t* plant_perm;
+} orc_llama;
+
+static size_t kv_idx(const orc_llama* m, int layer, int kv, int h, int pos) {
+    return ((((size_t)layer * 2 + kv) * m->Hkv + h) * m->max_seq + pos) * m->hd;
+}
+
+typedef struct {
+    orc_llama* m;
+    uint64_t seed;
+    float amp, coef;
+    int any;
+} head_arg;
+static void head_range(void* p, int64_t lo, int64_t hi) {
+    head_arg* a = (head_arg*)p;
+    const int d = a->m->d;
+    for (int64_t e = lo; e < hi; ++e) {
+        float w = unit(a->seed, (uint64_t)e) * a->amp;
+        const int64_t v = e / d, i = e % d;
+        const int32_t t = a->any ? a->m->plant_src[v] : -1;
+        if (t >= 0) w = fmaf(a->coef, bf2f(a->m->emb[(size_t)t * d + i]), w);
+        a->m->head[e] = f2bf(w);
+    }
+}
+
+orc_llama* orc_llama_create(int n_layers, int d, int n_heads, int n_kv_heads, int head_dim,
+                            int ffn, int vocab, float eps, float theta, int max_seq,
+                            uint64_t weight_seed, uint64_t plant_seed, double alpha, float gain,
+                            float emb_std, int n_threads) {
+    orc_llama* m = (orc_llama*)calloc(1, sizeof(orc_llama));
+    m->L = n_layers;
+    m->d = d;
+    m->H = n_heads;
+    m->Hkv = n_kv_heads > 0 ? n_kv_heads : n_heads;
+    m->hd = head_dim;
+    m->F = ffn;
+    m->V = vocab;
+    m->eps = eps;
+    m->theta = theta;
+    m->max_seq = max_seq;
+    m->n_threads = n_threads;
+    g_threads = n_threads > 0 ? (n_threads > 256 ? 256 : n_threads) : 1;
+    if (!(emb_std > 0.0f)) emb_std = 0.02f;
+    const int qd = m->H * m->hd, kvd = m->Hkv * m->hd;
+    const float amp_proj = (float)(0.02 * sqrt(3.0));
+    const float amp_out = (float)(0.02 / sqrt(2.0 * n_layers) * sqrt(3.0));
+    const float amp_emb = (float)(emb_std * sqrt(3.0));
+    m->emb = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)vocab * d);
+    m->head = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)vocab * d);
+    gen_matrix(m->emb, (uint64_t)vocab * d, derive(weight_seed, 0), amp_emb);
+    m->plant_src = (int32_t*)malloc(sizeof(int32_t) * vocab);
+    float coef = 0.0f;
+    const int any = make_plant(vocab, d, plant_seed, alpha, gain, emb_std, m->plant_src, &coef);
+    {
+        head_arg ha = {m, derive(weight_seed, 1), amp_proj, coef, any};
+        par_range((int64_t)vocab * d, head_range, &ha);
+    }
+    m->layers = (orc_layer*)calloc(n_layers, sizeof(orc_layer));
+    for (int l = 0; l < n_layers; ++l) {
+        orc_layer* Ly = &m->layers[l];
+        Ly->qkv = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)(qd + 2 * kvd) * d);
+        Ly->o = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)d * qd);
+        Ly->gu = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)2 * ffn * d);
+        Ly->dn = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)d * ffn);
+        gen_matrix(Ly->qkv, (uint64_t)qd * d, derive(weight_seed, tensor_id(l, T_WQ)), amp_proj);
+        gen_matrix(Ly->qkv + (size_t)qd * d, (uint64_t)kvd * d,
+                   derive(weight_seed, tensor_id(l, T_WK)), amp_proj);
+        gen_matrix(Ly->qkv + (size_t)(qd + kvd) * d, (uint64_t)kvd * d,
+                   derive(weight_seed, tensor_id(l, T_WV)), amp_proj);
+        gen_matrix(Ly->o, (uint64_t)d * qd, derive(weight_seed, tensor_id(l, T_WO)), amp_out);
+        gen_matrix(Ly->gu, (uint64_t)ffn * d, derive(weight_seed, tensor_id(l, T_WG)), amp_proj);
+        gen_matrix(Ly->gu + (size_t)ffn * d, (uint64_t)ffn * d,
+                   derive(weight_seed, tensor_id(l, T_WU)), amp_proj);
+        gen_matrix(Ly->dn, (uint64_t)d * ffn, derive(weight_seed, tensor_id(l, T_WD)), amp_out);
+    }
+    m->kv = (uint16_t*)calloc((size_t)n_layers * 2 * m->Hkv * max_seq * head_dim, sizeof(uint16_t));
+    const int half = head_dim / 2;
+    m->rope_cos = (float*)malloc(sizeof(float) * (size_t)max_seq * half);
+    m->rope_sin = (float*)malloc(sizeof(float) * (size_t)max_seq * half);
+    for (int p = 0; p < max_seq; ++p)
+        for (int i = 0; i < half; ++i) {
+            const double inv = pow((double)theta, -2.0 * i / (double)head_dim);
+            const double ang = (double)p * inv;
+            m->rope_cos[(size_t)p * half + i] = (float)cos(ang);
+            m->rope_sin[(size_t)p * half + i] = (float)sin(ang);
+        }
+    return m;
+}
+
+void orc_llama_free(orc_llama* m) {
+    if (!m) return;
+    for (int l = 0; l < m->L; ++l) {
+        free(m->layers[l].qkv);
+        free(m->layers[l].o);
+        free(m->layers[l].gu);
+        free(m->layers[l].dn);
+    }
+    free(m->layers);
+    free(m->emb);
+    free(m->head);
+    free(m->kv);
+    free(m->rope_cos);
+    free(m->rope_sin);
+    free(m->plant_src);
+    free(m);
+}
+
+int orc_llama_len(const orc_llama* m) { return m->n_cached; }
+void orc_llama_truncate(orc_llama* m, int n) {
+    if (n >= 0 && n <= m->n_cached) m->n_cached = n;
+}
+/* raw bf16 bits of a weight tensor: which 0 emb, 1 head, 2 qkv, 3 o, 4 gu, 5 down */
+const uint16_t* orc_llama_tensor(const orc_llama* m, int which, int layer) {
+    switch (which) {
+        case 0: return m->emb;
+        case 1: return m->head;
+        case 2: return m->layers[layer].qkv;
+        case 3: return m->layers[layer].o;
+        case 4: return m->layers[layer].gu;
+        default: return m->layers[layer].dn;
+    }
+}
+const int32_t* orc_llama_plant_src(const orc_llama* m) { return m->plant_src; }
+
+/* fp32 dot of a bf16 weight row with an fp32 activation row (16 partial sums) */
+static inline float dot_bf16(const uint16_t* w, const float* x, int k) {
+    float acc[16] = {0};
+    int i = 0;
+    for (; i + 16 <= k; i += 16)
+        for (int j = 0; j < 16; ++j) acc[j] += bf2f(w[i + j]) * x[i + j];
+    for (; i < k; ++i) acc[i & 15] += bf2f(w[i]) * x[i];
+    float s = 0.0f;
+    for (int j = 0; j < 16; ++j) s += acc[j];
+    return s;
+}
+
+/* y[t][n] = W[n,:] . x[t,:]  for t < w, n < rows */
+typedef struct {
+    const uint16_t* W;
+    int rows, k, w;
+    const float* x;
+    float* y;
+} mm_arg;
+static void mm_range(void* p, int64_t lo, int64_t hi) {
+    mm_arg* a = (mm_arg*)p;
+    for (int64_t n = lo; n < hi; ++n)
+        for (int t = 0; t < a->w; ++t)
+            a->y[(size_t)t * a->rows + n] =
+                dot_bf16(a->W + (size_t)n * a->k, a->x + (size_t)t * a->k, a->k);
+}
+static void matmul(const uint16_t* W, int rows, int k, const float* x, int w, float* y) {
+    mm_arg a = {W, rows, k, w, x, y};
+    par_range(rows, mm_range, &a);
+}
+
+static void rmsnorm_bf(const float* x, int d, float eps, float* h) {
+    float ss = 0.0f;
+    for (int i = 0; i < d; ++i) ss = fmaf(x[i], x[i], ss);
+    const float r = 1.0f / sqrtf(ss / (float)d + eps);
+    for (int i = 0; i < d; ++i) h[i] = bfr((x[i] * r) * 1.0f);
+}
+
+typedef struct {
+    orc_llama* m;
+    int l, n0, w;
+    const float* q;
+    float* o;
+    float scale;
+} attn_arg;
+static void attn_range(void* p, int64_t lo, int64_t hi) {
+    attn_arg* a = (attn_arg*)p;
+    orc_llama* m = a->m;
+    const int hd = m->hd, H = m->H, Hkv = m->Hkv, qd = H * hd, l = a->l;
+    for (int64_t job = lo; job < hi; ++job) {
+        const int head = (int)(job / a->w), t = (int)(job % a->w);
+        const int pos = a->n0 + t, nk = pos + 1;
+        const int kvh = head / (H / Hkv);
+        const float* qv = a->q + (size_t)t * qd + head * hd;
+        float* sc = (float*)malloc(sizeof(float) * nk);
+        float mx = -INFINITY;
+        for (int j = 0; j < nk; ++j) {
+            const uint16_t* kr = m->kv + kv_idx(m, l, 0, kvh, j);
+            float acc = 0.0f;
+            for (int i = 0; i < hd; ++i) acc = fmaf(qv[i], bf2f(kr[i]), acc);
+            sc[j] = acc * a->scale;
+            if (sc[j] > mx) mx = sc[j];
+        }
+        float sum = 0.0f;
+        for (int j = 0; j < nk; ++j) {
+            sc[j] = expf(sc[j] - mx);
+            sum += sc[j];
+        }
+        const float inv = 1.0f / sum;
+        for (int i = 0; i < hd; ++i) {
+            float acc = 0.0f;
+            for (int j = 0; j < nk; ++j) acc = fmaf(sc[j], bf2f(m->kv[kv_idx(m, l, 1, kvh, j) + i]), acc);
+            a->o[(size_t)t * qd + head * hd + i] = bfr(acc * inv);
+        }
+        free(sc);
+    }
+}
+
+/* One scored pass of w tokens at positions n_cached..; logits [w][V] (or only
+ * the last row when last_only, written at logits[0..V)). */
+int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits, int last_only) {
+    if (w < 1 || m->n_cached + w > m->max_seq) return -1;
+    const int d = m->d, hd = m->hd, H = m->H, Hkv = m->Hkv, F = m->F, V = m->V;
+    const int qd = H * hd, kvd = Hkv * hd, rows = qd + 2 * kvd, half = hd / 2;
+    const int n0 = m->n_cached;
+    float* x = (float*)malloc(sizeof(float) * (size_t)w * d);
+    float* h = (float*)malloc(sizeof(float) * (size_t)w * d);
+    float* qkv = (float*)malloc(sizeof(float) * (size_t)w * rows);
+    float* q = (float*)malloc(sizeof(float) * (size_t)w * qd);
+    float* o = (float*)malloc(sizeof(float) * (size_t)w * qd);
+    float* y = (float*)malloc(sizeof(float) * (size_t)w * (2 * F > d ? 2 * F : d));
+    float* a = (float*)malloc(sizeof(float) * (size_t)w * F);
+    for (int t = 0; t < w; ++t) {
+        if (tokens[t] < 0 || tokens[t] >= V) return -2;
+        for (int i = 0; i < d; ++i) x[(size_t)t * d + i] = bf2f(m->emb[(size_t)tokens[t] * d + i]);
+        rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+    }
+    const float scale = (float)(1.0 / sqrt((double)hd));
+    for (int l = 0; l < m->L; ++l) {
+        const orc_layer* Ly = &m->layers[l];
+        matmul(Ly->qkv, rows, d, h, w, qkv);
+        for (int t = 0; t < w; ++t) {
+            const int pos = n0 + t;
+            const float* cs = m->rope_cos + (size_t)pos * half;
+            const float* sn = m->rope_sin + (size_t)pos * half;
+            const float* r = qkv + (size_t)t * rows;
+            for (int head = 0; head < H + Hkv; ++head)
+                for (int i = 0; i < half; ++i) {
+                    const float av = r[head * hd + i], bv = r[head * hd + i + half];
+                    const float lo = fmaf(av, cs[i], -(bv * sn[i]));
+                    const float hi = fmaf(bv, cs[i], av * sn[i]);
+                    if (head < H) {
+                        q[(size_t)t * qd + head * hd + i] = lo;
+                        q[(size_t)t * qd + head * hd + i + half] = hi;
+                    } else {
+                        uint16_t* kd = m->kv + kv_idx(m, l, 0, head - H, pos);
+                        kd[i] = f2bf(lo);
+                        kd[i + half] = f2bf(hi);
+                    }
+                }
+            for (int e = 0; e < kvd; ++e)
+                m->kv[kv_idx(m, l, 1, e / hd, pos) + e % hd] = f2bf(r[qd + kvd + e]);
+        }
+        /* attention: query t (pos n0+t) over keys 0..pos */
+        {
+            attn_arg aa = {m, l, n0, w, q, o, scale};
+            par_range((int64_t)H * w, attn_range, &aa);
+        }
+        matmul(Ly->o, d, qd, o, w, y);
+        for (int t = 0; t < w; ++t) {
+            for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
+            rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+        }
+        matmul(Ly->gu, 2 * F, d, h, w, y);
+        for (int t = 0; t < w; ++t)
+            for (int f = 0; f < F; ++f) {
+                const float g = y[(size_t)t * 2 * F + f], u = y[(size_t)t * 2 * F + F + f];
+                const float silu = g / (1.0f + expf(-g));
+                a[(size_t)t * F + f] = bfr(silu * u);
+            }
+        matmul(Ly->dn, d, F, a, w, y);
+        for (int t = 0; t < w; ++t) {
+            for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
+            rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+        }
+    }
+    if (logits) {
+        if (last_only)
+            matmul(m->head, V, d, h + (size_t)(w - 1) * d, 1, logits);
+        else
+            matmul(m->head, V, d, h, w, logits);
+    }
+    m->n_cached += w;
+    free(x);
+    free(h);
+    free(qkv);
+    free(q);
+    free(o);
+    free(y);
+    free(a);
+    return 0;
+}

@@ -1,0 +1,85 @@
+// dd_ctx: the target-role context behind the C ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/duodec_b200.h"
+#include "gemm.h"
+#include "model.h"
+#include "plant.h"
+
+namespace dd {
+
+struct LayerW {
+    __nv_bfloat16* qkv = nullptr;  // [q_dim + 2 kv_dim, d]
+    __nv_bfloat16* o = nullptr;    // [d, q_dim]
+    __nv_bfloat16* gu = nullptr;   // [2 ffn, d]  (gate rows, then up rows)
+    __nv_bfloat16* dn = nullptr;   // [d, ffn]
+    CUtensorMap map_qkv, map_o, map_gu, map_d;
+};
+
+constexpr int kPsRing = 4;
+
+}  // namespace dd
+
+struct dd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    cudaEvent_t q_ready = nullptr;
+    cudaEvent_t ps_done[dd::kPsRing] = {};
+    dd::ModelDims m{};
+    int max_seq = 0, page_size = 16, n_pages = 0;
+    bool weights_ready = false, use_graphs = true;
+
+    __nv_bfloat16* emb = nullptr;
+    __nv_bfloat16* head = nullptr;
+    std::vector<dd::LayerW> layers;
+    float* gain_ones = nullptr;
+    CUtensorMap map_head;
+
+    float* x = nullptr;             // [256, d] fp32 residual stream
+    __nv_bfloat16* h = nullptr;     // [256, d] normed GEMM input
+    float* q = nullptr;             // [256, q_dim] fp32 roped queries
+    __nv_bfloat16* o = nullptr;     // [256, q_dim] attention output
+    __nv_bfloat16* a = nullptr;     // [256, ffn] SwiGLU output
+    float* ws = nullptr;            // split-K partials
+    float* logits = nullptr;        // [256, vocab]
+    CUtensorMap map_h, map_o, map_a;
+
+    __nv_bfloat16* kv_pool = nullptr;
+    int32_t* page_table = nullptr;
+    float* rope_cos = nullptr;
+    float* rope_sin = nullptr;
+
+    dd::PassState* d_ps = nullptr;
+    dd::PassState* h_ps = nullptr;  // pinned ring
+    int ps_slot = 0;
+
+    double* row_m = nullptr;
+    double* row_sum = nullptr;
+    int* row_argmax = nullptr;
+    unsigned* ticket = nullptr;
+    dd_verify_out* d_out = nullptr;
+    dd_verify_out* h_out = nullptr;
+    float* q_rows = nullptr;
+    float* h_q_stage = nullptr;
+    int q_rows_valid = 0;
+    int32_t* d_tail = nullptr;
+    double* d_probs = nullptr;
+    size_t probs_cap = 0;
+
+    int n_cached = 0;
+    int last_w = 0;  // width of the last scored pass with logits (0 = none)
+    std::map<int, dd::GemmPlan> plans;
+    std::map<int, cudaGraphExec_t> graphs;
+    std::string err;
+};
+
+int ctx_fail(dd_ctx* ctx, int code, const std::string& msg);
+int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits);

@@ -1,0 +1,75 @@
+// Target model description, synthetic-weight recipe and the device-side
+// kernels of one verification pass (see model.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/duodec_b200.h"
+
+namespace dd {
+
+// Tensor ids fed to derive_seed(weight_seed, id) for every generated matrix;
+// the CPU oracle (oracle/llama_ref.c) uses the same table.
+enum TensorKind { kWq = 0, kWk = 1, kWv = 2, kWo = 3, kWg = 4, kWu = 5, kWd = 6 };
+constexpr uint64_t kTensorEmb = 0;
+constexpr uint64_t kTensorHead = 1;
+__host__ __device__ inline uint64_t tensor_id(int layer, int kind) {
+    return 2 + static_cast<uint64_t>(layer) * 8 + static_cast<uint64_t>(kind);
+}
+
+struct ModelDims {
+    int n_layers, d, n_heads, n_kv_heads, head_dim, ffn, vocab;
+    float eps, rope_theta;
+    __host__ __device__ int q_dim() const { return n_heads * head_dim; }
+    __host__ __device__ int kv_dim() const { return n_kv_heads * head_dim; }
+    __host__ __device__ int qkv_rows() const { return q_dim() + 2 * kv_dim(); }
+};
+
+// Per-pass state shared by every kernel of a pass (device memory, updated by a
+// single small H2D copy before each pass so captured graphs stay valid).
+constexpr int kMaxPassTokens = 256;
+struct PassState {
+    int n_cached;  // tokens already in the KV cache (absolute position of row 0)
+    int w;         // tokens in this pass
+    int pad[2];
+    int32_t tokens[kMaxPassTokens];
+};
+
+// ---------------------------------------------------------------- kernels
+void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64_t seed,
+                        float amp, cudaStream_t s);
+void launch_init_head(__nv_bfloat16* head, const __nv_bfloat16* emb, const int32_t* plant_src,
+                      uint64_t vocab, uint64_t d, uint64_t seed, float amp, float plant_coef,
+                      cudaStream_t s);
+void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
+
+void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
+                       int d, float eps, float* x, __nv_bfloat16* h, cudaStream_t s);
+void launch_qkv_epilogue(const PassState* ps, int w, const float* ws, int splits,
+                         const ModelDims& m, const float* rope_cos, const float* rope_sin,
+                         float* q_out, __nv_bfloat16* kv_pool, const int32_t* page_table,
+                         int page_size, int layer, cudaStream_t s);
+void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
+                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                      int layer, __nv_bfloat16* o, cudaStream_t s);
+void attention_set_max_keys(int max_keys);
+void launch_residual_norm(int w, const float* ws, int splits, int d, const float* gain, float eps,
+                          float* x, __nv_bfloat16* h, cudaStream_t s);
+void launch_swiglu(int w, const float* ws, int splits, int ffn, __nv_bfloat16* a, cudaStream_t s);
+void launch_reduce_rows(int w, const float* ws, int splits, int n, float* out, cudaStream_t s);
+void launch_kv_compact(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                       const ModelDims& m, const int32_t* src_pos, const int32_t* dst_pos, int n,
+                       cudaStream_t s);
+
+// KV pool addressing: pool[page][layer][k|v][kv_head][page_size][head_dim]
+__host__ __device__ inline size_t kv_offset(const ModelDims& m, int page_size, int page,
+                                            int layer, int kv, int head, int slot) {
+    return ((((static_cast<size_t>(page) * m.n_layers + layer) * 2 + kv) * m.n_kv_heads + head) *
+                page_size +
+            slot) *
+           m.head_dim;
+}
+
+}  // namespace dd

@@ -1,0 +1,641 @@
+// Target-side context of the C ABI (include/duodec_b200.h): device weights,
+// paged bf16 KV cache, the scored verification pass (one CUDA graph per pass
+// width) and the acceptance kernel launch.
+//
+// A dd_ctx replaces the reference's ModelSpec on the target role
+// (proj/include/duodec/model.hpp:57-65) but is stateful: it owns the KV cache
+// and n_cached, so dd_score must be given exactly the tokens that are not yet
+// cached ([last committed token] ++ tail).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "accept.h"
+#include "common.cuh"
+#include "ctx.h"
+#include "gemm.h"
+#include "model.h"
+
+using namespace dd;
+
+thread_local std::string g_last_error;
+
+#define CK(expr)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (expr);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            return ctx_fail(ctx, DD_E_CUDA, std::string(#expr) + ": " +               \
+                                                cudaGetErrorString(e_));              \
+        }                                                                             \
+    } while (0)
+
+int ctx_fail(dd_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    g_last_error = msg;
+    return code;
+}
+
+namespace {
+
+enum GemmId { kGQkv = 0, kGO = 1, kGGu = 2, kGDown = 3, kGHead = 4, kNumGemm = 5 };
+
+int round_nt(int w) { return std::max(16, (w + 15) / 16 * 16); }
+
+void gemm_shape(const dd_ctx* c, int id, int* n_out, int* k) {
+    const ModelDims& m = c->m;
+    switch (id) {
+        case kGQkv: *n_out = m.qkv_rows(); *k = m.d; break;
+        case kGO: *n_out = m.d; *k = m.q_dim(); break;
+        case kGGu: *n_out = 2 * m.ffn; *k = m.d; break;
+        case kGDown: *n_out = m.d; *k = m.ffn; break;
+        default: *n_out = m.vocab; *k = m.d; break;
+    }
+}
+
+const GemmPlan& plan_for(dd_ctx* c, int id, int nt) {
+    auto key = id * 1000 + nt;
+    auto it = c->plans.find(key);
+    if (it != c->plans.end()) return it->second;
+    int n_out, k;
+    gemm_shape(c, id, &n_out, &k);
+    return c->plans[key] = plan_gemm(n_out, k, nt);
+}
+
+}  // namespace
+
+// Enqueue one scored pass of width w on ctx->stream (all state via d_ps).
+int enqueue_pass(dd_ctx* ctx, int w, bool want_logits) {
+    const ModelDims& m = ctx->m;
+    const int nt = round_nt(w);
+    cudaStream_t s = ctx->stream;
+    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx) -> cudaError_t {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        const GemmPlan& p = plan_for(ctx, id, nt);
+        return launch_gemm(mw, mx, n_out, k, w, nt, p, ctx->ws, s);
+    };
+    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, s);
+    for (int l = 0; l < m.n_layers; ++l) {
+        const LayerW& L = ctx->layers[l];
+        CK(gemm(kGQkv, &L.map_qkv, &ctx->map_h));
+        launch_qkv_epilogue(ctx->d_ps, w, ctx->ws, plan_for(ctx, kGQkv, nt).splits, m,
+                            ctx->rope_cos, ctx->rope_sin, ctx->q, ctx->kv_pool, ctx->page_table,
+                            ctx->page_size, l, s);
+        launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
+                         ctx->o, s);
+        CK(gemm(kGO, &L.map_o, &ctx->map_o));
+        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGO, nt).splits, m.d, ctx->gain_ones, m.eps,
+                             ctx->x, ctx->h, s);
+        CK(gemm(kGGu, &L.map_gu, &ctx->map_h));
+        launch_swiglu(w, ctx->ws, plan_for(ctx, kGGu, nt).splits, m.ffn, ctx->a, s);
+        CK(gemm(kGDown, &L.map_d, &ctx->map_a));
+        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGDown, nt).splits, m.d, ctx->gain_ones,
+                             m.eps, ctx->x, ctx->h, s);
+    }
+    if (want_logits) {
+        CK(gemm(kGHead, &ctx->map_head, &ctx->map_h));
+        launch_reduce_rows(w, ctx->ws, plan_for(ctx, kGHead, nt).splits, m.vocab, ctx->logits, s);
+    }
+    CK(cudaGetLastError());
+    return DD_OK;
+}
+
+// Upload pass state, then replay (or capture) the graph for width w.
+int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
+    if (w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_CAPACITY, "pass width out of range");
+    if (ctx->n_cached + w > ctx->max_seq)
+        return ctx_fail(ctx, DD_E_CAPACITY, "KV cache capacity exceeded");
+    for (int i = 0; i < w; ++i)
+        if (tokens[i] < 0 || tokens[i] >= ctx->m.vocab)
+            return ctx_fail(ctx, DD_E_ARG, "token outside vocabulary");
+    const int slot = ctx->ps_slot;
+    ctx->ps_slot = (slot + 1) % kPsRing;
+    CK(cudaEventSynchronize(ctx->ps_done[slot]));
+    PassState* hp = ctx->h_ps + slot;
+    hp->n_cached = ctx->n_cached;
+    hp->w = w;
+    std::memcpy(hp->tokens, tokens, sizeof(int32_t) * w);
+    CK(cudaMemcpyAsync(ctx->d_ps, hp, offsetof(PassState, tokens) + sizeof(int32_t) * w,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
+    if (ctx->use_graphs) {
+        const int key = w * 2 + (want_logits ? 1 : 0);
+        auto it = ctx->graphs.find(key);
+        if (it == ctx->graphs.end()) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            int rc = enqueue_pass(ctx, w, want_logits);
+            cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+            if (rc != DD_OK) return rc;
+            CK(e);
+            cudaGraphExec_t ge;
+            CK(cudaGraphInstantiate(&ge, g, 0));
+            cudaGraphDestroy(g);
+            it = ctx->graphs.emplace(key, ge).first;
+        }
+        CK(cudaGraphLaunch(it->second, ctx->stream));
+    } else {
+        int rc = enqueue_pass(ctx, w, want_logits);
+        if (rc != DD_OK) return rc;
+    }
+    ctx->n_cached += w;
+    ctx->last_w = want_logits ? w : 0;
+    return DD_OK;
+}
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* dd_last_error(const dd_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
+    dd_ctx* ctx = nullptr;
+    if (!desc || !out) return ctx_fail(nullptr, DD_E_ARG, "null argument");
+    *out = nullptr;
+    const dd_model_desc& d = *desc;
+    if (d.n_layers < 1 || d.d_model % 128 || d.head_dim % 32 || d.head_dim > 256 ||
+        d.n_heads % std::max(1, d.n_kv_heads) || d.ffn_dim % 128 || d.vocab % 128 ||
+        d.n_heads * d.head_dim % 64 || d.max_seq < 1)
+        return ctx_fail(nullptr, DD_E_ARG,
+                        "unsupported shape (d_model, ffn_dim, vocab must be multiples of 128; "
+                        "head_dim a multiple of 32 <= 256)");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cuda_device)
+        return ctx_fail(nullptr, DD_E_CUDA, "no CUDA device available (no CPU fallback exists)");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess || prop.major != 10)
+        return ctx_fail(nullptr, DD_E_CUDA, "device is not sm_100 (Blackwell)");
+    ctx = new dd_ctx();
+    ctx->device = cuda_device;
+    CK(cudaSetDevice(cuda_device));
+    ModelDims& m = ctx->m;
+    m.n_layers = d.n_layers;
+    m.d = d.d_model;
+    m.n_heads = d.n_heads;
+    m.n_kv_heads = d.n_kv_heads > 0 ? d.n_kv_heads : d.n_heads;
+    m.head_dim = d.head_dim;
+    m.ffn = d.ffn_dim;
+    m.vocab = d.vocab;
+    m.eps = d.rms_eps;
+    m.rope_theta = d.rope_theta;
+    ctx->page_size = d.page_size > 0 ? d.page_size : 16;
+    ctx->n_pages = (d.max_seq + ctx->page_size - 1) / ctx->page_size;
+    ctx->max_seq = ctx->n_pages * ctx->page_size;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->q_ready, cudaEventDisableTiming));
+    for (int i = 0; i < kPsRing; ++i) CK(cudaEventCreateWithFlags(&ctx->ps_done[i], cudaEventDisableTiming));
+
+    // weights
+    const size_t d_ = m.d;
+    CK(cudaMalloc(&ctx->emb, sizeof(__nv_bfloat16) * m.vocab * d_));
+    CK(cudaMalloc(&ctx->head, sizeof(__nv_bfloat16) * m.vocab * d_));
+    ctx->layers.resize(m.n_layers);
+    for (auto& L : ctx->layers) {
+        CK(cudaMalloc(&L.qkv, sizeof(__nv_bfloat16) * m.qkv_rows() * d_));
+        CK(cudaMalloc(&L.o, sizeof(__nv_bfloat16) * d_ * m.q_dim()));
+        CK(cudaMalloc(&L.gu, sizeof(__nv_bfloat16) * 2 * m.ffn * d_));
+        CK(cudaMalloc(&L.dn, sizeof(__nv_bfloat16) * d_ * m.ffn));
+        if (make_tmap_bf16(&L.map_qkv, L.qkv, m.qkv_rows(), d_, 128) ||
+            make_tmap_bf16(&L.map_o, L.o, d_, m.q_dim(), 128) ||
+            make_tmap_bf16(&L.map_gu, L.gu, 2 * m.ffn, d_, 128) ||
+            make_tmap_bf16(&L.map_d, L.dn, d_, m.ffn, 128))
+            return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    }
+    if (make_tmap_bf16(&ctx->map_head, ctx->head, m.vocab, d_, 128))
+        return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    const int gain_n = std::max(m.d, m.ffn);
+    CK(cudaMalloc(&ctx->gain_ones, sizeof(float) * gain_n));
+    launch_fill_f32(ctx->gain_ones, gain_n, 1.0f, ctx->stream);
+
+    // activations (kMaxPassTokens rows so every TMA box stays in bounds)
+    const size_t R = kMaxPassTokens;
+    CK(cudaMalloc(&ctx->x, sizeof(float) * R * d_));
+    CK(cudaMalloc(&ctx->h, sizeof(__nv_bfloat16) * R * d_));
+    CK(cudaMalloc(&ctx->q, sizeof(float) * R * m.q_dim()));
+    CK(cudaMalloc(&ctx->o, sizeof(__nv_bfloat16) * R * m.q_dim()));
+    CK(cudaMalloc(&ctx->a, sizeof(__nv_bfloat16) * R * m.ffn));
+    CK(cudaMemset(ctx->h, 0, sizeof(__nv_bfloat16) * R * d_));
+    CK(cudaMemset(ctx->o, 0, sizeof(__nv_bfloat16) * R * m.q_dim()));
+    CK(cudaMemset(ctx->a, 0, sizeof(__nv_bfloat16) * R * m.ffn));
+    if (make_tmap_bf16(&ctx->map_h, ctx->h, R, d_, 16) ||
+        make_tmap_bf16(&ctx->map_o, ctx->o, R, m.q_dim(), 16) ||
+        make_tmap_bf16(&ctx->map_a, ctx->a, R, m.ffn, 16))
+        return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    size_t ws_floats = 0;
+    for (int id = 0; id < kNumGemm; ++id) {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        for (int nt = 16; nt <= kMaxPassTokens; nt += 16) {
+            const GemmPlan& p = plan_for(ctx, id, nt);
+            ws_floats = std::max(ws_floats, static_cast<size_t>(p.splits) * nt * n_out);
+        }
+    }
+    CK(cudaMalloc(&ctx->ws, sizeof(float) * ws_floats));
+    CK(cudaMalloc(&ctx->logits, sizeof(float) * R * m.vocab));
+
+    // paged KV cache (all pages reserved up front; page table maps logical->physical)
+    const size_t kv_elems = static_cast<size_t>(ctx->n_pages) * m.n_layers * 2 * m.n_kv_heads *
+                            ctx->page_size * m.head_dim;
+    CK(cudaMalloc(&ctx->kv_pool, sizeof(__nv_bfloat16) * kv_elems));
+    std::vector<int32_t> pt(ctx->n_pages);
+    for (int i = 0; i < ctx->n_pages; ++i) pt[i] = i;
+    CK(cudaMalloc(&ctx->page_table, sizeof(int32_t) * ctx->n_pages));
+    CK(cudaMemcpy(ctx->page_table, pt.data(), sizeof(int32_t) * ctx->n_pages,
+                  cudaMemcpyHostToDevice));
+    attention_set_max_keys(ctx->max_seq);
+
+    // RoPE tables in double precision -> fp32 (shared with the oracle)
+    const int half = m.head_dim / 2;
+    std::vector<float> cs(static_cast<size_t>(ctx->max_seq) * half), sn(cs.size());
+    for (int p = 0; p < ctx->max_seq; ++p)
+        for (int i = 0; i < half; ++i) {
+            const double inv = std::pow(static_cast<double>(m.rope_theta),
+                                        -2.0 * i / static_cast<double>(m.head_dim));
+            const double ang = static_cast<double>(p) * inv;
+            cs[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(ang));
+            sn[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(ang));
+        }
+    CK(cudaMalloc(&ctx->rope_cos, sizeof(float) * cs.size()));
+    CK(cudaMalloc(&ctx->rope_sin, sizeof(float) * sn.size()));
+    CK(cudaMemcpy(ctx->rope_cos, cs.data(), sizeof(float) * cs.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->rope_sin, sn.data(), sizeof(float) * sn.size(), cudaMemcpyHostToDevice));
+
+    // pass state ring + acceptance scratch
+    CK(cudaMalloc(&ctx->d_ps, sizeof(PassState)));
+    CK(cudaHostAlloc(&ctx->h_ps, sizeof(PassState) * kPsRing, cudaHostAllocDefault));
+    CK(cudaMalloc(&ctx->row_m, sizeof(double) * (kMaxPassTokens + 1)));
+    CK(cudaMalloc(&ctx->row_sum, sizeof(double) * (kMaxPassTokens + 1)));
+    CK(cudaMalloc(&ctx->row_argmax, sizeof(int) * (kMaxPassTokens + 1)));
+    CK(cudaMalloc(&ctx->ticket, sizeof(unsigned)));
+    CK(cudaMemset(ctx->ticket, 0, sizeof(unsigned)));
+    CK(cudaMalloc(&ctx->d_out, sizeof(dd_verify_out)));
+    CK(cudaHostAlloc(&ctx->h_out, sizeof(dd_verify_out), cudaHostAllocDefault));
+    CK(cudaMalloc(&ctx->q_rows, sizeof(float) * kMaxPassTokens * m.vocab));
+    CK(cudaMalloc(&ctx->d_tail, sizeof(int32_t) * kMaxPassTokens));
+    CK(cudaHostAlloc(&ctx->h_q_stage, sizeof(float) * kMaxPassTokens * m.vocab,
+                     cudaHostAllocDefault));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->use_graphs = true;
+    *out = ctx;
+    return DD_OK;
+}
+
+void dd_ctx_destroy(dd_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& L : ctx->layers) {
+        cudaFree(L.qkv);
+        cudaFree(L.o);
+        cudaFree(L.gu);
+        cudaFree(L.dn);
+    }
+    void* dev[] = {ctx->emb, ctx->head, ctx->gain_ones, ctx->x, ctx->h, ctx->q, ctx->o, ctx->a,
+                   ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
+                   ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
+                   ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
+    if (ctx->h_out) cudaFreeHost(ctx->h_out);
+    if (ctx->h_q_stage) cudaFreeHost(ctx->h_q_stage);
+    for (int i = 0; i < kPsRing; ++i)
+        if (ctx->ps_done[i]) cudaEventDestroy(ctx->ps_done[i]);
+    if (ctx->q_ready) cudaEventDestroy(ctx->q_ready);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+}
+
+int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plant) {
+    if (!ctx) return ctx_fail(nullptr, DD_E_ARG, "null ctx");
+    CK(cudaSetDevice(ctx->device));
+    const ModelDims& m = ctx->m;
+    const float amp_proj = static_cast<float>(0.02 * std::sqrt(3.0));
+    const float amp_out = static_cast<float>(0.02 / std::sqrt(2.0 * m.n_layers) * std::sqrt(3.0));
+    PlantTable pt = make_plant_table(m.vocab, m.d, plant);
+    const float amp_emb = static_cast<float>(pt.emb_std * std::sqrt(3.0));
+    cudaStream_t s = ctx->stream;
+    const uint64_t d_ = m.d;
+    launch_init_matrix(ctx->emb, m.vocab, d_, derive_seed(weight_seed, kTensorEmb), amp_emb, s);
+    int32_t* d_src = nullptr;
+    if (pt.any) {
+        CK(cudaMalloc(&d_src, sizeof(int32_t) * m.vocab));
+        CK(cudaMemcpyAsync(d_src, pt.src.data(), sizeof(int32_t) * m.vocab, cudaMemcpyHostToDevice,
+                           s));
+    }
+    launch_init_head(ctx->head, ctx->emb, d_src, m.vocab, d_, derive_seed(weight_seed, kTensorHead),
+                     amp_proj, pt.coef, s);
+    for (int l = 0; l < m.n_layers; ++l) {
+        LayerW& L = ctx->layers[l];
+        const uint64_t qd = m.q_dim(), kvd = m.kv_dim();
+        launch_init_matrix(L.qkv, qd, d_, derive_seed(weight_seed, tensor_id(l, kWq)), amp_proj, s);
+        launch_init_matrix(L.qkv + qd * d_, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWk)),
+                           amp_proj, s);
+        launch_init_matrix(L.qkv + (qd + kvd) * d_, kvd, d_,
+                           derive_seed(weight_seed, tensor_id(l, kWv)), amp_proj, s);
+        launch_init_matrix(L.o, d_, qd, derive_seed(weight_seed, tensor_id(l, kWo)), amp_out, s);
+        launch_init_matrix(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWg)), amp_proj, s);
+        launch_init_matrix(L.gu + static_cast<uint64_t>(m.ffn) * d_, m.ffn, d_,
+                           derive_seed(weight_seed, tensor_id(l, kWu)), amp_proj, s);
+        launch_init_matrix(L.dn, d_, m.ffn, derive_seed(weight_seed, tensor_id(l, kWd)), amp_out, s);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    if (d_src) cudaFree(d_src);
+    ctx->weights_ready = true;
+    return DD_OK;
+}
+
+int dd_prefill(dd_ctx* ctx, const int32_t* tokens, int n) {
+    if (!ctx || (!tokens && n > 0) || n < 0) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (!ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
+    CK(cudaSetDevice(ctx->device));
+    for (int i = 0; i < n; i += kMaxPassTokens) {
+        const int w = std::min(kMaxPassTokens, n - i);
+        int rc = run_pass(ctx, tokens + i, w, false);
+        if (rc != DD_OK) return rc;
+    }
+    return DD_OK;
+}
+
+int dd_score(dd_ctx* ctx, const int32_t* tokens, int w) {
+    if (!ctx || !tokens) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (!ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
+    CK(cudaSetDevice(ctx->device));
+    return run_pass(ctx, tokens, w, true);
+}
+
+int dd_kv_len(const dd_ctx* ctx, int* n) {
+    if (!ctx || !n) return DD_E_ARG;
+    *n = ctx->n_cached;
+    return DD_OK;
+}
+
+int dd_kv_truncate(dd_ctx* ctx, int n_valid) {
+    if (!ctx) return ctx_fail(nullptr, DD_E_ARG, "null ctx");
+    if (n_valid < 0 || n_valid > ctx->n_cached)
+        return ctx_fail(ctx, DD_E_ARG, "truncate length outside [0, n_cached]");
+    ctx->n_cached = n_valid;  // pages stay reserved; slots past n_valid are dead
+    return DD_OK;
+}
+
+int dd_kv_compact(dd_ctx* ctx, const int32_t* src_pos, const int32_t* dst_pos, int n) {
+    if (!ctx || n < 0 || (n > 0 && (!src_pos || !dst_pos)))
+        return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    for (int i = 0; i < n; ++i)
+        if (src_pos[i] < 0 || src_pos[i] >= ctx->n_cached || dst_pos[i] < 0 ||
+            dst_pos[i] >= ctx->n_cached)
+            return ctx_fail(ctx, DD_E_ARG, "compaction slot outside the cache");
+    CK(cudaSetDevice(ctx->device));
+    launch_kv_compact(ctx->kv_pool, ctx->page_table, ctx->page_size, ctx->m, src_pos, dst_pos, n,
+                      ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DD_OK;
+}
+
+int dd_read_logits(dd_ctx* ctx, float* host, int row0, int rows) {
+    if (!ctx || !host) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (ctx->last_w == 0) return ctx_fail(ctx, DD_E_STATE, "no scored pass");
+    if (row0 < 0 || rows < 0 || row0 + rows > ctx->last_w)
+        return ctx_fail(ctx, DD_E_ARG, "rows outside the last pass");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(host, ctx->logits + static_cast<size_t>(row0) * ctx->m.vocab,
+                       sizeof(float) * rows * ctx->m.vocab, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DD_OK;
+}
+
+int dd_upload_q(dd_ctx* ctx, const float* q_rows, int rows, int vocab) {
+    if (!ctx || (!q_rows && rows > 0)) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (vocab != ctx->m.vocab || rows < 0 || rows > kMaxPassTokens)
+        return ctx_fail(ctx, DD_E_ARG, "q rows shape mismatch");
+    CK(cudaSetDevice(ctx->device));
+    const size_t bytes = sizeof(float) * static_cast<size_t>(rows) * vocab;
+    CK(cudaStreamSynchronize(ctx->copy_stream));  // staging buffer reuse
+    std::memcpy(ctx->h_q_stage, q_rows, bytes);
+    CK(cudaMemcpyAsync(ctx->q_rows, ctx->h_q_stage, bytes, cudaMemcpyHostToDevice,
+                       ctx->copy_stream));
+    CK(cudaEventRecord(ctx->q_ready, ctx->copy_stream));
+    ctx->q_rows_valid = rows;
+    return DD_OK;
+}
+
+static int verify_common(dd_ctx* ctx, AcceptParams& p, const dd_verify_args* args,
+                         dd_verify_out* out) {
+    p.mode = args->mode;
+    p.s = args->n_firsts;
+    p.greedy = args->greedy;
+    p.q_onehot = args->q_onehot;
+    p.inv_temp = args->greedy ? 1.0 : 1.0 / args->temperature;
+    p.seed = args->seed;
+    p.counter = args->counter;
+    for (int i = 0; i < 16; ++i) p.firsts[i] = i < args->n_firsts ? args->firsts[i] : -1;
+    p.q = ctx->q_rows;
+    p.row_m = ctx->row_m;
+    p.row_sum = ctx->row_sum;
+    p.row_argmax = ctx->row_argmax;
+    p.ticket = ctx->ticket;
+    p.out = ctx->d_out;
+    if (!p.q_onehot && p.mode != DD_MODE_VANILLA && p.L > 0) {
+        if (ctx->q_rows_valid < p.L) return ctx_fail(ctx, DD_E_STATE, "q rows not uploaded");
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->q_ready, 0));
+    }
+    CK(launch_accept(p, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(dd_verify_out), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    *out = *ctx->h_out;
+    return DD_OK;
+}
+
+static int check_verify_args(dd_ctx* ctx, const dd_verify_args* args) {
+    if (args->mode < DD_MODE_DUO || args->mode > DD_MODE_VANILLA)
+        return ctx_fail(ctx, DD_E_ARG, "unknown verify mode");
+    if (args->n_firsts < 0 || args->n_firsts > 16)
+        return ctx_fail(ctx, DD_E_ARG, "bundle size must be in [0, 16]");
+    if (!args->greedy && !(args->temperature > 0.0))
+        return ctx_fail(ctx, DD_E_ARG, "temperature must be positive");
+    if (args->tail_len < 0 || (args->mode == DD_MODE_VANILLA && args->tail_len != 0))
+        return ctx_fail(ctx, DD_E_ARG, "bad tail length");
+    for (int i = 0; i < args->n_firsts; ++i)
+        if (args->firsts[i] < 0 || args->firsts[i] >= ctx->m.vocab)
+            return ctx_fail(ctx, DD_E_ARG, "bundle token outside vocabulary");
+    return DD_OK;
+}
+
+int dd_verify(dd_ctx* ctx, const dd_verify_args* args, dd_verify_out* out) {
+    if (!ctx || !args || !out) return ctx_fail(ctx, DD_E_ARG, "null argument");
+    int rc = check_verify_args(ctx, args);
+    if (rc) return rc;
+    if (ctx->last_w == 0) return ctx_fail(ctx, DD_E_STATE, "no scored pass to verify");
+    const int L = args->tail_len;
+    if (L + 1 > ctx->last_w) return ctx_fail(ctx, DD_E_ARG, "tail longer than the scored pass");
+    CK(cudaSetDevice(ctx->device));
+    AcceptParams p{};
+    p.V = ctx->m.vocab;
+    p.L = L;
+    p.row0 = ctx->last_w - 1 - L;
+    p.logits = ctx->logits;
+    p.probs = nullptr;
+    p.tail = ctx->d_ps->tokens + (ctx->last_w - L);
+    return verify_common(ctx, p, args, out);
+}
+
+int dd_verify_probs(dd_ctx* ctx, const double* p_rows, const int32_t* tail_tokens, int vocab,
+                    const dd_verify_args* args, dd_verify_out* out) {
+    if (!ctx || !args || !out || !p_rows) return ctx_fail(ctx, DD_E_ARG, "null argument");
+    int rc = check_verify_args(ctx, args);
+    if (rc) return rc;
+    const int L = args->tail_len;
+    if (L > kMaxPassTokens - 1 || vocab < 1) return ctx_fail(ctx, DD_E_ARG, "bad shape");
+    CK(cudaSetDevice(ctx->device));
+    const size_t need = static_cast<size_t>(L + 1) * vocab;
+    if (need > ctx->probs_cap) {
+        if (ctx->d_probs) cudaFree(ctx->d_probs);
+        CK(cudaMalloc(&ctx->d_probs, sizeof(double) * need));
+        ctx->probs_cap = need;
+    }
+    CK(cudaMemcpyAsync(ctx->d_probs, p_rows, sizeof(double) * need, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    if (L > 0)
+        CK(cudaMemcpyAsync(ctx->d_tail, tail_tokens, sizeof(int32_t) * L, cudaMemcpyHostToDevice,
+                           ctx->stream));
+    AcceptParams p{};
+    p.V = vocab;
+    p.L = L;
+    p.row0 = 0;
+    p.logits = nullptr;
+    p.probs = ctx->d_probs;
+    p.tail = ctx->d_tail;
+    return verify_common(ctx, p, args, out);
+}
+
+int dd_time_pass(dd_ctx* ctx, int w, int trials, float* median_ms) {
+    if (!ctx || !median_ms || trials < 1) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    std::vector<int32_t> toks(w, 0);
+    const int n0 = ctx->n_cached;
+    std::vector<float> ms;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    for (int t = 0; t < trials; ++t) {
+        CK(cudaEventRecord(a, ctx->stream));
+        int rc = run_pass(ctx, toks.data(), w, true);
+        if (rc) return rc;
+        CK(cudaEventRecord(b, ctx->stream));
+        CK(cudaEventSynchronize(b));
+        float x = 0;
+        CK(cudaEventElapsedTime(&x, a, b));
+        ms.push_back(x);
+        ctx->n_cached = n0;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    ctx->last_w = 0;
+    std::sort(ms.begin(), ms.end());
+    const size_t n = ms.size();
+    *median_ms = n % 2 ? ms[n / 2] : 0.5f * (ms[n / 2 - 1] + ms[n / 2]);
+    return DD_OK;
+}
+
+int dd_profile_pass(dd_ctx* ctx, int w, float* ms4) {
+    if (!ctx || !ms4 || w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    const ModelDims& m = ctx->m;
+    const int n0 = ctx->n_cached;
+    std::vector<int32_t> toks(w, 0);
+    // upload pass state via a zero-cost pass setup
+    const int slot = ctx->ps_slot;
+    ctx->ps_slot = (slot + 1) % kPsRing;
+    CK(cudaEventSynchronize(ctx->ps_done[slot]));
+    PassState* hp = ctx->h_ps + slot;
+    hp->n_cached = n0;
+    hp->w = w;
+    std::memcpy(hp->tokens, toks.data(), sizeof(int32_t) * w);
+    CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
+    const int nt = round_nt(w);
+    cudaStream_t s = ctx->stream;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;
+    auto mark = [&](int c) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.push_back(e);
+        cls.push_back(c);
+    };
+    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx) {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        launch_gemm(mw, mx, n_out, k, w, nt, plan_for(ctx, id, nt), ctx->ws, s);
+    };
+    mark(-1);
+    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, s);
+    mark(2);
+    for (int l = 0; l < m.n_layers; ++l) {
+        const LayerW& L = ctx->layers[l];
+        gemm(kGQkv, &L.map_qkv, &ctx->map_h);
+        mark(0);
+        launch_qkv_epilogue(ctx->d_ps, w, ctx->ws, plan_for(ctx, kGQkv, nt).splits, m,
+                            ctx->rope_cos, ctx->rope_sin, ctx->q, ctx->kv_pool, ctx->page_table,
+                            ctx->page_size, l, s);
+        mark(2);
+        launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
+                         ctx->o, s);
+        mark(1);
+        gemm(kGO, &L.map_o, &ctx->map_o);
+        mark(0);
+        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGO, nt).splits, m.d, ctx->gain_ones, m.eps,
+                             ctx->x, ctx->h, s);
+        mark(2);
+        gemm(kGGu, &L.map_gu, &ctx->map_h);
+        mark(0);
+        launch_swiglu(w, ctx->ws, plan_for(ctx, kGGu, nt).splits, m.ffn, ctx->a, s);
+        mark(2);
+        gemm(kGDown, &L.map_d, &ctx->map_a);
+        mark(0);
+        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGDown, nt).splits, m.d, ctx->gain_ones,
+                             m.eps, ctx->x, ctx->h, s);
+        mark(2);
+    }
+    gemm(kGHead, &ctx->map_head, &ctx->map_h);
+    mark(0);
+    launch_reduce_rows(w, ctx->ws, plan_for(ctx, kGHead, nt).splits, m.vocab, ctx->logits, s);
+    mark(2);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) ms4[i] = 0.0f;
+    for (size_t i = 1; i < ev.size(); ++i) {
+        float x = 0;
+        cudaEventElapsedTime(&x, ev[i - 1], ev[i]);
+        ms4[cls[i]] += x;
+        ms4[3] += x;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ctx->n_cached = n0;
+    ctx->last_w = 0;
+    return DD_OK;
+}
+
+uint64_t dd_pass_weight_bytes(const dd_ctx* ctx) {
+    if (!ctx) return 0;
+    const ModelDims& m = ctx->m;
+    const uint64_t per_layer = static_cast<uint64_t>(m.qkv_rows()) * m.d +
+                               static_cast<uint64_t>(m.d) * m.q_dim() +
+                               2ull * m.ffn * m.d + static_cast<uint64_t>(m.d) * m.ffn;
+    return 2ull * (per_layer * m.n_layers + static_cast<uint64_t>(m.vocab) * m.d);
+}
+
+}  // extern "C"
