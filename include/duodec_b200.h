@@ -155,6 +155,15 @@ int dd_profile_pass(dd_ctx* ctx, int w, float* ms4);
  * embedding), for the roofline. */
 uint64_t dd_pass_weight_bytes(const dd_ctx* ctx);
 
+/* ------------------------------------------------------------ test seams */
+/* Raw bf16 bits of a generated weight tensor (which: 0 embedding, 1 LM head,
+ * 2 fused qkv, 3 o-proj, 4 fused gate/up, 5 down) for bit-exact checks
+ * against the oracle generator. n = element count expected. */
+int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n);
+/* Standalone run of the skinny tcgen05 GEMM: Y[w][n_out] = X[w][k] . W[n_out][k]^T
+ * (bf16 bits in, fp32 out; n_out % 128 == 0, k % 64 == 0, w <= 256). */
+int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, float* Y);
+
 /* ------------------------------------------------------------ CPU draft */
 int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_plant_desc* plant,
                     int n_threads, const int* cpus, int n_cpus, dd_draft** out);

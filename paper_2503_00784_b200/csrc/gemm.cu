@@ -174,7 +174,10 @@ GemmPlan plan_gemm(int n_out, int k, int nt) {
         ctas_per_sm = 1;
     }
     stages = std::min(stages, 8);
-    const int slots = kNumSMs * ctas_per_sm;
+    // The split count depends only on the GEMM shape (never on nt), so a token's
+    // fp32 reduction order is identical whatever the pass width: greedy outputs
+    // do not depend on how tokens are batched into passes.
+    const int slots = kNumSMs * 2;
     // choose split-K maximising wave efficiency, keeping >= 6 k-blocks per CTA
     int best_s = 1;
     double best_eff = -1.0;
@@ -192,6 +195,7 @@ GemmPlan plan_gemm(int n_out, int k, int nt) {
             best_s = real_s;
         }
     }
+    (void)ctas_per_sm;
     p.kb_per_split = (nkb + best_s - 1) / best_s;
     p.splits = (nkb + p.kb_per_split - 1) / p.kb_per_split;
     p.stages = stages;

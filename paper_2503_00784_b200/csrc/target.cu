@@ -417,7 +417,8 @@ int dd_read_logits(dd_ctx* ctx, float* host, int row0, int rows) {
 
 int dd_upload_q(dd_ctx* ctx, const float* q_rows, int rows, int vocab) {
     if (!ctx || (!q_rows && rows > 0)) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
-    if (vocab != ctx->m.vocab || rows < 0 || rows > kMaxPassTokens)
+    // vocab may be below the model's for dd_verify_probs (Markov-table rows)
+    if (vocab < 1 || vocab > ctx->m.vocab || rows < 0 || rows > kMaxPassTokens)
         return ctx_fail(ctx, DD_E_ARG, "q rows shape mismatch");
     CK(cudaSetDevice(ctx->device));
     const size_t bytes = sizeof(float) * static_cast<size_t>(rows) * vocab;
@@ -636,6 +637,63 @@ uint64_t dd_pass_weight_bytes(const dd_ctx* ctx) {
                                static_cast<uint64_t>(m.d) * m.q_dim() +
                                2ull * m.ffn * m.d + static_cast<uint64_t>(m.d) * m.ffn;
     return 2ull * (per_layer * m.n_layers + static_cast<uint64_t>(m.vocab) * m.d);
+}
+
+int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n) {
+    if (!ctx || !host) return ctx_fail(ctx, DD_E_ARG, "null argument");
+    const ModelDims& m = ctx->m;
+    if (which >= 2 && (layer < 0 || layer >= m.n_layers))
+        return ctx_fail(ctx, DD_E_ARG, "layer out of range");
+    const void* src = nullptr;
+    size_t count = 0;
+    const size_t d_ = m.d;
+    switch (which) {
+        case 0: src = ctx->emb; count = static_cast<size_t>(m.vocab) * d_; break;
+        case 1: src = ctx->head; count = static_cast<size_t>(m.vocab) * d_; break;
+        case 2: src = ctx->layers[layer].qkv; count = static_cast<size_t>(m.qkv_rows()) * d_; break;
+        case 3: src = ctx->layers[layer].o; count = d_ * m.q_dim(); break;
+        case 4: src = ctx->layers[layer].gu; count = 2 * static_cast<size_t>(m.ffn) * d_; break;
+        case 5: src = ctx->layers[layer].dn; count = d_ * m.ffn; break;
+        default: return ctx_fail(ctx, DD_E_ARG, "unknown tensor");
+    }
+    if (n != count) return ctx_fail(ctx, DD_E_ARG, "element count mismatch");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpy(host, src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
+    return DD_OK;
+}
+
+int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, float* Y) {
+    dd_ctx* ctx = nullptr;
+    if (!W || !X || !Y || n_out % 128 || k % 64 || w < 1 || w > kMaxPassTokens)
+        return ctx_fail(nullptr, DD_E_ARG, "bad gemm shape");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+        return ctx_fail(nullptr, DD_E_CUDA, "no CUDA device available");
+    const int nt = round_nt(w);
+    void *dW = nullptr, *dX = nullptr;
+    float* dws = nullptr;
+    float* dY = nullptr;
+    CK(cudaMalloc(&dW, sizeof(uint16_t) * n_out * static_cast<size_t>(k)));
+    CK(cudaMalloc(&dX, sizeof(uint16_t) * kMaxPassTokens * static_cast<size_t>(k)));
+    CK(cudaMemset(dX, 0, sizeof(uint16_t) * kMaxPassTokens * static_cast<size_t>(k)));
+    CK(cudaMemcpy(dW, W, sizeof(uint16_t) * n_out * static_cast<size_t>(k), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dX, X, sizeof(uint16_t) * w * static_cast<size_t>(k), cudaMemcpyHostToDevice));
+    CUtensorMap mw, mx;
+    if (make_tmap_bf16(&mw, dW, n_out, k, 128) || make_tmap_bf16(&mx, dX, kMaxPassTokens, k, 16))
+        return ctx_fail(nullptr, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmPlan p = plan_gemm(n_out, k, nt);
+    CK(cudaMalloc(&dws, sizeof(float) * p.splits * static_cast<size_t>(w) * n_out));
+    CK(cudaMalloc(&dY, sizeof(float) * static_cast<size_t>(w) * n_out));
+    CK(launch_gemm(&mw, &mx, n_out, k, w, nt, p, dws, 0));
+    launch_reduce_rows(w, dws, p.splits, n_out, dY, 0);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(Y, dY, sizeof(float) * static_cast<size_t>(w) * n_out, cudaMemcpyDeviceToHost));
+    cudaFree(dW);
+    cudaFree(dX);
+    cudaFree(dws);
+    cudaFree(dY);
+    return DD_OK;
 }
 
 }  // extern "C"
