@@ -49,6 +49,7 @@ struct dd_ctx {
     __nv_bfloat16* o = nullptr;     // [256, q_dim] attention output
     __nv_bfloat16* a = nullptr;     // [256, ffn] SwiGLU output
     float* ws = nullptr;            // split-K partials
+    int* counters = nullptr;        // per-tile split arrival counters
     float* logits = nullptr;        // [256, vocab]
     CUtensorMap map_h, map_o, map_a;
 

@@ -1,0 +1,471 @@
+// CPU draft model: Llama-family forward on pinned host cores (AVX-512 BF16).
+//
+// This is the draft side of DuoDecoding (north star: "the draft model runs on
+// host CPU cores in a concurrent thread").  The reference's draft is a
+// ModelSpec table (proj/src/model.cpp:286-320) queried by draft_dynamic
+// (proj/src/drafting.cpp:71-136); here it is a Llama-68M-shape transformer
+// with the same synthetic-weight generator as the GPU target and the oracle
+// (oracle/llama_ref.c), so its logits are checked against the oracle too.
+// The KV cache follows the draft context: logits(ctx) keeps the longest
+// cached prefix of ctx and runs only the new tokens (branch forks of
+// draft_dynamic re-run one token).
+#include "draft.h"
+
+#include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "plant.h"
+
+namespace dd {
+
+namespace {
+
+inline uint64_t mix(uint64_t seed, uint64_t m) {
+    uint64_t z = seed + m * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+inline uint64_t derive(uint64_t base, uint64_t index) {
+    uint64_t z = base + (index + 1) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 30)) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+inline float unit(uint64_t seed, uint64_t e) {
+    return static_cast<float>(static_cast<int32_t>(mix(seed, e + 1) >> 40)) * 0x1.0p-23f - 1.0f;
+}
+inline uint16_t f2bf(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+inline float bf2f(uint16_t b) {
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+uint64_t tensor_id(int layer, int kind) { return 2 + static_cast<uint64_t>(layer) * 8 + kind; }
+
+void gen(SpinPool& pool, std::vector<uint16_t>& dst, uint64_t offset, uint64_t n, uint64_t seed,
+         float amp) {
+    pool.run([&](int tid, int nt) {
+        const uint64_t lo = n * tid / nt, hi = n * (tid + 1) / nt;
+        for (uint64_t e = lo; e < hi; ++e) dst[offset + e] = f2bf(unit(seed, e) * amp);
+    });
+}
+
+__attribute__((target("avx512f,avx512bw,avx512bf16"))) inline float dot_bf16(const uint16_t* w,
+                                                                            const uint16_t* x,
+                                                                            int k) {
+    __m512 acc0 = _mm512_setzero_ps(), acc1 = _mm512_setzero_ps();
+    int i = 0;
+    for (; i + 64 <= k; i += 64) {
+        acc0 = _mm512_dpbf16_ps(acc0, (__m512bh)_mm512_loadu_si512(w + i),
+                                (__m512bh)_mm512_loadu_si512(x + i));
+        acc1 = _mm512_dpbf16_ps(acc1, (__m512bh)_mm512_loadu_si512(w + i + 32),
+                                (__m512bh)_mm512_loadu_si512(x + i + 32));
+    }
+    for (; i + 32 <= k; i += 32)
+        acc0 = _mm512_dpbf16_ps(acc0, (__m512bh)_mm512_loadu_si512(w + i),
+                                (__m512bh)_mm512_loadu_si512(x + i));
+    float s = _mm512_reduce_add_ps(_mm512_add_ps(acc0, acc1));
+    for (; i < k; ++i) s += bf2f(w[i]) * bf2f(x[i]);
+    return s;
+}
+
+// Y[t][n] = W[n,:] . X[t,:] for rows n split across the pool
+void matmul(SpinPool& pool, const uint16_t* W, int rows, int k, const uint16_t* X, int w,
+            float* Y) {
+    pool.run([&](int tid, int nt) {
+        const int lo = static_cast<int>(static_cast<int64_t>(rows) * tid / nt);
+        const int hi = static_cast<int>(static_cast<int64_t>(rows) * (tid + 1) / nt);
+        for (int n = lo; n < hi; ++n) {
+            const uint16_t* wr = W + static_cast<size_t>(n) * k;
+            for (int t = 0; t < w; ++t)
+                Y[static_cast<size_t>(t) * rows + n] = dot_bf16(wr, X + static_cast<size_t>(t) * k, k);
+        }
+    });
+}
+
+void rmsnorm_bf(const float* x, int d, float eps, uint16_t* h) {
+    float ss = 0.0f;
+    for (int i = 0; i < d; ++i) ss = std::fmaf(x[i], x[i], ss);
+    const float r = 1.0f / std::sqrt(ss / static_cast<float>(d) + eps);
+    for (int i = 0; i < d; ++i) h[i] = f2bf(x[i] * r);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ pool
+SpinPool::SpinPool(int n_threads, const std::vector<int>& cpus) : n_(std::max(1, n_threads)) {
+    // workers 1..n-1 are pinned to cpus[1..]; the calling thread (tid 0, the
+    // engine's draft worker) pins itself to cpus[0]
+    for (int i = 1; i < n_; ++i) {
+        th_.emplace_back([this, i] { worker(i); });
+        if (!cpus.empty()) {
+            cpu_set_t set;
+            CPU_ZERO(&set);
+            CPU_SET(cpus[static_cast<size_t>(i) % cpus.size()], &set);
+            pthread_setaffinity_np(th_.back().native_handle(), sizeof(set), &set);
+        }
+    }
+}
+
+SpinPool::~SpinPool() {
+    stop_.store(true, std::memory_order_release);
+    gen_.fetch_add(1, std::memory_order_acq_rel);
+    for (auto& t : th_) t.join();
+}
+
+void SpinPool::worker(int tid) {
+    uint64_t seen = 0;
+    for (;;) {
+        int spins = 0;
+        while (gen_.load(std::memory_order_acquire) == seen) {
+            if (++spins < 20000) {
+                _mm_pause();
+            } else {
+                std::this_thread::yield();
+            }
+        }
+        seen = gen_.load(std::memory_order_acquire);
+        if (stop_.load(std::memory_order_acquire)) return;
+        (*job_)(tid, n_);
+        done_.fetch_add(1, std::memory_order_acq_rel);
+    }
+}
+
+void SpinPool::run(const std::function<void(int, int)>& fn) {
+    if (n_ == 1) {
+        fn(0, 1);
+        return;
+    }
+    job_ = &fn;
+    done_.store(0, std::memory_order_relaxed);
+    gen_.fetch_add(1, std::memory_order_acq_rel);
+    fn(0, n_);
+    while (done_.load(std::memory_order_acquire) != n_ - 1) _mm_pause();
+}
+
+// ------------------------------------------------------------------ model
+CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_desc* plant,
+                   int n_threads, const std::vector<int>& cpus)
+    : L_(d.n_layers), d_(d.d_model), H_(d.n_heads), Hkv_(d.n_kv_heads > 0 ? d.n_kv_heads : d.n_heads),
+      hd_(d.head_dim), F_(d.ffn_dim), V_(d.vocab), max_seq_(d.max_seq), eps_(d.rms_eps) {
+    pool_ = std::make_unique<SpinPool>(n_threads, cpus);
+    const int qd = H_ * hd_, kvd = Hkv_ * hd_;
+    const float amp_proj = static_cast<float>(0.02 * std::sqrt(3.0));
+    const float amp_out = static_cast<float>(0.02 / std::sqrt(2.0 * L_) * std::sqrt(3.0));
+    PlantTable pt = make_plant_table(V_, d_, plant);
+    const float amp_emb = static_cast<float>(pt.emb_std * std::sqrt(3.0));
+    const uint64_t D = static_cast<uint64_t>(d_);
+    emb_.resize(static_cast<size_t>(V_) * D);
+    head_.resize(static_cast<size_t>(V_) * D);
+    gen(*pool_, emb_, 0, V_ * D, derive(weight_seed, 0), amp_emb);
+    {
+        const uint64_t hs = derive(weight_seed, 1);
+        const uint64_t n = V_ * D;
+        pool_->run([&](int tid, int nt) {
+            const uint64_t lo = n * tid / nt, hi = n * (tid + 1) / nt;
+            for (uint64_t e = lo; e < hi; ++e) {
+                float w = unit(hs, e) * amp_proj;
+                const int32_t t = pt.any ? pt.src[e / D] : -1;
+                if (t >= 0) w = std::fmaf(pt.coef, bf2f(emb_[static_cast<size_t>(t) * D + e % D]), w);
+                head_[e] = f2bf(w);
+            }
+        });
+    }
+    layers_.resize(L_);
+    for (int l = 0; l < L_; ++l) {
+        DraftLayer& Ly = layers_[l];
+        Ly.qkv.resize(static_cast<size_t>(qd + 2 * kvd) * D);
+        Ly.o.resize(D * qd);
+        Ly.gu.resize(2 * static_cast<size_t>(F_) * D);
+        Ly.dn.resize(D * F_);
+        gen(*pool_, Ly.qkv, 0, qd * D, derive(weight_seed, tensor_id(l, 0)), amp_proj);
+        gen(*pool_, Ly.qkv, qd * D, kvd * D, derive(weight_seed, tensor_id(l, 1)), amp_proj);
+        gen(*pool_, Ly.qkv, (qd + kvd) * D, kvd * D, derive(weight_seed, tensor_id(l, 2)), amp_proj);
+        gen(*pool_, Ly.o, 0, D * qd, derive(weight_seed, tensor_id(l, 3)), amp_out);
+        gen(*pool_, Ly.gu, 0, F_ * D, derive(weight_seed, tensor_id(l, 4)), amp_proj);
+        gen(*pool_, Ly.gu, F_ * D, F_ * D, derive(weight_seed, tensor_id(l, 5)), amp_proj);
+        gen(*pool_, Ly.dn, 0, D * F_, derive(weight_seed, tensor_id(l, 6)), amp_out);
+    }
+    kv_.assign(static_cast<size_t>(L_) * 2 * Hkv_ * max_seq_ * hd_, 0);
+    const int half = hd_ / 2;
+    rope_cos_.resize(static_cast<size_t>(max_seq_) * half);
+    rope_sin_.resize(rope_cos_.size());
+    for (int p = 0; p < max_seq_; ++p)
+        for (int i = 0; i < half; ++i) {
+            const double inv = std::pow(static_cast<double>(d.rope_theta), -2.0 * i / hd_);
+            rope_cos_[static_cast<size_t>(p) * half + i] = static_cast<float>(std::cos(p * inv));
+            rope_sin_[static_cast<size_t>(p) * half + i] = static_cast<float>(std::sin(p * inv));
+        }
+    logits_tmp_.resize(V_);
+}
+
+bool CpuLlama::logits(const int32_t* ctx, int n, float* out) {
+    if (n < 1 || n > max_seq_) {
+        err = "draft context length out of range";
+        return false;
+    }
+    for (int i = 0; i < n; ++i)
+        if (ctx[i] < 0 || ctx[i] >= V_) {
+            err = "draft token outside vocabulary";
+            return false;
+        }
+    // keep the longest cached prefix, always re-running at least the last token
+    int keep = 0;
+    const int lim = std::min<int>(static_cast<int>(tokens_.size()), n - 1);
+    while (keep < lim && tokens_[keep] == ctx[keep]) ++keep;
+    tokens_.resize(keep);
+    int pos = keep;
+    while (pos < n) {
+        const int w = std::min(256, n - pos);
+        forward(ctx + pos, w, out);
+        pos += w;
+    }
+    return true;
+}
+
+void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
+    const int n0 = static_cast<int>(tokens_.size());
+    const int qd = H_ * hd_, kvd = Hkv_ * hd_, rows = qd + 2 * kvd, half = hd_ / 2;
+    const size_t W = static_cast<size_t>(w);
+    x_.resize(W * d_);
+    hb_.resize(W * d_);
+    qkv_.resize(W * rows);
+    q_.resize(W * qd);
+    ob_.resize(W * qd);
+    gu_.resize(W * 2 * F_);
+    ab_.resize(W * F_);
+    y_.resize(W * std::max(d_, 2 * F_));
+    for (int t = 0; t < w; ++t) {
+        for (int i = 0; i < d_; ++i)
+            x_[t * d_ + i] = bf2f(emb_[static_cast<size_t>(toks[t]) * d_ + i]);
+        rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+    }
+    auto kvp = [&](int l, int kv, int h, int pos) {
+        return &kv_[((((static_cast<size_t>(l) * 2 + kv) * Hkv_ + h) * max_seq_) + pos) * hd_];
+    };
+    const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd_)));
+    for (int l = 0; l < L_; ++l) {
+        const DraftLayer& Ly = layers_[l];
+        matmul(*pool_, Ly.qkv.data(), rows, d_, hb_.data(), w, qkv_.data());
+        for (int t = 0; t < w; ++t) {
+            const int pos = n0 + t;
+            const float* cs = &rope_cos_[static_cast<size_t>(pos) * half];
+            const float* sn = &rope_sin_[static_cast<size_t>(pos) * half];
+            const float* r = &qkv_[t * rows];
+            for (int head = 0; head < H_ + Hkv_; ++head)
+                for (int i = 0; i < half; ++i) {
+                    const float av = r[head * hd_ + i], bv = r[head * hd_ + i + half];
+                    const float lo = std::fmaf(av, cs[i], -(bv * sn[i]));
+                    const float hi = std::fmaf(bv, cs[i], av * sn[i]);
+                    if (head < H_) {
+                        q_[t * qd + head * hd_ + i] = lo;
+                        q_[t * qd + head * hd_ + i + half] = hi;
+                    } else {
+                        uint16_t* kd = kvp(l, 0, head - H_, pos);
+                        kd[i] = f2bf(lo);
+                        kd[i + half] = f2bf(hi);
+                    }
+                }
+            for (int e = 0; e < kvd; ++e) kvp(l, 1, e / hd_, pos)[e % hd_] = f2bf(r[qd + kvd + e]);
+        }
+        pool_->run([&](int tid, int nt) {
+            std::vector<float> sc;
+            for (int job = tid; job < H_ * w; job += nt) {
+                const int head = job / w, t = job % w;
+                const int pos = n0 + t, nk = pos + 1, kvh = head / (H_ / Hkv_);
+                const float* qv = &q_[t * qd + head * hd_];
+                sc.resize(nk);
+                float mx = -INFINITY;
+                for (int j = 0; j < nk; ++j) {
+                    const uint16_t* kr = kvp(l, 0, kvh, j);
+                    float acc = 0.0f;
+                    for (int i = 0; i < hd_; ++i) acc = std::fmaf(qv[i], bf2f(kr[i]), acc);
+                    sc[j] = acc * scale;
+                    mx = std::max(mx, sc[j]);
+                }
+                float sum = 0.0f;
+                for (int j = 0; j < nk; ++j) {
+                    sc[j] = std::exp(sc[j] - mx);
+                    sum += sc[j];
+                }
+                const float inv = 1.0f / sum;
+                float acc[256];
+                for (int i = 0; i < hd_; ++i) acc[i] = 0.0f;
+                for (int j = 0; j < nk; ++j) {
+                    const uint16_t* vr = kvp(l, 1, kvh, j);
+                    for (int i = 0; i < hd_; ++i) acc[i] = std::fmaf(sc[j], bf2f(vr[i]), acc[i]);
+                }
+                for (int i = 0; i < hd_; ++i) ob_[t * qd + head * hd_ + i] = f2bf(acc[i] * inv);
+            }
+        });
+        matmul(*pool_, Ly.o.data(), d_, qd, ob_.data(), w, y_.data());
+        for (int t = 0; t < w; ++t) {
+            for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
+            rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+        }
+        matmul(*pool_, Ly.gu.data(), 2 * F_, d_, hb_.data(), w, gu_.data());
+        for (int t = 0; t < w; ++t)
+            for (int f = 0; f < F_; ++f) {
+                const float g = gu_[t * 2 * F_ + f], u = gu_[t * 2 * F_ + F_ + f];
+                ab_[t * F_ + f] = f2bf(g / (1.0f + std::exp(-g)) * u);
+            }
+        matmul(*pool_, Ly.dn.data(), d_, F_, ab_.data(), w, y_.data());
+        for (int t = 0; t < w; ++t) {
+            for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
+            rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+        }
+    }
+    matmul(*pool_, head_.data(), V_, d_, &hb_[(W - 1) * d_], 1, logits_last);
+    tokens_.insert(tokens_.end(), toks, toks + w);
+}
+
+int CpuLlama::distribution(const float* lg, double temperature, bool greedy, float* q) {
+    // argmax, lowest index on ties (kernels_scalar.cpp:40-48)
+    const int nt = pool_->size();
+    std::vector<float> bestv(nt, -INFINITY);
+    std::vector<int> besti(nt, 0);
+    std::vector<double> sums(nt, 0.0);
+    pool_->run([&](int tid, int n) {
+        const int lo = static_cast<int>(static_cast<int64_t>(V_) * tid / n);
+        const int hi = static_cast<int>(static_cast<int64_t>(V_) * (tid + 1) / n);
+        float bv = -INFINITY;
+        int bi = lo;
+        for (int i = lo; i < hi; ++i)
+            if (lg[i] > bv) {
+                bv = lg[i];
+                bi = i;
+            }
+        bestv[tid] = bv;
+        besti[tid] = bi;
+    });
+    float bv = bestv[0];
+    int bi = besti[0];
+    for (int t = 1; t < nt; ++t)
+        if (bestv[t] > bv) {
+            bv = bestv[t];
+            bi = besti[t];
+        }
+    if (greedy) {
+        std::memset(q, 0, sizeof(float) * V_);
+        q[bi] = 1.0f;
+        return bi;
+    }
+    const double inv_t = 1.0 / temperature;
+    const double m = static_cast<double>(bv) * inv_t;
+    pool_->run([&](int tid, int n) {
+        const int lo = static_cast<int>(static_cast<int64_t>(V_) * tid / n);
+        const int hi = static_cast<int>(static_cast<int64_t>(V_) * (tid + 1) / n);
+        double s = 0.0;
+        for (int i = lo; i < hi; ++i) s += std::exp(static_cast<double>(lg[i]) * inv_t - m);
+        sums[tid] = s;
+    });
+    double tot = 0.0;
+    for (double s : sums) tot += s;
+    const double inv = 1.0 / tot;
+    pool_->run([&](int tid, int n) {
+        const int lo = static_cast<int>(static_cast<int64_t>(V_) * tid / n);
+        const int hi = static_cast<int>(static_cast<int64_t>(V_) * (tid + 1) / n);
+        for (int i = lo; i < hi; ++i)
+            q[i] = static_cast<float>(std::exp(static_cast<double>(lg[i]) * inv_t - m) * inv);
+    });
+    return bi;
+}
+
+void CpuLlama::top_k(const float* q, int k, int32_t* out) {
+    // partial selection keeping "descending probability, then ascending id"
+    // (ranked_tokens, proj/src/distribution.cpp:80-87) without a full sort
+    const int nt = pool_->size();
+    std::vector<std::vector<int32_t>> part(nt);
+    auto better = [&](int32_t a, int32_t b) { return q[a] > q[b] || (q[a] == q[b] && a < b); };
+    pool_->run([&](int tid, int n) {
+        const int lo = static_cast<int>(static_cast<int64_t>(V_) * tid / n);
+        const int hi = static_cast<int>(static_cast<int64_t>(V_) * (tid + 1) / n);
+        std::vector<int32_t>& p = part[tid];
+        p.clear();
+        for (int i = lo; i < hi; ++i) {
+            if (static_cast<int>(p.size()) < k) {
+                p.push_back(i);
+                std::push_heap(p.begin(), p.end(), better);  // heap top = worst kept
+            } else if (better(i, p.front())) {
+                std::pop_heap(p.begin(), p.end(), better);
+                p.back() = i;
+                std::push_heap(p.begin(), p.end(), better);
+            }
+        }
+    });
+    std::vector<int32_t> all;
+    for (auto& p : part) all.insert(all.end(), p.begin(), p.end());
+    std::sort(all.begin(), all.end(), better);
+    for (int i = 0; i < k; ++i) out[i] = all[i];
+}
+
+}  // namespace dd
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_plant_desc* plant,
+                    int n_threads, const int* cpus, int n_cpus, dd_draft** out) {
+    if (!desc || !out) return DD_E_ARG;
+    *out = nullptr;
+    if (!__builtin_cpu_supports("avx512bf16")) return DD_E_ARG;  // single native path
+    const dd_model_desc& d = *desc;
+    if (d.n_layers < 1 || d.d_model % 32 || d.ffn_dim % 32 || d.head_dim > 256 || d.max_seq < 2 ||
+        d.n_heads % std::max(1, d.n_kv_heads))
+        return DD_E_ARG;
+    std::vector<int> cl;
+    for (int i = 0; i < n_cpus; ++i) cl.push_back(cpus[i]);
+    int nt = n_threads;
+    if (nt <= 0) nt = !cl.empty() ? static_cast<int>(cl.size())
+                                  : std::max(1, static_cast<int>(std::thread::hardware_concurrency()) - 2);
+    auto* dr = new dd_draft();
+    dr->cpus = cl;
+    dr->model = std::make_unique<dd::CpuLlama>(d, weight_seed, plant, nt, cl);
+    *out = dr;
+    return DD_OK;
+}
+
+void dd_draft_destroy(dd_draft* d) { delete d; }
+
+int dd_draft_logits(dd_draft* d, const int32_t* ctx_tokens, int n, float* logits) {
+    if (!d || !ctx_tokens || !logits) return DD_E_ARG;
+    return d->model->logits(ctx_tokens, n, logits) ? DD_OK : DD_E_ARG;
+}
+
+int dd_draft_time_token(dd_draft* d, int trials, float* median_ms) {
+    if (!d || !median_ms || trials < 1) return DD_E_ARG;
+    // calibrate()'s denominator: one single-token forward (engine.cpp:559-561),
+    // measured as the incremental cost of one token on a 8-token context
+    std::vector<int32_t> ctx(9, 0);
+    std::vector<float> lg(d->model->vocab());
+    std::vector<double> ms;
+    for (int i = 0; i < 5 + trials; ++i) {
+        ctx.back() = i % 7 + 1;
+        d->model->logits(ctx.data(), 8, lg.data());  // cache holds 8 tokens
+        const auto t0 = std::chrono::steady_clock::now();
+        d->model->logits(ctx.data(), 9, lg.data());  // exactly one new token
+        const double x =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (i >= 5) ms.push_back(x);
+    }
+    std::sort(ms.begin(), ms.end());
+    const size_t n = ms.size();
+    *median_ms = static_cast<float>(n % 2 ? ms[n / 2] : 0.5 * (ms[n / 2 - 1] + ms[n / 2]));
+    return DD_OK;
+}
+
+}  // extern "C"

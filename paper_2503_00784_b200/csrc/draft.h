@@ -1,0 +1,78 @@
+// CPU draft model (Llama-family, bf16 weights) for the host draft worker.
+#pragma once
+
+#include <stdint.h>
+
+#include <atomic>
+#include <functional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/duodec_b200.h"
+
+namespace dd {
+
+// Fixed-size pool of pinned spinning workers; run(fn) calls fn(tid, nthreads)
+// on every thread (the caller is tid 0) and returns when all are done.
+class SpinPool {
+  public:
+    SpinPool(int n_threads, const std::vector<int>& cpus);
+    ~SpinPool();
+    int size() const { return n_; }
+    void run(const std::function<void(int, int)>& fn);
+
+  private:
+    void worker(int tid);
+    int n_;
+    std::vector<std::thread> th_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> done_{0};
+    std::atomic<bool> stop_{false};
+    const std::function<void(int, int)>* job_ = nullptr;
+};
+
+struct DraftLayer {
+    std::vector<uint16_t> qkv, o, gu, dn;  // bf16 bits, row-major [out][in]
+};
+
+// Llama forward on host cores with a KV cache that follows the draft
+// context: logits(ctx) reuses the longest cached prefix of ctx.
+class CpuLlama {
+  public:
+    CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_desc* plant,
+             int n_threads, const std::vector<int>& cpus);
+    int vocab() const { return V_; }
+    // next-token logits after ctx (fp32, V); returns false on bad input
+    bool logits(const int32_t* ctx, int n, float* out);
+    // q = softmax(logits / T) rounded to fp32 (greedy: one-hot at the argmax);
+    // also returns the argmax (lowest id on ties)
+    int distribution(const float* logits, double temperature, bool greedy, float* q);
+    // indices of the k largest q (descending, ties ascending id)
+    void top_k(const float* q, int k, int32_t* out);
+    SpinPool& pool() { return *pool_; }
+    int cached() const { return static_cast<int>(tokens_.size()); }
+    std::string err;
+
+  private:
+    void forward(const int32_t* toks, int w, float* logits_last);
+    int L_, d_, H_, Hkv_, hd_, F_, V_, max_seq_;
+    float eps_;
+    std::vector<uint16_t> emb_, head_;
+    std::vector<DraftLayer> layers_;
+    std::vector<uint16_t> kv_;  // [L][2][Hkv][max_seq][hd] bf16
+    std::vector<float> rope_cos_, rope_sin_;
+    std::vector<int32_t> tokens_;  // tokens whose K/V are cached
+    std::unique_ptr<SpinPool> pool_;
+    // scratch
+    std::vector<float> x_, qkv_, q_, o_, gu_, a_, y_, logits_tmp_;
+    std::vector<uint16_t> hb_, ob_, ab_;
+};
+
+}  // namespace dd
+
+struct dd_draft {
+    std::unique_ptr<dd::CpuLlama> model;
+    std::vector<int> cpus;
+    std::string err;
+};

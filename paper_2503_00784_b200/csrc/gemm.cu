@@ -13,10 +13,13 @@
 // - One elected thread issues tcgen05.mma (M=128, N=NT, K=16) into a TMEM
 //   accumulator; tcgen05.commit releases each smem stage back to the TMA
 //   producer through an mbarrier ring.
-// - Split-K across blockIdx.y so that tiles x splits fills the 148 SMs; the
-//   fp32 partials go to a workspace ws[split][token][row] and the consumer's
-//   fused epilogue kernel reduces them in a fixed order (deterministic, and a
-//   token's result does not depend on how many other tokens share the pass).
+// - Split-K across blockIdx.y so that tiles x splits fills the 148 SMs.  The
+//   S split CTAs of one tile form a thread-block cluster (1 x S): each stages
+//   its fp32 accumulator in its own shared memory, and after a cluster barrier
+//   CTA rank r reduces the tokens t = r (mod S) by reading all S partials over
+//   DSMEM in rank order (deterministic, and a token's result does not depend
+//   on the pass width).  The fused epilogue (RoPE + paged-KV append, residual
+//   add, SwiGLU, logits store) is applied right there — no global workspace.
 #include "common.cuh"
 #include "gemm.h"
 
@@ -31,6 +34,7 @@ constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;
 constexpr uint32_t kABytes = kBlockM * kBlockK * 2;  // 16 KiB
 constexpr int kTmemCols = 256;
+constexpr int kMaxSplits = 16;  // cluster size (non-portable above 8)
 
 __global__ void __launch_bounds__(128, 1)
     gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
@@ -109,21 +113,94 @@ __global__ void __launch_bounds__(128, 1)
         umma_commit(done);
     }
 
-    // ---- epilogue: TMEM -> registers -> fp32 partials (all 4 warps) ----
+    // ---- epilogue: cluster (DSMEM) split-K reduction + fused epilogue ----
     __syncwarp();
     mbar_wait(done, 0);
     __syncwarp();
     tc_fence_after();
-    const int row = m0 + warp * 32 + lane;
-    float* out = a.ws + static_cast<size_t>(split) * a.w * a.n_out;
+    const int tid = threadIdx.x;
+    const uint32_t S = static_cast<uint32_t>(a.splits);
+    const uint32_t rank = S > 1 ? cluster_ctarank() : 0u;
+    float* red = reinterpret_cast<float*>(smem);  // [kChunk][128] staging, reuses the ring
+    const uint32_t red_addr = smem_u32(red);
+    constexpr int kChunk = 64;
     const uint32_t t_lane = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    for (int c0 = 0; c0 < a.nt; c0 += 16) {
-        float v[16];
-        tmem_ld16(t_lane + c0, v);
+    const GemmEpiParams& e = a.epi;
+    // sum over the cluster's partials of element (t, r) of the current chunk
+    auto csum = [&](int t, int r) -> float {
+        if (S == 1) return red[t * 128 + r];
+        const uint32_t off = static_cast<uint32_t>((t * 128 + r) * 4);
+        // issue all remote loads first (independent), then add in rank order
+        float v[kMaxSplits];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            if (c0 + j < a.w) out[static_cast<size_t>(c0 + j) * a.n_out + row] = v[j];
+        for (uint32_t s2 = 0; s2 < kMaxSplits; ++s2)
+            if (s2 < S) v[s2] = ld_dsmem_f32(dsmem_addr(red_addr + off, s2));
+        float acc = 0.0f;
+#pragma unroll
+        for (uint32_t s2 = 0; s2 < kMaxSplits; ++s2)
+            if (s2 < S) acc = __fadd_rn(acc, v[s2]);
+        return acc;
+    };
+    for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+        const int tn = min(kChunk, a.w - t0);
+        for (int c0 = 0; c0 < tn; c0 += 16) {
+            float v[16];
+            tmem_ld16(t_lane + t0 + c0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (c0 + j < tn) red[(c0 + j) * 128 + warp * 32 + lane] = v[j];
         }
+        if (S > 1) cluster_sync(); else __syncthreads();
+        for (int t = static_cast<int>(rank); t < tn; t += static_cast<int>(S)) {
+            const int tg = t0 + t;  // token index in the pass
+            if (e.kind == kEpiStore) {
+                e.out[static_cast<size_t>(tg) * a.n_out + m0 + tid] = csum(t, tid);
+            } else if (e.kind == kEpiResidual) {
+                float* x = e.out + static_cast<size_t>(tg) * a.n_out + m0 + tid;
+                *x = __fadd_rn(*x, csum(t, tid));
+            } else if (e.kind == kEpiSwiGLU) {
+                if (tid < 64) {
+                    const float g = csum(t, tid), u = csum(t, 64 + tid);
+                    const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+                    e.out_bf[static_cast<size_t>(tg) * (a.n_out / 2) + blockIdx.x * 64 + tid] =
+                        __float2bfloat16_rn(__fmul_rn(silu, u));
+                }
+            } else {  // kEpiQkvRope
+                const ModelDims& md = e.m;
+                const int hd = md.head_dim, half = hd / 2;
+                const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+                const int pos = e.ps->n_cached + tg;
+                const int page = e.page_table[pos / e.page_size], slot = pos % e.page_size;
+                if (m0 < q_dim + kv_dim) {
+                    if (tid < 64) {
+                        const int hl = tid / half, i = tid % half;
+                        const int r0 = hl * hd + i;
+                        const float av = csum(t, r0), bv = csum(t, r0 + half);
+                        const float c = e.rope_cos[static_cast<size_t>(pos) * half + i];
+                        const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
+                        const float lo = __fmaf_rn(av, c, -__fmul_rn(bv, sn));
+                        const float hi = __fmaf_rn(bv, c, __fmul_rn(av, sn));
+                        const int grow = m0 + r0;
+                        if (grow < q_dim) {
+                            float* qd = e.q_out + static_cast<size_t>(tg) * q_dim + grow;
+                            qd[0] = lo;
+                            qd[half] = hi;
+                        } else {
+                            const int kh = (grow - q_dim) / hd;
+                            __nv_bfloat16* kd =
+                                e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 0, kh, slot) + i;
+                            kd[0] = __float2bfloat16_rn(lo);
+                            kd[half] = __float2bfloat16_rn(hi);
+                        }
+                    }
+                } else {
+                    const int ve = m0 + tid - q_dim - kv_dim;
+                    e.kv_pool[kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) +
+                              ve % hd] = __float2bfloat16_rn(csum(t, tid));
+                }
+            }
+        }
+        if (S > 1) cluster_sync(); else __syncthreads();
     }
     tc_fence_before();
     __syncthreads();
@@ -181,7 +258,7 @@ GemmPlan plan_gemm(int n_out, int k, int nt) {
     // choose split-K maximising wave efficiency, keeping >= 6 k-blocks per CTA
     int best_s = 1;
     double best_eff = -1.0;
-    for (int s = 1; s <= 32; ++s) {
+    for (int s = 1; s <= kMaxSplits; ++s) {
         const int kbps = (nkb + s - 1) / s;
         if (kbps < 6 && s > 1) break;
         const int real_s = (nkb + kbps - 1) / kbps;
@@ -205,11 +282,13 @@ GemmPlan plan_gemm(int n_out, int k, int nt) {
 }
 
 cudaError_t launch_gemm(const CUtensorMap* map_w, const CUtensorMap* map_x, int n_out, int k,
-                        int w, int nt, const GemmPlan& plan, float* ws, cudaStream_t stream) {
+                        int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
+                        cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
+                             220 * 1024);
+        cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
     GemmArgs a;
@@ -221,9 +300,20 @@ cudaError_t launch_gemm(const CUtensorMap* map_w, const CUtensorMap* map_x, int 
     a.splits = plan.splits;
     a.stages = plan.stages;
     a.ws = ws;
-    dim3 grid(plan.tiles, plan.splits);
-    gemm_skinny_kernel<<<grid, 128, plan.smem_bytes, stream>>>(*map_w, *map_x, a);
-    return cudaGetLastError();
+    a.epi = epi;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(plan.tiles, plan.splits, 1);
+    cfg.blockDim = dim3(128, 1, 1);
+    cfg.dynamicSmemBytes = plan.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = plan.splits;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_skinny_kernel, *map_w, *map_x, a);
 }
 
 }  // namespace dd

@@ -25,6 +25,25 @@ void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64
     init_matrix_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows * cols, seed, amp);
 }
 
+// Logical row r of a [rows, cols] tensor stored at physical row
+// (r / 64) * 128 + offset + r % 64: the gate/up interleave that lets one
+// 128-row GEMM tile hold matching gate and up features (SwiGLU epilogue).
+__global__ void init_matrix_il_kernel(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
+                                      uint64_t seed, float amp, int offset) {
+    const uint64_t n = rows * cols;
+    for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = e / cols, c = e % cols;
+        const uint64_t pr = (r / 64) * 128 + offset + r % 64;
+        dst[pr * cols + c] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
+    }
+}
+
+void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
+                                    uint64_t seed, float amp, int offset, cudaStream_t s) {
+    init_matrix_il_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, offset);
+}
+
 // LM head: random rows plus, for planted tokens t, row pi(t) += coef * E[t].
 // plant_src[v] = t (or -1) with pi(t) = v.
 __global__ void init_head_kernel(__nv_bfloat16* head, const __nv_bfloat16* emb,
@@ -100,117 +119,67 @@ void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, con
     embed_norm_kernel<<<w, 256, 0, s>>>(ps, emb, gain, d, eps, x, h);
 }
 
-// ------------------------------------------------------------ QKV epilogue
-// Reduce split-K partials of the fused QKV projection, apply RoPE (HF
-// rotate_half convention) to q and k at absolute position n_cached + t, keep
-// q in fp32, append bf16 k and v to the paged cache.
-__global__ void qkv_epilogue_kernel(const PassState* ps, const float* ws, int splits,
-                                    ModelDims m, const float* rope_cos, const float* rope_sin,
-                                    float* q_out, __nv_bfloat16* kv_pool,
-                                    const int32_t* page_table, int page_size, int layer) {
-    const int t = blockIdx.x;
-    const int w = ps->w;
-    const int pos = ps->n_cached + t;
-    const int hd = m.head_dim, half = hd / 2;
-    const int rows = m.qkv_rows();
-    const int n_q = m.q_dim(), n_kv = m.kv_dim();
-    const size_t split_stride = static_cast<size_t>(w) * rows;
-    const float* base = ws + static_cast<size_t>(t) * rows;
-    const float* cs = rope_cos + static_cast<size_t>(pos) * half;
-    const float* sn = rope_sin + static_cast<size_t>(pos) * half;
-    const int page = page_table[pos / page_size], slot = pos % page_size;
-
-    // rotary pairs over q heads and k heads
-    const int n_pairs = (m.n_heads + m.n_kv_heads) * half;
-    for (int p = threadIdx.x; p < n_pairs; p += blockDim.x) {
-        const int head = p / half, i = p % half;
-        const int r0 = head * hd + i;  // q heads first, then k heads (contiguous in qkv rows)
-        float a = 0.0f, b = 0.0f;
-        for (int s = 0; s < splits; ++s) {
-            a = __fadd_rn(a, base[s * split_stride + r0]);
-            b = __fadd_rn(b, base[s * split_stride + r0 + half]);
-        }
-        const float c = cs[i], sv = sn[i];
-        const float lo = __fmaf_rn(a, c, -__fmul_rn(b, sv));
-        const float hi = __fmaf_rn(b, c, __fmul_rn(a, sv));
-        if (head < m.n_heads) {
-            float* qd = q_out + static_cast<size_t>(t) * n_q + head * hd;
-            qd[i] = lo;
-            qd[i + half] = hi;
-        } else {
-            const int kh = head - m.n_heads;
-            __nv_bfloat16* kd = kv_pool + kv_offset(m, page_size, page, layer, 0, kh, slot);
-            kd[i] = __float2bfloat16_rn(lo);
-            kd[i + half] = __float2bfloat16_rn(hi);
-        }
-    }
-    for (int e = threadIdx.x; e < n_kv; e += blockDim.x) {
-        const int r = n_q + n_kv + e;
-        float v = 0.0f;
-        for (int s = 0; s < splits; ++s) v = __fadd_rn(v, base[s * split_stride + r]);
-        const int vh = e / hd, i = e % hd;
-        kv_pool[kv_offset(m, page_size, page, layer, 1, vh, slot) + i] = __float2bfloat16_rn(v);
-    }
-}
-
-void launch_qkv_epilogue(const PassState* ps, int w, const float* ws, int splits,
-                         const ModelDims& m, const float* rope_cos, const float* rope_sin,
-                         float* q_out, __nv_bfloat16* kv_pool, const int32_t* page_table,
-                         int page_size, int layer, cudaStream_t s) {
-    qkv_epilogue_kernel<<<w, 256, 0, s>>>(ps, ws, splits, m, rope_cos, rope_sin, q_out, kv_pool,
-                                          page_table, page_size, layer);
-}
-
 // ------------------------------------------------------------ attention
-// One CTA per (query head, new token). The query at absolute position
+// One CTA per (query head, new token): the query at absolute position
 // pos = n_cached + t attends to keys 0..pos (cached prefix + the chain of new
-// tokens up to itself).  Work per CTA depends only on (head, pos), so a
-// token's output is independent of the pass width.
+// tokens up to itself).  Scores: one thread per key (16-byte K loads, q
+// broadcast from shared memory); PV: warp w takes keys w, w+4, ..., each lane
+// owns head_dim/32 output dims, then a fixed-order cross-warp sum.  The work
+// of a CTA depends only on (head, pos), so a token's output is independent of
+// the pass width.
 constexpr int kAttnThreads = 128;
+constexpr int kAttnWarps = kAttnThreads / 32;
 __global__ void __launch_bounds__(kAttnThreads)
     attention_kernel(const PassState* ps, ModelDims m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                      int layer, float scale, __nv_bfloat16* o) {
-    extern __shared__ float scores[];  // [n_keys]
-    __shared__ float red[kAttnThreads / 32];
+    extern __shared__ float scores[];  // [max_keys]
+    __shared__ float qs[256];
+    __shared__ float red[kAttnWarps];
+    __shared__ float part[kAttnThreads / 8][64];  // [KG][hd] with KG * hd = 16 * 128
     const int head = blockIdx.x, t = blockIdx.y;
     const int pos = ps->n_cached + t;
     const int n_keys = pos + 1;
     const int hd = m.head_dim;
     const int kvh = head / (m.n_heads / m.n_kv_heads);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const float* qv = q + static_cast<size_t>(t) * m.q_dim() + head * hd;
-
-    // scores: one warp per key, lanes split head_dim (hd <= 256, multiple of 32)
-    const int per_lane = hd / 32;
-    float qr[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) qr[j] = j < per_lane ? qv[lane * per_lane + j] : 0.0f;
-    for (int key = warp; key < n_keys; key += kAttnThreads / 32) {
-        const int page = page_table[key / page_size], slot = key % page_size;
-        const __nv_bfloat16* kr = kv_pool + kv_offset(m, page_size, page, layer, 0, kvh, slot);
-        float acc = 0.0f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (j < per_lane) acc = __fmaf_rn(qr[j], __bfloat162float(kr[lane * per_lane + j]), acc);
-        acc = warp_sum(acc);
-        if (lane == 0) scores[key] = __fmul_rn(acc, scale);
-    }
+    for (int i = threadIdx.x; i < hd; i += kAttnThreads)
+        qs[i] = q[static_cast<size_t>(t) * m.q_dim() + head * hd + i];
     __syncthreads();
-    // softmax (fp32)
+
+    // scores
     float mx = -INFINITY;
-    for (int k = threadIdx.x; k < n_keys; k += kAttnThreads) mx = fmaxf(mx, scores[k]);
+    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
+        const int page = page_table[key / page_size], slot = key % page_size;
+        const uint4* kr = reinterpret_cast<const uint4*>(
+            kv_pool + kv_offset(m, page_size, page, layer, 0, kvh, slot));
+        float acc = 0.0f;
+#pragma unroll 4
+        for (int c = 0; c < hd / 8; ++c) {
+            const uint4 v = __ldg(kr + c);
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(b2[j]);
+                acc = __fmaf_rn(qs[c * 8 + 2 * j], f.x, acc);
+                acc = __fmaf_rn(qs[c * 8 + 2 * j + 1], f.y, acc);
+            }
+        }
+        const float sc = __fmul_rn(acc, scale);
+        scores[key] = sc;
+        mx = fmaxf(mx, sc);
+    }
     mx = warp_max(mx);
     if (lane == 0) red[warp] = mx;
     __syncthreads();
     mx = red[0];
 #pragma unroll
-    for (int i = 1; i < kAttnThreads / 32; ++i) mx = fmaxf(mx, red[i]);
+    for (int i = 1; i < kAttnWarps; ++i) mx = fmaxf(mx, red[i]);
     __syncthreads();
     float sum = 0.0f;
-    for (int k = threadIdx.x; k < n_keys; k += kAttnThreads) {
-        const float e = expf(scores[k] - mx);
-        scores[k] = e;
+    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
+        const float e = expf(scores[key] - mx);
+        scores[key] = e;
         sum += e;
     }
     sum = warp_sum(sum);
@@ -218,19 +187,63 @@ __global__ void __launch_bounds__(kAttnThreads)
     __syncthreads();
     sum = 0.0f;
 #pragma unroll
-    for (int i = 0; i < kAttnThreads / 32; ++i) sum += red[i];
+    for (int i = 0; i < kAttnWarps; ++i) sum += red[i];
     const float inv = 1.0f / sum;
-    // o[d] = sum_k p_k v_k[d]; thread per dim (hd <= 128 here; loop otherwise)
-    for (int d0 = threadIdx.x; d0 < hd; d0 += kAttnThreads) {
-        float acc = 0.0f;
-        for (int k = 0; k < n_keys; ++k) {
-            const int page = page_table[k / page_size], slot = k % page_size;
-            const __nv_bfloat16* vr =
-                kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot);
-            acc = __fmaf_rn(scores[k], __bfloat162float(vr[d0]), acc);
+
+    // PV: thread = (key group kg = tid / G, dim group dg = tid % G), G = hd / 8,
+    // 8 dims (one 16-byte load) per thread, keys kg, kg + 128/G, ...; then a
+    // fixed-order sum over key groups.
+    const int G = hd / 8;
+    const int KG = kAttnThreads / G;
+    const int kg = threadIdx.x / G, dg = threadIdx.x % G;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    int key = kg;
+    for (; key + 3 * KG < n_keys; key += 4 * KG) {
+        uint4 v[4];
+        float p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int kk = key + u * KG;
+            const int page = page_table[kk / page_size], slot = kk % page_size;
+            v[u] = __ldg(reinterpret_cast<const uint4*>(
+                       kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
+            p[u] = scores[kk];
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(b2[j]);
+                acc[2 * j] = __fmaf_rn(p[u], f.x, acc[2 * j]);
+                acc[2 * j + 1] = __fmaf_rn(p[u], f.y, acc[2 * j + 1]);
+            }
+        }
+    }
+    for (; key < n_keys; key += KG) {
+        const int page = page_table[key / page_size], slot = key % page_size;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(
+                            kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
+        const float p = scores[key];
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(b2[j]);
+            acc[2 * j] = __fmaf_rn(p, f.x, acc[2 * j]);
+            acc[2 * j + 1] = __fmaf_rn(p, f.y, acc[2 * j + 1]);
+        }
+    }
+    float* pv = &part[0][0];  // [KG][hd]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pv[kg * hd + dg * 8 + j] = acc[j];
+    __syncthreads();
+    for (int d0 = threadIdx.x; d0 < hd; d0 += kAttnThreads) {
+        float s2 = 0.0f;
+        for (int g2 = 0; g2 < KG; ++g2) s2 = __fadd_rn(s2, pv[g2 * hd + d0]);
         o[static_cast<size_t>(t) * m.q_dim() + head * hd + d0] =
-            __float2bfloat16_rn(__fmul_rn(acc, inv));
+            __float2bfloat16_rn(__fmul_rn(s2, inv));
     }
 }
 
@@ -238,9 +251,8 @@ static int g_attn_smem_bytes = 48 * 1024;
 
 void attention_set_max_keys(int max_keys) {
     g_attn_smem_bytes = max_keys * static_cast<int>(sizeof(float));
-    if (g_attn_smem_bytes > 48 * 1024)
-        cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             g_attn_smem_bytes);
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         g_attn_smem_bytes);
 }
 
 void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
@@ -252,64 +264,18 @@ void launch_attention(const PassState* ps, int w, const ModelDims& m, const floa
                                                                    page_size, layer, scale, o);
 }
 
-// ------------------------------------------------------------ residual + norm
-__global__ void residual_norm_kernel(const float* ws, int splits, int w, int d,
-                                     const float* gain, float eps, float* x, __nv_bfloat16* h) {
+// ------------------------------------------------------------ RMSNorm
+// h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g); one CTA per token row.
+__global__ void rmsnorm_kernel(const float* x, int d, const float* gain, float eps,
+                               __nv_bfloat16* h) {
     __shared__ float red[8];
     const int t = blockIdx.x;
-    float* xr = x + static_cast<size_t>(t) * d;
-    const size_t split_stride = static_cast<size_t>(w) * d;
-    for (int i = threadIdx.x; i < d; i += 256) {
-        float acc = 0.0f;
-        for (int s = 0; s < splits; ++s)
-            acc = __fadd_rn(acc, ws[s * split_stride + static_cast<size_t>(t) * d + i]);
-        xr[i] = __fadd_rn(xr[i], acc);
-    }
-    __syncthreads();
-    rmsnorm_row(xr, gain, d, eps, h + static_cast<size_t>(t) * d, red);
+    rmsnorm_row(x + static_cast<size_t>(t) * d, gain, d, eps, h + static_cast<size_t>(t) * d, red);
 }
 
-void launch_residual_norm(int w, const float* ws, int splits, int d, const float* gain, float eps,
-                          float* x, __nv_bfloat16* h, cudaStream_t s) {
-    residual_norm_kernel<<<w, 256, 0, s>>>(ws, splits, w, d, gain, eps, x, h);
-}
-
-// ------------------------------------------------------------ SwiGLU
-__global__ void swiglu_kernel(const float* ws, int splits, int w, int ffn, __nv_bfloat16* a) {
-    const int t = blockIdx.y;
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= ffn) return;
-    const size_t row = static_cast<size_t>(t) * 2 * ffn;
-    const size_t split_stride = static_cast<size_t>(w) * 2 * ffn;
-    float g = 0.0f, u = 0.0f;
-    for (int s = 0; s < splits; ++s) {
-        g = __fadd_rn(g, ws[s * split_stride + row + f]);
-        u = __fadd_rn(u, ws[s * split_stride + row + ffn + f]);
-    }
-    const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    a[static_cast<size_t>(t) * ffn + f] = __float2bfloat16_rn(__fmul_rn(silu, u));
-}
-
-void launch_swiglu(int w, const float* ws, int splits, int ffn, __nv_bfloat16* a, cudaStream_t s) {
-    dim3 grid((ffn + 255) / 256, w);
-    swiglu_kernel<<<grid, 256, 0, s>>>(ws, splits, w, ffn, a);
-}
-
-// ------------------------------------------------------------ logits reduce
-__global__ void reduce_rows_kernel(const float* ws, int splits, int w, int n, float* out) {
-    const int t = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const size_t split_stride = static_cast<size_t>(w) * n;
-    float acc = 0.0f;
-    for (int s = 0; s < splits; ++s)
-        acc = __fadd_rn(acc, ws[s * split_stride + static_cast<size_t>(t) * n + i]);
-    out[static_cast<size_t>(t) * n + i] = acc;
-}
-
-void launch_reduce_rows(int w, const float* ws, int splits, int n, float* out, cudaStream_t s) {
-    dim3 grid((n + 255) / 256, w);
-    reduce_rows_kernel<<<grid, 256, 0, s>>>(ws, splits, w, n, out);
+void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
+                    cudaStream_t s) {
+    rmsnorm_kernel<<<w, 256, 0, s>>>(x, d, gain, eps, h);
 }
 
 // ------------------------------------------------------------ KV compaction

@@ -47,18 +47,14 @@ void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
                        int d, float eps, float* x, __nv_bfloat16* h, cudaStream_t s);
-void launch_qkv_epilogue(const PassState* ps, int w, const float* ws, int splits,
-                         const ModelDims& m, const float* rope_cos, const float* rope_sin,
-                         float* q_out, __nv_bfloat16* kv_pool, const int32_t* page_table,
-                         int page_size, int layer, cudaStream_t s);
 void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                       const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                       int layer, __nv_bfloat16* o, cudaStream_t s);
 void attention_set_max_keys(int max_keys);
-void launch_residual_norm(int w, const float* ws, int splits, int d, const float* gain, float eps,
-                          float* x, __nv_bfloat16* h, cudaStream_t s);
-void launch_swiglu(int w, const float* ws, int splits, int ffn, __nv_bfloat16* a, cudaStream_t s);
-void launch_reduce_rows(int w, const float* ws, int splits, int n, float* out, cudaStream_t s);
+void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
+                    cudaStream_t s);
+void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
+                                    uint64_t seed, float amp, int offset, cudaStream_t s);
 void launch_kv_compact(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                        const ModelDims& m, const int32_t* src_pos, const int32_t* dst_pos, int n,
                        cudaStream_t s);

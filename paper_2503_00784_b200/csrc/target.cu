@@ -68,40 +68,69 @@ const GemmPlan& plan_for(dd_ctx* c, int id, int nt) {
 }  // namespace
 
 // Enqueue one scored pass of width w on ctx->stream (all state via d_ps).
-int enqueue_pass(dd_ctx* ctx, int w, bool want_logits) {
+// `mark(cls)` (optional) records a CUDA event after each kernel for profiling:
+// cls 0 = GEMM (+fused epilogue), 1 = attention, 2 = norms/embedding.
+template <typename Mark>
+int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     const ModelDims& m = ctx->m;
     const int nt = round_nt(w);
     cudaStream_t s = ctx->stream;
-    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx) -> cudaError_t {
+    GemmEpiParams e{};
+    e.counters = ctx->counters;
+    e.ps = ctx->d_ps;
+    e.rope_cos = ctx->rope_cos;
+    e.rope_sin = ctx->rope_sin;
+    e.q_out = ctx->q;
+    e.kv_pool = ctx->kv_pool;
+    e.page_table = ctx->page_table;
+    e.page_size = ctx->page_size;
+    e.m = m;
+    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx,
+                    const GemmEpiParams& ep) -> cudaError_t {
         int n_out, k;
         gemm_shape(ctx, id, &n_out, &k);
         const GemmPlan& p = plan_for(ctx, id, nt);
-        return launch_gemm(mw, mx, n_out, k, w, nt, p, ctx->ws, s);
+        cudaError_t r = launch_gemm(mw, mx, n_out, k, w, nt, p, ctx->ws, ep, s);
+        mark(0);
+        return r;
     };
     launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, s);
+    mark(2);
     for (int l = 0; l < m.n_layers; ++l) {
         const LayerW& L = ctx->layers[l];
-        CK(gemm(kGQkv, &L.map_qkv, &ctx->map_h));
-        launch_qkv_epilogue(ctx->d_ps, w, ctx->ws, plan_for(ctx, kGQkv, nt).splits, m,
-                            ctx->rope_cos, ctx->rope_sin, ctx->q, ctx->kv_pool, ctx->page_table,
-                            ctx->page_size, l, s);
+        GemmEpiParams eq = e;
+        eq.kind = kEpiQkvRope;
+        eq.layer = l;
+        CK(gemm(kGQkv, &L.map_qkv, &ctx->map_h, eq));
         launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
                          ctx->o, s);
-        CK(gemm(kGO, &L.map_o, &ctx->map_o));
-        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGO, nt).splits, m.d, ctx->gain_ones, m.eps,
-                             ctx->x, ctx->h, s);
-        CK(gemm(kGGu, &L.map_gu, &ctx->map_h));
-        launch_swiglu(w, ctx->ws, plan_for(ctx, kGGu, nt).splits, m.ffn, ctx->a, s);
-        CK(gemm(kGDown, &L.map_d, &ctx->map_a));
-        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGDown, nt).splits, m.d, ctx->gain_ones,
-                             m.eps, ctx->x, ctx->h, s);
+        mark(1);
+        GemmEpiParams er = e;
+        er.kind = kEpiResidual;
+        er.out = ctx->x;
+        CK(gemm(kGO, &L.map_o, &ctx->map_o, er));
+        launch_rmsnorm(w, ctx->x, m.d, ctx->gain_ones, m.eps, ctx->h, s);
+        mark(2);
+        GemmEpiParams eg = e;
+        eg.kind = kEpiSwiGLU;
+        eg.out_bf = ctx->a;
+        CK(gemm(kGGu, &L.map_gu, &ctx->map_h, eg));
+        CK(gemm(kGDown, &L.map_d, &ctx->map_a, er));
+        launch_rmsnorm(w, ctx->x, m.d, ctx->gain_ones, m.eps, ctx->h, s);
+        mark(2);
     }
     if (want_logits) {
-        CK(gemm(kGHead, &ctx->map_head, &ctx->map_h));
-        launch_reduce_rows(w, ctx->ws, plan_for(ctx, kGHead, nt).splits, m.vocab, ctx->logits, s);
+        GemmEpiParams el = e;
+        el.kind = kEpiStore;
+        el.out = ctx->logits;
+        CK(gemm(kGHead, &ctx->map_head, &ctx->map_h, el));
     }
     CK(cudaGetLastError());
     return DD_OK;
+}
+
+int enqueue_pass(dd_ctx* ctx, int w, bool want_logits) {
+    return enqueue_pass_impl(ctx, w, want_logits, [](int) {});
 }
 
 // Upload pass state, then replay (or capture) the graph for width w.
@@ -161,10 +190,11 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     const dd_model_desc& d = *desc;
     if (d.n_layers < 1 || d.d_model % 128 || d.head_dim % 32 || d.head_dim > 256 ||
         d.n_heads % std::max(1, d.n_kv_heads) || d.ffn_dim % 128 || d.vocab % 128 ||
-        d.n_heads * d.head_dim % 64 || d.max_seq < 1)
+        (d.n_heads * d.head_dim) % 128 || (std::max(1, d.n_kv_heads) * d.head_dim) % 128 ||
+        128 % d.head_dim || d.max_seq < 1)
         return ctx_fail(nullptr, DD_E_ARG,
                         "unsupported shape (d_model, ffn_dim, vocab must be multiples of 128; "
-                        "head_dim a multiple of 32 <= 256)");
+                        "head_dim 32/64/128; q and kv widths multiples of 128)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cuda_device)
         return ctx_fail(nullptr, DD_E_CUDA, "no CUDA device available (no CPU fallback exists)");
@@ -238,6 +268,8 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
         }
     }
     CK(cudaMalloc(&ctx->ws, sizeof(float) * ws_floats));
+    CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
+    CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
     CK(cudaMalloc(&ctx->logits, sizeof(float) * R * m.vocab));
 
     // paged KV cache (all pages reserved up front; page table maps logical->physical)
@@ -301,7 +333,8 @@ void dd_ctx_destroy(dd_ctx* ctx) {
     void* dev[] = {ctx->emb, ctx->head, ctx->gain_ones, ctx->x, ctx->h, ctx->q, ctx->o, ctx->a,
                    ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
-                   ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs};
+                   ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
+                   ctx->counters};
     for (void* p : dev)
         if (p) cudaFree(p);
     if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
@@ -343,9 +376,10 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
         launch_init_matrix(L.qkv + (qd + kvd) * d_, kvd, d_,
                            derive_seed(weight_seed, tensor_id(l, kWv)), amp_proj, s);
         launch_init_matrix(L.o, d_, qd, derive_seed(weight_seed, tensor_id(l, kWo)), amp_out, s);
-        launch_init_matrix(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWg)), amp_proj, s);
-        launch_init_matrix(L.gu + static_cast<uint64_t>(m.ffn) * d_, m.ffn, d_,
-                           derive_seed(weight_seed, tensor_id(l, kWu)), amp_proj, s);
+        launch_init_matrix_interleaved(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWg)),
+                                       amp_proj, 0, s);
+        launch_init_matrix_interleaved(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWu)),
+                                       amp_proj, 64, s);
         launch_init_matrix(L.dn, d_, m.ffn, derive_seed(weight_seed, tensor_id(l, kWd)), amp_out, s);
     }
     CK(cudaGetLastError());
@@ -552,71 +586,31 @@ int dd_time_pass(dd_ctx* ctx, int w, int trials, float* median_ms) {
 
 int dd_profile_pass(dd_ctx* ctx, int w, float* ms4) {
     if (!ctx || !ms4 || w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (ctx->n_cached + w > ctx->max_seq) return ctx_fail(ctx, DD_E_CAPACITY, "cache full");
     CK(cudaSetDevice(ctx->device));
-    const ModelDims& m = ctx->m;
     const int n0 = ctx->n_cached;
-    std::vector<int32_t> toks(w, 0);
-    // upload pass state via a zero-cost pass setup
     const int slot = ctx->ps_slot;
     ctx->ps_slot = (slot + 1) % kPsRing;
     CK(cudaEventSynchronize(ctx->ps_done[slot]));
     PassState* hp = ctx->h_ps + slot;
     hp->n_cached = n0;
     hp->w = w;
-    std::memcpy(hp->tokens, toks.data(), sizeof(int32_t) * w);
+    for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
     CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
-    const int nt = round_nt(w);
-    cudaStream_t s = ctx->stream;
     std::vector<cudaEvent_t> ev;
     std::vector<int> cls;
     auto mark = [&](int c) {
         cudaEvent_t e;
         cudaEventCreate(&e);
-        cudaEventRecord(e, s);
+        cudaEventRecord(e, ctx->stream);
         ev.push_back(e);
         cls.push_back(c);
     };
-    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx) {
-        int n_out, k;
-        gemm_shape(ctx, id, &n_out, &k);
-        launch_gemm(mw, mx, n_out, k, w, nt, plan_for(ctx, id, nt), ctx->ws, s);
-    };
     mark(-1);
-    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, s);
-    mark(2);
-    for (int l = 0; l < m.n_layers; ++l) {
-        const LayerW& L = ctx->layers[l];
-        gemm(kGQkv, &L.map_qkv, &ctx->map_h);
-        mark(0);
-        launch_qkv_epilogue(ctx->d_ps, w, ctx->ws, plan_for(ctx, kGQkv, nt).splits, m,
-                            ctx->rope_cos, ctx->rope_sin, ctx->q, ctx->kv_pool, ctx->page_table,
-                            ctx->page_size, l, s);
-        mark(2);
-        launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
-                         ctx->o, s);
-        mark(1);
-        gemm(kGO, &L.map_o, &ctx->map_o);
-        mark(0);
-        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGO, nt).splits, m.d, ctx->gain_ones, m.eps,
-                             ctx->x, ctx->h, s);
-        mark(2);
-        gemm(kGGu, &L.map_gu, &ctx->map_h);
-        mark(0);
-        launch_swiglu(w, ctx->ws, plan_for(ctx, kGGu, nt).splits, m.ffn, ctx->a, s);
-        mark(2);
-        gemm(kGDown, &L.map_d, &ctx->map_a);
-        mark(0);
-        launch_residual_norm(w, ctx->ws, plan_for(ctx, kGDown, nt).splits, m.d, ctx->gain_ones,
-                             m.eps, ctx->x, ctx->h, s);
-        mark(2);
-    }
-    gemm(kGHead, &ctx->map_head, &ctx->map_h);
-    mark(0);
-    launch_reduce_rows(w, ctx->ws, plan_for(ctx, kGHead, nt).splits, m.vocab, ctx->logits, s);
-    mark(2);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
+    int rc = enqueue_pass_impl(ctx, w, true, mark);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < 4; ++i) ms4[i] = 0.0f;
     for (size_t i = 1; i < ev.size(); ++i) {
         float x = 0;
@@ -658,6 +652,16 @@ int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n)
     }
     if (n != count) return ctx_fail(ctx, DD_E_ARG, "element count mismatch");
     CK(cudaSetDevice(ctx->device));
+    if (which == 4) {  // stored interleaved in 64-row blocks; return [gate; up]
+        std::vector<uint16_t> tmp(n);
+        CK(cudaMemcpy(tmp.data(), src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
+        for (size_t pr = 0; pr < 2 * static_cast<size_t>(m.ffn); ++pr) {
+            const size_t blk = pr / 128, off = pr % 128;
+            const size_t lr = off < 64 ? blk * 64 + off : m.ffn + blk * 64 + (off - 64);
+            std::memcpy(host + lr * d_, tmp.data() + pr * d_, sizeof(uint16_t) * d_);
+        }
+        return DD_OK;
+    }
     CK(cudaMemcpy(host, src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
     return DD_OK;
 }
@@ -684,8 +688,14 @@ int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, 
     GemmPlan p = plan_gemm(n_out, k, nt);
     CK(cudaMalloc(&dws, sizeof(float) * p.splits * static_cast<size_t>(w) * n_out));
     CK(cudaMalloc(&dY, sizeof(float) * static_cast<size_t>(w) * n_out));
-    CK(launch_gemm(&mw, &mx, n_out, k, w, nt, p, dws, 0));
-    launch_reduce_rows(w, dws, p.splits, n_out, dY, 0);
+    int* dcnt = nullptr;
+    CK(cudaMalloc(&dcnt, sizeof(int) * p.tiles));
+    CK(cudaMemset(dcnt, 0, sizeof(int) * p.tiles));
+    GemmEpiParams ep{};
+    ep.kind = kEpiStore;
+    ep.counters = dcnt;
+    ep.out = dY;
+    CK(launch_gemm(&mw, &mx, n_out, k, w, nt, p, dws, ep, 0));
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(Y, dY, sizeof(float) * static_cast<size_t>(w) * n_out, cudaMemcpyDeviceToHost));
@@ -693,6 +703,7 @@ int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, 
     cudaFree(dX);
     cudaFree(dws);
     cudaFree(dY);
+    cudaFree(dcnt);
     return DD_OK;
 }
 
