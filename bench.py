@@ -1,0 +1,378 @@
+"""bench.py — DuoDecoding on B200: decode tokens/sec + p50 TTFT (BASELINE.json).
+
+Workload (BASELINE.json configs[1], "config 2"): Llama-2-7B-shape bf16 target on
+one B200 + Llama-68M-shape draft on host cores, seeded random-init weights with
+a planted shared bigram (alpha recorded), 128-token synthetic prompt, 128 new
+tokens, greedy, DuoDecoding with the draft budget calibrated on this box.
+
+One step = one generation through the public C-ABI engine (dd_engine_run):
+prefill of the prompt, then decode until 128 new tokens are committed.
+  value  = decode tokens/sec: tokens committed after the first iteration over
+           the device (CUDA-event) time after the first iteration, summed over
+           the timed steps; whole job over N ranks (weak scaling: one
+           independent request stream + pinned draft worker per GPU).
+  e2e    = reference-style TPS (proj/src/engine.cpp:117-122: generated tokens /
+           total wall time incl. prefill and TTFT) of the same calls, host
+           prompt in, host tokens out.
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+(N > 1 under torch.distributed.run; rank r uses GPU LOCAL_RANK and a disjoint
+slice of host cores).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+SEED_W_TARGET, SEED_W_DRAFT = 1234, 99
+PROMPT_LEN, NEW_TOKENS = 128, 128
+METRIC = ("decode tokens/sec (Llama-2-7B-shape target on B200 + Llama-68M-shape CPU draft, "
+          "DuoDecoding, greedy)")
+
+
+def splitmix(seed: int, m: int) -> int:
+    M = (1 << 64) - 1
+    z = (seed + m * 0x9E3779B97F4A7C15) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def make_prompt(prompt_seed: int, n: int = PROMPT_LEN, vocab: int = 32000):
+    """token_i = splitmix64(prompt_seed, i) mod V."""
+    return [splitmix(prompt_seed, i + 1) % vocab for i in range(n)]
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def core_slice(rank: int, world: int):
+    cpus = sorted(os.sched_getaffinity(0))
+    per = max(2, len(cpus) // world)
+    mine = cpus[rank * per:(rank + 1) * per] or cpus[-per:]
+    return mine[0], mine[1:] or mine[:1]  # (target thread core, draft cores)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                self.rows.append(p)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-pass DRAM bytes of the GEMM launches from the committed ncu capture."""
+    p = ROOT / "profiles" / "gemm_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return None
+    return None
+
+
+def decode_stats(res):
+    first = res.iterations[0].tokens_processed if res.iterations else 0
+    return len(res.tokens) - first
+
+
+# ---------------------------------------------------------------- CPU side
+def cpu_decode_sample(shape_t, shape_d, plant, budget, threads, sample_tokens, prefilled=None):
+    """The all-CPU restated reference loop (oracle/cpu_engine.py) on host cores:
+    returns (decode tok/s, description, cores)."""
+    from oracle.cpu_engine import run_cpu
+    from oracle.llama import OracleLlama
+    tgt = prefilled[0] if prefilled else OracleLlama(shape_t, SEED_W_TARGET, plant,
+                                                      max_seq=PROMPT_LEN + 512, threads=threads)
+    drf = prefilled[1] if prefilled else OracleLlama(shape_d, SEED_W_DRAFT, plant,
+                                                      max_seq=PROMPT_LEN + 512, threads=threads)
+    prompt = make_prompt(1)
+    r = run_cpu("duo", tgt, drf, prompt, budget, 4, sample_tokens, greedy=True)
+    first = r["iterations"][0]
+    dec_tok = len(r["tokens"]) - first
+    dec_ms = r["total_ms"] - r["ttft_ms"]
+    return dec_tok / (dec_ms / 1e3), r, (tgt, drf)
+
+
+def run_reference(args):
+    """--impl reference: the reference's loop restated on the CPU oracle (the
+    reference itself runs only Markov tables), all host threads, rank 0 only."""
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        if rank != 0:
+            dist.barrier()
+            return
+    from paper_2503_00784_b200 import DEFAULT_PLANT, SHAPES
+    threads = len(os.sched_getaffinity(0))
+    plant = dict(DEFAULT_PLANT)
+    budget = args.budget or 8
+    from oracle.cpu_engine import run_cpu
+    from oracle.llama import OracleLlama
+    tgt = OracleLlama(SHAPES["llama2_7b"], SEED_W_TARGET, plant, PROMPT_LEN + 512, threads)
+    drf = OracleLlama(SHAPES["llama_68m"], SEED_W_DRAFT, plant, PROMPT_LEN + 512, threads)
+    prompt = make_prompt(1)
+    rates = []
+    for step in range(args.warmup + args.steps):
+        r = run_cpu("duo", tgt, drf, prompt, budget, 4, args.ref_tokens, greedy=True)
+        dec = len(r["tokens"]) - r["iterations"][0]
+        rate = dec / ((r["total_ms"] - r["ttft_ms"]) / 1e3)
+        if step >= args.warmup:
+            rates.append((dec, r["total_ms"] - r["ttft_ms"], r["ttft_ms"]))
+    tok = sum(x[0] for x in rates)
+    ms = sum(x[1] for x in rates)
+    value = tok / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms / len(rates), 2), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 weights / fp32 compute (CPU)", "data": "synthetic",
+        "config": {"workload": "config2 on host cores: restated reference duo loop "
+                                "(oracle/cpu_engine.py) with the CPU Llama oracle as target "
+                                "and draft", "prompt_len": PROMPT_LEN,
+                   "decode_tokens_per_step": args.ref_tokens, "budget": budget, "greedy": True,
+                   "alpha": plant["alpha"]},
+        "ttft_p50_ms": round(statistics.median(x[2] for x in rates), 1),
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{args.ref_tokens} new tokens after a 128-token prompt per "
+                                   f"step, decode phase timed (prefill excluded)"},
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- GPU side
+def run_ours(args):
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    from paper_2503_00784_b200 import (DEFAULT_PLANT, SHAPES, Draft, EngineConfig, Target,
+                                       calibrate, run_generation)
+    plant = dict(DEFAULT_PLANT, alpha=args.alpha)
+    tcore, dcores = core_slice(rank, ws)
+    os.sched_setaffinity(0, {tcore})  # target-role thread
+    tgt = Target(SHAPES["llama2_7b"], weight_seed=SEED_W_TARGET, plant=plant,
+                 max_seq=PROMPT_LEN + NEW_TOKENS + 512, device=local)
+    drf = Draft(SHAPES["llama_68m"], weight_seed=SEED_W_DRAFT, plant=plant, threads=len(dcores),
+                cpus=dcores)
+    if args.budget:
+        budget, coef = args.budget, None
+    else:
+        coef, budget = calibrate(tgt, drf, probe_len=8, trials=12)
+    cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=args.max_sequences,
+                       max_new_tokens=NEW_TOKENS, greedy=True)
+
+    def one(step):
+        return run_generation(tgt, drf, make_prompt(1000 * rank + step + 1), cfg)
+
+    for s in range(args.warmup):
+        one(s)
+    if dist:
+        dist.barrier()
+    results, walls = [], []
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            t0 = time.perf_counter()
+            r = one(args.warmup + s)
+            walls.append(time.perf_counter() - t0)
+            results.append(r)
+    if dist:
+        dist.barrier()
+    dec_tok = sum(decode_stats(r) for r in results)
+    dec_ms = sum(r.device_ms - r.device_ttft_ms for r in results)
+    gen_tok = sum(len(r.tokens) for r in results)
+    wall_s = sum(walls)
+    ttfts = [r.device_ttft_ms for r in results]
+    launches = sum(r.gpu_launches for r in results)
+    h2d = sum(r.h2d_bytes for r in results) / len(results)
+    d2h = sum(r.d2h_bytes for r in results) / len(results)
+    widths = [it.width for r in results for it in r.iterations]
+    tok_per_iter = statistics.mean(it.tokens_processed for r in results for it in r.iterations)
+    if dist:
+        import torch
+        t = torch.tensor([dec_tok, gen_tok], dtype=torch.float64, device=f"cuda:{local}")
+        m = torch.tensor([dec_ms, wall_s], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        dec_tok_all, gen_tok_all = float(t[0]), float(t[1])
+        dec_ms_max, wall_max = float(m[0]), float(m[1])
+    else:
+        dec_tok_all, gen_tok_all, dec_ms_max, wall_max = dec_tok, gen_tok, dec_ms, wall_s
+    value = dec_tok_all / (dec_ms_max / 1e3)
+    e2e_value = gen_tok_all / wall_max
+
+    extra = {}
+    if rank == 0:
+        # roofline of the dominant kernel: the weight-streaming GEMM launches of a pass
+        w_typ = max(1, int(round(statistics.mean(widths))))
+        tgt.truncate(0)
+        tgt.prefill(make_prompt(7))
+        gemm_ms, n_launch = tgt.time_gemms(w_typ, trials=5)
+        pass_ms = tgt.time_pass(w_typ, trials=10)
+        wb = tgt.pass_weight_bytes()
+        peak, peak_src = measured_peak()
+        achieved = wb / (gemm_ms / 1e3) / 1e9
+        tr = ncu_traffic()
+        extra["roofline"] = {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": (tr.get("dram_bytes_per_pass") if tr else None),
+            "kernel": "gemm_skinny_kernel (tcgen05 + TMA weight streaming, cluster split-K)",
+            "launches_per_pass": n_launch, "algorithmic_bytes_per_pass": wb,
+            "width": w_typ, "gemm_ms_per_pass": round(gemm_ms, 4), "peak_source": peak_src,
+            "pass_ms": round(pass_ms, 4),
+            "pass_frac": round(wb / (pass_ms / 1e3) / 1e9 / peak, 4)}
+        # same-run GPU baselines: target-only AR and conventional SpS
+        base = {}
+        for mode, bud in (("vanilla", 2), ("sps", max(2, budget // 2))):
+            c2 = EngineConfig(mode=mode, budget=bud, max_new_tokens=NEW_TOKENS, greedy=True)
+            r2 = run_generation(tgt, drf if mode != "vanilla" else None, make_prompt(1), c2)
+            base[mode] = {"decode_tps": round(decode_stats(r2) / (first_decode_ms(r2) / 1e3), 1),
+                          "tps_reference_style": round(r2.tps, 1),
+                          "ttft_ms": round(r2.device_ttft_ms, 2), "budget": bud}
+        extra["gpu_baselines"] = base
+        if ws == 1 and not args.no_cpu_baseline:
+            thr = os.cpu_count()
+            os.sched_setaffinity(0, set(range(os.cpu_count())))
+            rate, r, _ = cpu_decode_sample(SHAPES["llama2_7b"], SHAPES["llama_68m"], plant,
+                                           budget, thr, args.cpu_tokens)
+            extra["cpu_baseline"] = {
+                "value": round(rate, 3), "unit": "tokens/s", "cores": thr, "kind": "port",
+                "sample": f"restated reference duo loop (oracle/cpu_engine.py) with the CPU "
+                          f"Llama oracle as 7B target and 68M draft: {args.cpu_tokens} new "
+                          f"tokens after the 128-token prompt, decode phase timed; "
+                          f"prefill/TTFT {r['ttft_ms'] / 1e3:.1f} s"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dec_ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data":
+                "synthetic: seeded random-init weights (planted shared bigram, alpha recorded), "
+                "splitmix64 prompts",
+            "config": {"workload": "config2: Llama-2-7B-shape bf16 target on 1 B200 per rank + "
+                                   "Llama-68M-shape draft on pinned host cores, 128-token "
+                                   "prompt, 128 new tokens, greedy, DuoDecoding",
+                       "model": "llama2_7b target / llama_68m draft", "global_batch": ws,
+                       "seq_len": PROMPT_LEN + NEW_TOKENS, "parallelism": f"replicas{ws}",
+                       "mode": args.mode, "budget": budget, "calibrated_c": coef,
+                       "max_sequences": args.max_sequences, "alpha": plant["alpha"],
+                       "draft_cores": len(dcores),
+                       "l2": "weights 13.2 GB >> 126 MB L2: every pass re-streams from HBM"},
+            "ttft_p50_ms": round(statistics.median(ttfts), 2),
+            "tps_reference_style": round(gen_tok_all / sum(r.total_ms for r in results) * 1e3, 2),
+            "tokens_per_iteration": round(tok_per_iter, 3),
+            "mean_pass_width": round(statistics.mean(widths), 2),
+            "e2e": {"value": round(e2e_value, 2), "unit": "tokens/s",
+                    "definition": "generated/total wall incl. prefill (engine.cpp:117-122)",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    tgt.close()
+    drf.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def first_decode_ms(r):
+    return max(1e-6, r.device_ms - r.device_ttft_ms)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="duo", choices=["duo", "sps", "vanilla"])
+    ap.add_argument("--budget", type=int, default=0, help="0 = calibrate on this box")
+    ap.add_argument("--max-sequences", type=int, default=4)
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--cpu-tokens", type=int, default=16)
+    ap.add_argument("--ref-tokens", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from paper_2503_00784_b200 import DEFAULT_PLANT
+    if args.alpha is None:
+        args.alpha = DEFAULT_PLANT["alpha"]
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,11 @@ int dd_time_pass(dd_ctx* ctx, int w, int trials, float* median_ms);
  * 0 gemm, 1 attention, 2 epilogues/norms, 3 total). */
 int dd_profile_pass(dd_ctx* ctx, int w, float* ms4);
 
+/* Device time of the GEMM launches of one pass of width w (the 4 per layer
+ * plus the LM head, back to back, fused epilogues included), median of
+ * `trials`; the weight-streaming roofline of the dominant kernel. */
+int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launches);
+
 /* Algorithmic weight bytes streamed by one pass (excludes the gathered
  * embedding), for the roofline. */
 uint64_t dd_pass_weight_bytes(const dd_ctx* ctx);
@@ -216,6 +221,11 @@ typedef struct dd_generation_result { /* GenerationResult (engine.hpp:72-78) */
     double tps;
     double prefill_ms;
     int budget_used;
+    double device_ms;      /* CUDA-event time on the target stream, start->end */
+    uint64_t h2d_bytes;    /* host->device bytes copied during the run        */
+    uint64_t d2h_bytes;    /* device->host bytes copied during the run        */
+    uint64_t gpu_launches; /* kernels launched (graph nodes counted)          */
+    double device_ttft_ms; /* CUDA-event time start -> end of iteration 1     */
 } dd_generation_result;
 
 /* Run one generation: target on the GPU (ctx), draft on host cores (draft,

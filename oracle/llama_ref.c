@@ -293,12 +293,31 @@ typedef struct {
     const float* x;
     float* y;
 } mm_arg;
+static inline float dot_f32(const float* w, const float* x, int k) {
+    float acc[16] = {0};
+    int i = 0;
+    for (; i + 16 <= k; i += 16)
+        for (int j = 0; j < 16; ++j) acc[j] += w[i + j] * x[i + j];
+    for (; i < k; ++i) acc[i & 15] += w[i] * x[i];
+    float s = 0.0f;
+    for (int j = 0; j < 16; ++j) s += acc[j];
+    return s;
+}
 static void mm_range(void* p, int64_t lo, int64_t hi) {
     mm_arg* a = (mm_arg*)p;
-    for (int64_t n = lo; n < hi; ++n)
+    if (a->w == 1) {
+        for (int64_t n = lo; n < hi; ++n)
+            a->y[n] = dot_bf16(a->W + (size_t)n * a->k, a->x, a->k);
+        return;
+    }
+    float* wr = (float*)malloc(sizeof(float) * a->k);  /* row converted once */
+    for (int64_t n = lo; n < hi; ++n) {
+        const uint16_t* src = a->W + (size_t)n * a->k;
+        for (int i = 0; i < a->k; ++i) wr[i] = bf2f(src[i]);
         for (int t = 0; t < a->w; ++t)
-            a->y[(size_t)t * a->rows + n] =
-                dot_bf16(a->W + (size_t)n * a->k, a->x + (size_t)t * a->k, a->k);
+            a->y[(size_t)t * a->rows + n] = dot_f32(wr, a->x + (size_t)t * a->k, a->k);
+    }
+    free(wr);
 }
 static void matmul(const uint16_t* W, int rows, int k, const float* x, int w, float* y) {
     mm_arg a = {W, rows, k, w, x, y};

@@ -188,6 +188,13 @@ class Target:
         _check(_L.lib().dd_profile_pass(self.h, w, ms), self.h)
         return dict(gemm=ms[0], attention=ms[1], epilogue=ms[2], total=ms[3])
 
+    def time_gemms(self, w: int, trials: int = 5):
+        """(median ms, launches) of the pass's GEMM launches back to back."""
+        ms = C.c_float()
+        n = C.c_int()
+        _check(_L.lib().dd_time_gemms(self.h, w, trials, C.byref(ms), C.byref(n)), self.h)
+        return ms.value, n.value
+
     def pass_weight_bytes(self) -> int:
         return int(_L.lib().dd_pass_weight_bytes(self.h))
 
@@ -315,6 +322,11 @@ class GenerationResult:
     tps: float = 0.0
     prefill_ms: float = 0.0
     budget: int = 0
+    device_ms: float = 0.0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    gpu_launches: int = 0
+    device_ttft_ms: float = 0.0
 
 
 def run_generation(target: Target, draft: Optional[Draft], prompt: Sequence[int],
@@ -334,7 +346,9 @@ def run_generation(target: Target, draft: Optional[Draft], prompt: Sequence[int]
                                   len(p), C.byref(r)), target.h)
     out = GenerationResult(tokens=[int(x) for x in toks[:r.n_tokens]], ttft_ms=r.ttft_ms,
                            total_ms=r.total_ms, tps=r.tps, prefill_ms=r.prefill_ms,
-                           budget=r.budget_used)
+                           budget=r.budget_used, device_ms=r.device_ms, h2d_bytes=r.h2d_bytes,
+                           d2h_bytes=r.d2h_bytes, gpu_launches=r.gpu_launches,
+                           device_ttft_ms=r.device_ttft_ms)
     for i in range(r.n_iterations):
         it = iters[i]
         out.iterations.append(IterationRecord(it.draft_ms, it.target_ms, it.verify_ms, it.comm_ms,

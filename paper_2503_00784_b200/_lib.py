@@ -59,7 +59,9 @@ class GenerationResultC(C.Structure):
                 ("n_tokens", C.c_int), ("iterations", C.POINTER(IterationRecordC)),
                 ("max_iterations", C.c_int), ("n_iterations", C.c_int), ("ttft_ms", C.c_double),
                 ("total_ms", C.c_double), ("tps", C.c_double), ("prefill_ms", C.c_double),
-                ("budget_used", C.c_int)]
+                ("budget_used", C.c_int), ("device_ms", C.c_double), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("gpu_launches", C.c_uint64),
+                ("device_ttft_ms", C.c_double)]
 
 
 # every entry point of include/duodec_b200.h: name -> (restype, argtypes)
@@ -86,6 +88,7 @@ SIGNATURES = {
     "dd_time_pass": (C.c_int, [_vp, C.c_int, C.c_int, _f32p]),
     "dd_profile_pass": (C.c_int, [_vp, C.c_int, _f32p]),
     "dd_pass_weight_bytes": (C.c_uint64, [_vp]),
+    "dd_time_gemms": (C.c_int, [_vp, C.c_int, C.c_int, _f32p, C.POINTER(C.c_int)]),
     "dd_read_weights": (C.c_int, [_vp, C.c_int, C.c_int, _u16p, C.c_size_t]),
     "dd_test_gemm": (C.c_int, [_u16p, _u16p, C.c_int, C.c_int, C.c_int, _f32p]),
     "dd_draft_create": (C.c_int, [C.POINTER(ModelDesc), C.c_uint64, C.POINTER(PlantDesc), C.c_int,

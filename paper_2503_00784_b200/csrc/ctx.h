@@ -80,7 +80,15 @@ struct dd_ctx {
     std::map<int, dd::GemmPlan> plans;
     std::map<int, cudaGraphExec_t> graphs;
     std::string err;
+    // accounting for dd_engine_run
+    uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
+    std::map<int, int> graph_kernels;  // kernels per captured pass graph
+    cudaEvent_t t_start = nullptr, t_end = nullptr, t_first = nullptr;
 };
+
+// engine-side helpers (target.cu)
+int ctx_mark(dd_ctx* ctx, int which);      // record start (0) / end (1) / first-iteration (2)
+double ctx_elapsed_ms(dd_ctx* ctx, int which);  // start -> end (1) or first (2); syncs
 
 int ctx_fail(dd_ctx* ctx, int code, const std::string& msg);
 int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits);

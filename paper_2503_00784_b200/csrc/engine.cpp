@@ -31,8 +31,7 @@
 #include "../../include/duodec_b200.h"
 #include "draft.h"
 
-struct dd_ctx;
-int ctx_fail(dd_ctx* ctx, int code, const std::string& msg);
+#include "ctx.h"
 
 namespace {
 
@@ -227,7 +226,10 @@ struct Runner {
 
     void record(dd_iteration_record r) {
         recs.push_back(r);
-        if (recs.size() == 1) ttft = ms_since(t_start);
+        if (recs.size() == 1) {
+            ttft = ms_since(t_start);
+            ck(ctx_mark(ctx, 2), ctx);
+        }
     }
 
     dd_verify_out verify(int mode, int L, const std::vector<int32_t>& firsts, bool q_onehot) {
@@ -478,6 +480,8 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
         r.prompt_len = static_cast<size_t>(n_prompt);
         r.rng_draft.seed = c.draft_seed;
         r.rng_verify.seed = c.verify_seed;
+        ctx->h2d_bytes = ctx->d2h_bytes = ctx->launches = 0;
+        ck(ctx_mark(ctx, 0), ctx);
         r.t_start = Clock::now();
         ck(dd_kv_truncate(ctx, 0), ctx);
         if (n_prompt > 1) ck(dd_prefill(ctx, prompt, n_prompt - 1), ctx);
@@ -493,6 +497,12 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
             }
         }
         const double total = ms_since(r.t_start);
+        ck(ctx_mark(ctx, 1), ctx);
+        out->device_ms = ctx_elapsed_ms(ctx, 1);
+        out->device_ttft_ms = ctx_elapsed_ms(ctx, 2);
+        out->h2d_bytes = ctx->h2d_bytes + sizeof(int32_t) * static_cast<uint64_t>(n_prompt);
+        out->d2h_bytes = ctx->d2h_bytes;
+        out->gpu_launches = ctx->launches;
         const size_t gen = r.verified.size() - r.prompt_len;
         out->n_tokens = static_cast<int>(gen);
         for (size_t i = 0; i < gen && static_cast<int>(i) < out->max_tokens; ++i)

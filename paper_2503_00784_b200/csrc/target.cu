@@ -129,8 +129,27 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     return DD_OK;
 }
 
-int enqueue_pass(dd_ctx* ctx, int w, bool want_logits) {
-    return enqueue_pass_impl(ctx, w, want_logits, [](int) {});
+int enqueue_pass(dd_ctx* ctx, int w, bool want_logits, int* kernels) {
+    int n = 0;
+    int rc = enqueue_pass_impl(ctx, w, want_logits, [&n](int) { ++n; });
+    if (kernels) *kernels = n;
+    return rc;
+}
+
+int ctx_mark(dd_ctx* ctx, int which) {
+    cudaEvent_t* e = which == 0 ? &ctx->t_start : which == 1 ? &ctx->t_end : &ctx->t_first;
+    if (!*e) CK(cudaEventCreate(e));
+    CK(cudaEventRecord(*e, ctx->stream));
+    return DD_OK;
+}
+
+double ctx_elapsed_ms(dd_ctx* ctx, int which) {
+    cudaEvent_t e = which == 2 ? ctx->t_first : ctx->t_end;
+    if (!ctx->t_start || !e) return 0.0;
+    cudaEventSynchronize(e);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, ctx->t_start, e);
+    return ms;
 }
 
 // Upload pass state, then replay (or capture) the graph for width w.
@@ -150,6 +169,7 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
     std::memcpy(hp->tokens, tokens, sizeof(int32_t) * w);
     CK(cudaMemcpyAsync(ctx->d_ps, hp, offsetof(PassState, tokens) + sizeof(int32_t) * w,
                        cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += offsetof(PassState, tokens) + sizeof(int32_t) * w;
     CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
     if (ctx->use_graphs) {
         const int key = w * 2 + (want_logits ? 1 : 0);
@@ -157,7 +177,9 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
         if (it == ctx->graphs.end()) {
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-            int rc = enqueue_pass(ctx, w, want_logits);
+            int nk = 0;
+            int rc = enqueue_pass(ctx, w, want_logits, &nk);
+            ctx->graph_kernels[key] = nk;
             cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
             if (rc != DD_OK) return rc;
             CK(e);
@@ -167,9 +189,12 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
             it = ctx->graphs.emplace(key, ge).first;
         }
         CK(cudaGraphLaunch(it->second, ctx->stream));
+        ctx->launches += ctx->graph_kernels[key];
     } else {
-        int rc = enqueue_pass(ctx, w, want_logits);
+        int nk = 0;
+        int rc = enqueue_pass(ctx, w, want_logits, &nk);
         if (rc != DD_OK) return rc;
+        ctx->launches += nk;
     }
     ctx->n_cached += w;
     ctx->last_w = want_logits ? w : 0;
@@ -330,6 +355,8 @@ void dd_ctx_destroy(dd_ctx* ctx) {
         cudaFree(L.gu);
         cudaFree(L.dn);
     }
+    for (cudaEvent_t e : {ctx->t_start, ctx->t_end, ctx->t_first})
+        if (e) cudaEventDestroy(e);
     void* dev[] = {ctx->emb, ctx->head, ctx->gain_ones, ctx->x, ctx->h, ctx->q, ctx->o, ctx->a,
                    ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
@@ -460,6 +487,7 @@ int dd_upload_q(dd_ctx* ctx, const float* q_rows, int rows, int vocab) {
     std::memcpy(ctx->h_q_stage, q_rows, bytes);
     CK(cudaMemcpyAsync(ctx->q_rows, ctx->h_q_stage, bytes, cudaMemcpyHostToDevice,
                        ctx->copy_stream));
+    ctx->h2d_bytes += bytes;
     CK(cudaEventRecord(ctx->q_ready, ctx->copy_stream));
     ctx->q_rows_valid = rows;
     return DD_OK;
@@ -486,8 +514,10 @@ static int verify_common(dd_ctx* ctx, AcceptParams& p, const dd_verify_args* arg
         CK(cudaStreamWaitEvent(ctx->stream, ctx->q_ready, 0));
     }
     CK(launch_accept(p, ctx->stream));
+    ctx->launches += 1;
     CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(dd_verify_out), cudaMemcpyDeviceToHost,
                        ctx->stream));
+    ctx->d2h_bytes += sizeof(dd_verify_out);
     CK(cudaStreamSynchronize(ctx->stream));
     *out = *ctx->h_out;
     return DD_OK;
@@ -619,6 +649,93 @@ int dd_profile_pass(dd_ctx* ctx, int w, float* ms4) {
         ms4[3] += x;
     }
     for (auto e : ev) cudaEventDestroy(e);
+    ctx->n_cached = n0;
+    ctx->last_w = 0;
+    return DD_OK;
+}
+
+int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launches) {
+    if (!ctx || !median_ms || w < 1 || w > kMaxPassTokens || trials < 1)
+        return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (ctx->n_cached + w > ctx->max_seq) return ctx_fail(ctx, DD_E_CAPACITY, "cache full");
+    CK(cudaSetDevice(ctx->device));
+    const ModelDims& m = ctx->m;
+    const int nt = round_nt(w);
+    const int n0 = ctx->n_cached;
+    // pass state for the qkv epilogue positions
+    const int slot = ctx->ps_slot;
+    ctx->ps_slot = (slot + 1) % kPsRing;
+    CK(cudaEventSynchronize(ctx->ps_done[slot]));
+    PassState* hp = ctx->h_ps + slot;
+    hp->n_cached = n0;
+    hp->w = w;
+    for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
+    CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
+    GemmEpiParams e{};
+    e.counters = ctx->counters;
+    e.ps = ctx->d_ps;
+    e.rope_cos = ctx->rope_cos;
+    e.rope_sin = ctx->rope_sin;
+    e.q_out = ctx->q;
+    e.kv_pool = ctx->kv_pool;
+    e.page_table = ctx->page_table;
+    e.page_size = ctx->page_size;
+    e.m = m;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    std::vector<float> ms;
+    int n_launch = 0;
+    for (int t = 0; t < trials + 1; ++t) {
+        n_launch = 0;
+        CK(cudaEventRecord(a, ctx->stream));
+        for (int l = 0; l < m.n_layers; ++l) {
+            const LayerW& L = ctx->layers[l];
+            int n_out, k;
+            GemmEpiParams eq = e;
+            eq.kind = kEpiQkvRope;
+            eq.layer = l;
+            gemm_shape(ctx, kGQkv, &n_out, &k);
+            CK(launch_gemm(&L.map_qkv, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGQkv, nt),
+                           ctx->ws, eq, ctx->stream));
+            GemmEpiParams er = e;
+            er.kind = kEpiResidual;
+            er.out = ctx->x;
+            gemm_shape(ctx, kGO, &n_out, &k);
+            CK(launch_gemm(&L.map_o, &ctx->map_o, n_out, k, w, nt, plan_for(ctx, kGO, nt), ctx->ws,
+                           er, ctx->stream));
+            GemmEpiParams eg = e;
+            eg.kind = kEpiSwiGLU;
+            eg.out_bf = ctx->a;
+            gemm_shape(ctx, kGGu, &n_out, &k);
+            CK(launch_gemm(&L.map_gu, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGGu, nt),
+                           ctx->ws, eg, ctx->stream));
+            gemm_shape(ctx, kGDown, &n_out, &k);
+            CK(launch_gemm(&L.map_d, &ctx->map_a, n_out, k, w, nt, plan_for(ctx, kGDown, nt),
+                           ctx->ws, er, ctx->stream));
+            n_launch += 4;
+        }
+        GemmEpiParams el = e;
+        el.kind = kEpiStore;
+        el.out = ctx->logits;
+        int n_out, k;
+        gemm_shape(ctx, kGHead, &n_out, &k);
+        CK(launch_gemm(&ctx->map_head, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGHead, nt),
+                       ctx->ws, el, ctx->stream));
+        ++n_launch;
+        CK(cudaEventRecord(b, ctx->stream));
+        CK(cudaEventSynchronize(b));
+        float x = 0.0f;
+        CK(cudaEventElapsedTime(&x, a, b));
+        if (t > 0) ms.push_back(x);  // first run warms up
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    std::sort(ms.begin(), ms.end());
+    const size_t n = ms.size();
+    *median_ms = n % 2 ? ms[n / 2] : 0.5f * (ms[n / 2 - 1] + ms[n / 2]);
+    if (launches) *launches = n_launch;
     ctx->n_cached = n0;
     ctx->last_w = 0;
     return DD_OK;
