@@ -19,6 +19,7 @@ import numpy as np
 from . import _lib as _L
 
 __all__ = [
+    "StateError",
     "SHAPES", "Target", "Draft", "EngineConfig", "GenerationResult", "IterationRecord",
     "run_generation", "run_vanilla", "run_sps", "run_duo", "calibrate", "choose_budget",
     "ConfigError", "DegenerateTiming", "DeviceError", "DuoError",

@@ -124,18 +124,23 @@ SpinPool::SpinPool(int n_threads, const std::vector<int>& cpus) : n_(std::max(1,
 SpinPool::~SpinPool() {
     stop_.store(true, std::memory_order_release);
     gen_.fetch_add(1, std::memory_order_acq_rel);
+    gen_.notify_all();
     for (auto& t : th_) t.join();
 }
 
 void SpinPool::worker(int tid) {
     uint64_t seen = 0;
     for (;;) {
+        // spin ~50 us (the engine issues back-to-back jobs), then sleep in a
+        // futex wait so an idle draft does not steal host cores
         int spins = 0;
         while (gen_.load(std::memory_order_acquire) == seen) {
             if (++spins < 20000) {
                 _mm_pause();
             } else {
-                std::this_thread::yield();
+                sleepers_.fetch_add(1, std::memory_order_acq_rel);
+                gen_.wait(seen, std::memory_order_acquire);
+                sleepers_.fetch_sub(1, std::memory_order_acq_rel);
             }
         }
         seen = gen_.load(std::memory_order_acquire);
@@ -153,6 +158,7 @@ void SpinPool::run(const std::function<void(int, int)>& fn) {
     job_ = &fn;
     done_.store(0, std::memory_order_relaxed);
     gen_.fetch_add(1, std::memory_order_acq_rel);
+    if (sleepers_.load(std::memory_order_acquire) > 0) gen_.notify_all();
     fn(0, n_);
     while (done_.load(std::memory_order_acquire) != n_ - 1) _mm_pause();
 }

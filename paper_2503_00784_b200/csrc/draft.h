@@ -28,6 +28,7 @@ class SpinPool {
     std::vector<std::thread> th_;
     std::atomic<uint64_t> gen_{0};
     std::atomic<int> done_{0};
+    std::atomic<int> sleepers_{0};
     std::atomic<bool> stop_{false};
     const std::function<void(int, int)>* job_ = nullptr;
 };

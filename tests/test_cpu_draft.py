@@ -1,0 +1,41 @@
+"""The product's CPU draft model (AVX-512 BF16, host cores) vs the oracle."""
+import numpy as np
+import pytest
+
+from oracle.llama import OracleLlama
+from paper_2503_00784_b200 import Draft
+
+SHAPE = dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=4, head_dim=64, ffn_dim=640,
+             vocab=1024, rms_eps=1e-5, rope_theta=1e4)
+PLANT = dict(plant_seed=3, alpha=0.5, gain=1.0, emb_std=1.0)
+
+
+@pytest.fixture(scope="module")
+def draft(native):
+    import ctypes
+    try:
+        d = Draft(SHAPE, weight_seed=31, plant=PLANT, threads=4, max_seq=256)
+    except Exception as e:  # host without AVX-512 BF16: single native path
+        pytest.skip(str(e))
+    yield d
+    d.close()
+
+
+def test_draft_logits_match_oracle(draft):
+    orc = OracleLlama(SHAPE, weight_seed=31, plant=PLANT, max_seq=256, threads=4)
+    rng = np.random.default_rng(1)
+    ctx = rng.integers(0, SHAPE["vocab"], 50).tolist()
+    o = orc.forward(ctx)
+    for n in (1, 7, 30, 50):  # prefix reuse, branch forks, re-extension
+        g = draft.logits(ctx[:n])
+        rel = np.abs(g - o[n - 1]).max() / np.abs(o[n - 1]).max()
+        assert rel < 5e-3, (n, rel)
+    # fork: different continuation then back
+    g1 = draft.logits(ctx[:20] + [5, 6])
+    g2 = draft.logits(ctx[:25])
+    assert np.abs(g2 - o[24]).max() / np.abs(o[24]).max() < 5e-3
+    orc.close()
+
+
+def test_draft_time_token(draft):
+    assert draft.time_token(10) > 0.0
