@@ -169,6 +169,17 @@ int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n)
  * (bf16 bits in, fp32 out; n_out % 128 == 0, k % 64 == 0, w <= 256). */
 int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, float* Y);
 
+/* Debug: per-CTA globaltimer timeline (8 u64 per CTA: start, setup, first
+ * stage, last MMA issued, accumulator done, end, -, smid) of one launch of
+ * layer-0 GEMM `which` (0 qkv, 1 o, 2 gate/up, 3 down, 4 LM head). */
+int dd_debug_gemm_trace(dd_ctx* ctx, int which, int w, uint64_t* trace, int max_ctas,
+                        int* n_ctas);
+
+/* Debug: per-CTA stamps of every GEMM launch of one pass sequence (stride =
+ * 8 * ctas_per_launch u64 per launch). */
+int dd_debug_pass_trace(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_launch,
+                        int* ctas_per_launch);
+
 /* ------------------------------------------------------------ CPU draft */
 int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_plant_desc* plant,
                     int n_threads, const int* cpus, int n_cpus, dd_draft** out);

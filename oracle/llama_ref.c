@@ -324,11 +324,18 @@ static void matmul(const uint16_t* W, int rows, int k, const float* x, int w, fl
     par_range(rows, mm_range, &a);
 }
 
-static void rmsnorm_bf(const float* x, int d, float eps, float* h) {
+/* Deferred RMSNorm (mirrors the GPU pass): h = bf16(x * g) and the scale
+ * r = 1/sqrt(mean(x^2) + eps) is applied to the consuming GEMM's fp32 output,
+ * since W.(x*r*g) == r * (W.(x*g)).  Gains are 1. */
+static float rmsnorm_bf(const float* x, int d, float eps, float* h) {
     float ss = 0.0f;
     for (int i = 0; i < d; ++i) ss = fmaf(x[i], x[i], ss);
-    const float r = 1.0f / sqrtf(ss / (float)d + eps);
-    for (int i = 0; i < d; ++i) h[i] = bfr((x[i] * r) * 1.0f);
+    for (int i = 0; i < d; ++i) h[i] = bfr(x[i] * 1.0f);
+    return 1.0f / sqrtf(ss / (float)d + eps);
+}
+static void scale_rows(float* y, int w, int n, const float* r) {
+    for (int t = 0; t < w; ++t)
+        for (int i = 0; i < n; ++i) y[(size_t)t * n + i] *= r[t];
 }
 
 typedef struct {
@@ -385,15 +392,17 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
     float* o = (float*)malloc(sizeof(float) * (size_t)w * qd);
     float* y = (float*)malloc(sizeof(float) * (size_t)w * (2 * F > d ? 2 * F : d));
     float* a = (float*)malloc(sizeof(float) * (size_t)w * F);
+    float* rn = (float*)malloc(sizeof(float) * (size_t)w);
     for (int t = 0; t < w; ++t) {
         if (tokens[t] < 0 || tokens[t] >= V) return -2;
         for (int i = 0; i < d; ++i) x[(size_t)t * d + i] = bf2f(m->emb[(size_t)tokens[t] * d + i]);
-        rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+        rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
     }
     const float scale = (float)(1.0 / sqrt((double)hd));
     for (int l = 0; l < m->L; ++l) {
         const orc_layer* Ly = &m->layers[l];
         matmul(Ly->qkv, rows, d, h, w, qkv);
+        scale_rows(qkv, w, rows, rn);
         for (int t = 0; t < w; ++t) {
             const int pos = n0 + t;
             const float* cs = m->rope_cos + (size_t)pos * half;
@@ -424,9 +433,10 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
         matmul(Ly->o, d, qd, o, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
-            rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+            rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
         }
         matmul(Ly->gu, 2 * F, d, h, w, y);
+        scale_rows(y, w, 2 * F, rn);
         for (int t = 0; t < w; ++t)
             for (int f = 0; f < F; ++f) {
                 const float g = y[(size_t)t * 2 * F + f], u = y[(size_t)t * 2 * F + F + f];
@@ -436,14 +446,17 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
         matmul(Ly->dn, d, F, a, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
-            rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+            rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
         }
     }
     if (logits) {
-        if (last_only)
+        if (last_only) {
             matmul(m->head, V, d, h + (size_t)(w - 1) * d, 1, logits);
-        else
+            scale_rows(logits, 1, V, rn + (w - 1));
+        } else {
             matmul(m->head, V, d, h, w, logits);
+            scale_rows(logits, w, V, rn);
+        }
     }
     m->n_cached += w;
     free(x);
@@ -453,5 +466,6 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
     free(o);
     free(y);
     free(a);
+    free(rn);
     return 0;
 }

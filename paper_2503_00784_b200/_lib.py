@@ -91,6 +91,10 @@ SIGNATURES = {
     "dd_time_gemms": (C.c_int, [_vp, C.c_int, C.c_int, _f32p, C.POINTER(C.c_int)]),
     "dd_read_weights": (C.c_int, [_vp, C.c_int, C.c_int, _u16p, C.c_size_t]),
     "dd_test_gemm": (C.c_int, [_u16p, _u16p, C.c_int, C.c_int, C.c_int, _f32p]),
+    "dd_debug_pass_trace": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
+                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "dd_debug_gemm_trace": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.c_int,
+                                      C.POINTER(C.c_int)]),
     "dd_draft_create": (C.c_int, [C.POINTER(ModelDesc), C.c_uint64, C.POINTER(PlantDesc), C.c_int,
                                   C.POINTER(C.c_int), C.c_int, C.POINTER(_vp)]),
     "dd_draft_destroy": (None, [_vp]),

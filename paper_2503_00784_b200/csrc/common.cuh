@@ -61,6 +61,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -95,6 +98,28 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
+}
+
+// 1-D bulk copy global -> shared (contiguous bytes), completion on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// Pre-tiled weight layout: a [rows, cols] bf16 matrix (rows % 128 == 0,
+// cols % 64 == 0) is stored as [rows/128][cols/64] blocks of 16 KiB, each the
+// exact shared-memory image of a 128x64 K-major tile with the 128-byte
+// swizzle (16-byte chunk c of row r sits at chunk c ^ (r % 8)).  One pipeline
+// stage is then a single contiguous cp.async.bulk of 16 KiB.
+__host__ __device__ __forceinline__ size_t tiled_offset(size_t r, size_t c, size_t cols) {
+    const size_t tile = r >> 7, rr = r & 127, kb = c >> 6, kk = c & 63;
+    const size_t block = tile * (cols >> 6) + kb;
+    const size_t chunk = (kk >> 3) ^ (rr & 7);
+    return block * 8192 + rr * 64 + chunk * 8 + (kk & 7);  // in elements
 }
 
 // ---------------------------------------------------------------------------

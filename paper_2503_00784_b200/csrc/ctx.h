@@ -21,7 +21,7 @@ struct LayerW {
     __nv_bfloat16* o = nullptr;    // [d, q_dim]
     __nv_bfloat16* gu = nullptr;   // [2 ffn, d]  (gate rows, then up rows)
     __nv_bfloat16* dn = nullptr;   // [d, ffn]
-    CUtensorMap map_qkv, map_o, map_gu, map_d;
+    // all four stored pre-tiled (common.cuh tiled_offset) for 16 KiB bulk loads
 };
 
 constexpr int kPsRing = 4;
@@ -41,7 +41,6 @@ struct dd_ctx {
     __nv_bfloat16* head = nullptr;
     std::vector<dd::LayerW> layers;
     float* gain_ones = nullptr;
-    CUtensorMap map_head;
 
     float* x = nullptr;             // [256, d] fp32 residual stream
     __nv_bfloat16* h = nullptr;     // [256, d] normed GEMM input
@@ -50,6 +49,7 @@ struct dd_ctx {
     __nv_bfloat16* a = nullptr;     // [256, ffn] SwiGLU output
     float* ws = nullptr;            // split-K partials
     int* counters = nullptr;        // per-tile split arrival counters
+    float* ss = nullptr;            // [256][d/128] deferred-RMSNorm sum-of-squares partials
     float* logits = nullptr;        // [256, vocab]
     CUtensorMap map_h, map_o, map_a;
 

@@ -97,11 +97,13 @@ void matmul(SpinPool& pool, const uint16_t* W, int rows, int k, const uint16_t* 
     });
 }
 
-void rmsnorm_bf(const float* x, int d, float eps, uint16_t* h) {
+// deferred RMSNorm (same formulation as the GPU target and the oracle):
+// h = bf16(x * g), r applied to the consuming matmul's fp32 output
+float rmsnorm_bf(const float* x, int d, float eps, uint16_t* h) {
     float ss = 0.0f;
     for (int i = 0; i < d; ++i) ss = std::fmaf(x[i], x[i], ss);
-    const float r = 1.0f / std::sqrt(ss / static_cast<float>(d) + eps);
-    for (int i = 0; i < d; ++i) h[i] = f2bf(x[i] * r);
+    for (int i = 0; i < d; ++i) h[i] = f2bf(x[i]);
+    return 1.0f / std::sqrt(ss / static_cast<float>(d) + eps);
 }
 
 }  // namespace
@@ -255,10 +257,15 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     gu_.resize(W * 2 * F_);
     ab_.resize(W * F_);
     y_.resize(W * std::max(d_, 2 * F_));
+    std::vector<float> rn(W);
+    auto scale_rn = [&](float* y, int n) {
+        for (int t = 0; t < w; ++t)
+            for (int i = 0; i < n; ++i) y[static_cast<size_t>(t) * n + i] *= rn[t];
+    };
     for (int t = 0; t < w; ++t) {
         for (int i = 0; i < d_; ++i)
             x_[t * d_ + i] = bf2f(emb_[static_cast<size_t>(toks[t]) * d_ + i]);
-        rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+        rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
     }
     auto kvp = [&](int l, int kv, int h, int pos) {
         return &kv_[((((static_cast<size_t>(l) * 2 + kv) * Hkv_ + h) * max_seq_) + pos) * hd_];
@@ -267,6 +274,7 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     for (int l = 0; l < L_; ++l) {
         const DraftLayer& Ly = layers_[l];
         matmul(*pool_, Ly.qkv.data(), rows, d_, hb_.data(), w, qkv_.data());
+        scale_rn(qkv_.data(), rows);
         for (int t = 0; t < w; ++t) {
             const int pos = n0 + t;
             const float* cs = &rope_cos_[static_cast<size_t>(pos) * half];
@@ -321,9 +329,10 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
         matmul(*pool_, Ly.o.data(), d_, qd, ob_.data(), w, y_.data());
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
-            rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+            rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
         }
         matmul(*pool_, Ly.gu.data(), 2 * F_, d_, hb_.data(), w, gu_.data());
+        scale_rn(gu_.data(), 2 * F_);
         for (int t = 0; t < w; ++t)
             for (int f = 0; f < F_; ++f) {
                 const float g = gu_[t * 2 * F_ + f], u = gu_[t * 2 * F_ + F_ + f];
@@ -332,10 +341,11 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
         matmul(*pool_, Ly.dn.data(), d_, F_, ab_.data(), w, y_.data());
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
-            rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
+            rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
         }
     }
     matmul(*pool_, head_.data(), V_, d_, &hb_[(W - 1) * d_], 1, logits_last);
+    for (int i = 0; i < V_; ++i) logits_last[i] *= rn[W - 1];
     tokens_.insert(tokens_.end(), toks, toks + w);
 }
 

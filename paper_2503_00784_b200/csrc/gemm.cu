@@ -6,25 +6,34 @@
 //
 //   D[128 weight rows, NT tokens] (+)= Wtile[128, K] . X[NT, K]^T
 //
-// - A operand: a 128-row weight tile, K-major, fetched by TMA in 64-column
-//   (128-byte) boxes with 128B swizzle and an evict-first L2 policy.
-// - B operand: the NT (multiple of 16) activation rows, same layout, fetched
-//   in 16-row boxes (evict-last: every CTA re-reads them from L2).
-// - One elected thread issues tcgen05.mma (M=128, N=NT, K=16) into a TMEM
-//   accumulator; tcgen05.commit releases each smem stage back to the TMA
-//   producer through an mbarrier ring.
-// - Split-K across blockIdx.y so that tiles x splits fills the 148 SMs.  The
-//   S split CTAs of one tile form a thread-block cluster (1 x S): each stages
-//   its fp32 accumulator in its own shared memory, and after a cluster barrier
-//   CTA rank r reduces the tokens t = r (mod S) by reading all S partials over
-//   DSMEM in rank order (deterministic, and a token's result does not depend
-//   on the pass width).  The fused epilogue (RoPE + paged-KV append, residual
-//   add, SwiGLU, logits store) is applied right there — no global workspace.
+// Persistent, warp-specialised, stream-K:
+// - One CTA per SM.  The (tile, k-block) space of the matrix is cut into P
+//   equal contiguous ranges, one per CTA, so every SM streams the same number
+//   of weight bytes with no waves and no tail.  A range crossing a tile
+//   boundary yields one "segment" per tile it touches.
+// - Weights are stored pre-tiled and pre-swizzled in HBM (common.cuh
+//   tiled_offset): a CTA's range is ONE contiguous run of 16 KiB blocks, each
+//   loaded by a single cp.async.bulk into the SW128 K-major image UMMA
+//   expects, with an evict-first policy and an L2 prefetch running ahead of
+//   the smem ring.  Activations (B) come through a TMA tensor map (L2-resident).
+// - warp 0: producer; warp 1: single-thread tcgen05.mma issuer (M=128,
+//   N=NT, K=16) into one of two TMEM accumulators; warps 2-5: epilogue
+//   (tcgen05.ld -> registers), overlapping the next segment's streaming.
+// - Segment reduction: a tile covered by one segment is finished from
+//   shared memory directly; otherwise each segment writes fp32 partials and
+//   the last-arriving segment sums them in segment order (deterministic; the
+//   partition depends only on the matrix shape, never on W, so a token's
+//   result is independent of the pass width) and applies the fused epilogue
+//   (RoPE + paged-KV append, residual add, SwiGLU, logits store).
+// - Programmatic dependent launch: the first ring stages of weights are
+//   requested before griddepcontrol.wait, so a GEMM starts streaming while
+//   the previous kernel of the pass drains.
 #include "common.cuh"
 #include "gemm.h"
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 namespace dd {
 
@@ -33,178 +42,389 @@ namespace {
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;
 constexpr uint32_t kABytes = kBlockM * kBlockK * 2;  // 16 KiB
-constexpr int kTmemCols = 256;
-constexpr int kMaxSplits = 16;  // cluster size (non-portable above 8)
+constexpr int kThreads = 192;                         // 6 warps
+constexpr int kEpiThreads = 128;                      // warps 2..5
+constexpr int kChunk = 16;                            // tokens per staging chunk
+constexpr int kMaxSeg = 16;                           // stream-K segments per tile (host-checked)
 
-__global__ void __launch_bounds__(128, 1)
-    gemm_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
-                       const __grid_constant__ CUtensorMap map_x, GemmArgs a) {
+
+__host__ __device__ inline long sk_begin(int c, long T, int P) {
+    return static_cast<long>(c) * T / P;
+}
+// CTA whose range contains global k-block g
+__host__ __device__ inline int sk_owner(long g, long T, int P) {
+    int c = static_cast<int>(g * P / T);
+    while (c + 1 < P && sk_begin(c + 1, T, P) <= g) ++c;
+    while (c > 0 && sk_begin(c, T, P) > g) --c;
+    return c;
+}
+
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Apply the fused epilogue to tokens [t0, t0+tn) of tile `tile` whose reduced
+// fp32 values are staged in red[t][128].
+__device__ void apply_epilogue(const GemmArgs& a, int tile, int t0, int tn, const float* red,
+                               int tid, float* part /* [4][kChunk] scratch */) {
+    const GemmEpiParams& e = a.epi;
+    const int m0 = tile * kBlockM;
+    if (e.kind == kEpiStore || e.kind == kEpiResidual) {
+        // batch every load before any store (red is a generic pointer into
+        // shared memory, so interleaving would serialise on aliasing)
+        float v[kChunk], x[kChunk];
+        float* dst = e.out + static_cast<size_t>(t0) * a.n_out + m0 + tid;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t) v[t] = t < tn ? red[t * 128 + tid] : 0.0f;
+        if (e.kind == kEpiResidual) {
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t)
+                x[t] = t < tn ? dst[static_cast<size_t>(t) * a.n_out] : 0.0f;
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) v[t] = __fadd_rn(x[t], v[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < tn) dst[static_cast<size_t>(t) * a.n_out] = v[t];
+        if (e.kind == kEpiResidual && e.u_out != nullptr) {
+            // deferred RMSNorm producer: u = bf16(x * g) and per-token sum of
+            // squares of this tile's 128 rows (fixed shuffle / smem tree)
+            const float g = e.gain[m0 + tid];
+            __nv_bfloat16* u = e.u_out + static_cast<size_t>(t0) * a.n_out + m0 + tid;
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                if (t < tn) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(v[t], g));
+                float sq = __fmul_rn(v[t], v[t]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+                if ((tid & 31) == 0) part[(tid >> 5) * kChunk + t] = sq;
+            }
+            epi_bar();
+            if (tid < tn) {
+                const float tot = __fadd_rn(__fadd_rn(part[tid], part[kChunk + tid]),
+                                            __fadd_rn(part[2 * kChunk + tid], part[3 * kChunk + tid]));
+                e.ss_out[static_cast<size_t>(t0 + tid) * a.tiles + tile] = tot;
+            }
+        }
+    } else if (e.kind == kEpiSwiGLU) {
+        const int ffn = a.n_out / 2;
+        for (int idx = tid; idx < tn * 64; idx += kEpiThreads) {
+            const int t = idx >> 6, f = idx & 63;
+            const float g = red[t * 128 + f], u = red[t * 128 + 64 + f];
+            const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+            e.out_bf[static_cast<size_t>(t0 + t) * ffn + tile * 64 + f] =
+                __float2bfloat16_rn(__fmul_rn(silu, u));
+        }
+    } else {  // kEpiQkvRope
+        const ModelDims& md = e.m;
+        const int hd = md.head_dim, half = hd / 2;
+        const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+        const int n_cached = e.ps->n_cached;
+        if (m0 < q_dim + kv_dim) {
+            for (int idx = tid; idx < tn * 64; idx += kEpiThreads) {
+                const int t = idx >> 6, pr = idx & 63;
+                const int hl = pr / half, i = pr % half;
+                const int r0 = hl * hd + i;
+                const float av = red[t * 128 + r0], bv = red[t * 128 + r0 + half];
+                const int pos = n_cached + t0 + t;
+                const float c = e.rope_cos[static_cast<size_t>(pos) * half + i];
+                const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
+                const float lo = __fmaf_rn(av, c, -__fmul_rn(bv, sn));
+                const float hi = __fmaf_rn(bv, c, __fmul_rn(av, sn));
+                const int grow = m0 + r0;
+                if (grow < q_dim) {
+                    float* qd = e.q_out + static_cast<size_t>(t0 + t) * q_dim + grow;
+                    qd[0] = lo;
+                    qd[half] = hi;
+                } else {
+                    const int kh = (grow - q_dim) / hd;
+                    const int page = e.page_table[pos / e.page_size], slot = pos % e.page_size;
+                    __nv_bfloat16* kd =
+                        e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 0, kh, slot) + i;
+                    kd[0] = __float2bfloat16_rn(lo);
+                    kd[half] = __float2bfloat16_rn(hi);
+                }
+            }
+        } else {
+            for (int idx = tid; idx < tn * 128; idx += kEpiThreads) {
+                const int t = idx >> 7, r = idx & 127;
+                const int pos = n_cached + t0 + t;
+                const int ve = m0 + r - q_dim - kv_dim;
+                const int page = e.page_table[pos / e.page_size], slot = pos % e.page_size;
+                e.kv_pool[kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd] =
+                    __float2bfloat16_rn(red[t * 128 + r]);
+            }
+        }
+    }
+}
+
+// Deferred-RMSNorm consumer side: scale the staged accumulator rows of
+// tokens [t0, t0+tn) by r[t] = 1/sqrt(sum_tiles(ss_in[t][:]) / d + eps).
+__device__ void scale_by_rnorm(const GemmArgs& a, int t0, int tn, float* red, int tid,
+                               float* s_r) {
+    const GemmEpiParams& e = a.epi;
+    if (e.ss_in == nullptr) return;
+    if (tid < tn) {
+        const float* ss = e.ss_in + static_cast<size_t>(t0 + tid) * e.ss_tiles;
+        float acc = 0.0f;
+        for (int i = 0; i < e.ss_tiles; ++i) acc = __fadd_rn(acc, __ldcg(ss + i));
+        s_r[tid] = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(e.norm_d)), e.eps));
+    }
+    epi_bar();
+    for (int t = 0; t < tn; ++t) red[t * 128 + tid] = __fmul_rn(red[t * 128 + tid], s_r[t]);
+    epi_bar();
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    gemm_sk_kernel(const __nv_bfloat16* __restrict__ w_tiled,
+                   const __grid_constant__ CUtensorMap map_x, GemmArgs a) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * kBlockM;
-    const int split = blockIdx.y;
-    const int kb0 = split * a.kb_per_split;
-    const int nkb = min(a.kb_per_split, a.k / kBlockK - kb0);
+    const int P = gridDim.x, c = blockIdx.x;
+    const long T = static_cast<long>(a.tiles) * a.nkb;
+    const long g0 = sk_begin(c, T, P), g1 = sk_begin(c + 1, T, P);
+    const int len = static_cast<int>(g1 - g0);
     const uint32_t b_bytes = static_cast<uint32_t>(a.nt) * 128u;
     const uint32_t stage_bytes = kABytes + b_bytes;
     const int stages = a.stages;
 
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * stage_bytes);
+    float* red = reinterpret_cast<float*>(smem + stages * stage_bytes);  // [kChunk][128]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
     uint64_t* empty = full + stages;
-    uint64_t* done = empty + stages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + stages;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ int s_last;
+    __shared__ float s_r[kChunk];
+    __shared__ float s_part[4 * kChunk];
+
+    unsigned long long* tr =
+        a.trace ? a.trace + 8 * static_cast<size_t>(blockIdx.x) : nullptr;
+    auto stamp = [&](int i) {
+        if (tr) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tr[i] = t;
+        }
+    };
 
     if (threadIdx.x == 0) {
-        tma_prefetch_desc(&map_w);
+        stamp(0);
+        if (tr) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            tr[7] = smid;
+        }
         tma_prefetch_desc(&map_x);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiThreads);
+        }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == 1) {
+        const uint32_t cols = static_cast<uint32_t>(a.tmem_buf * 2);
+        if (cols <= 32) tmem_alloc<32>(tmem_slot);
+        else if (cols <= 64) tmem_alloc<64>(tmem_slot);
+        else if (cols <= 128) tmem_alloc<128>(tmem_slot);
+        else if (cols <= 256) tmem_alloc<256>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_launch();  // the next kernel may start prefetching its weights
+    if (threadIdx.x == 0) stamp(1);
 
-    if (threadIdx.x == 0) {
-        // ---- TMA producer ----
-        const uint64_t pol_w = policy_evict_first();
-        const uint64_t pol_x = policy_evict_last();
-        const int nbox = a.nt >> 4;
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % stages;
-            const uint32_t use = static_cast<uint32_t>(kb / stages);
-            mbar_wait(&empty[s], (use & 1u) ^ 1u);
-            uint8_t* sa = smem + s * stage_bytes;
-            uint8_t* sb = sa + kABytes;
-            mbar_arrive_expect_tx(&full[s], stage_bytes);
-            const int kc = (kb0 + kb) * kBlockK;
-            tma_load_2d(sa, &map_w, &full[s], kc, m0, pol_w);
-            for (int r = 0; r < nbox; ++r)
-                tma_load_2d(sb + r * 2048, &map_x, &full[s], kc, r * 16, pol_x);
+    // first / last tile touched by this CTA
+    const int tile_lo = len > 0 ? static_cast<int>(g0 / a.nkb) : 0;
+    const int tile_hi = len > 0 ? static_cast<int>((g1 - 1) / a.nkb) : -1;
+
+    if (warp == 0) {
+        if (lane == 0 && len > 0) {
+            // ---------------- producer ----------------
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            const int nbox = a.nt >> 4;
+            const int pre = min(stages, len);
+            const int kPrefetch = a.prefetch;
+            // timing experiment only (DD_GEMM_INTERLEAVE): lockstep-sequential addresses
+            auto blk = [&](int i) -> const __nv_bfloat16* {
+                if (a.interleave) {
+                    const long pidx = static_cast<long>(i) * P + c;
+                    return w_tiled + (pidx < T ? pidx : (g0 + i)) * 8192;
+                }
+                return w_tiled + (g0 + i) * 8192;
+            };
+            for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
+                mbar_arrive_expect_tx(&full[i], stage_bytes);
+                bulk_load(smem + i * stage_bytes, blk(i), kABytes, &full[i], pol_w);
+            }
+            for (int i = pre; i < min(len, pre + kPrefetch); ++i)
+                prefetch_l2(w_tiled + (g0 + i) * 8192, kABytes);
+            griddep_wait();  // activations are produced by the previous kernel
+            stamp(2);
+            for (int i = 0; i < len; ++i) {
+                const int s = i % stages;
+                const uint32_t use = static_cast<uint32_t>(i / stages);
+                uint8_t* sa = smem + s * stage_bytes;
+                if (i >= pre) {
+                    mbar_wait(&empty[s], (use & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], stage_bytes);
+                    bulk_load(sa, blk(i), kABytes, &full[s], pol_w);
+
+                }
+                const int kc = static_cast<int>((g0 + i) % a.nkb) * kBlockK;
+                for (int r = 0; r < nbox; ++r)
+                    tma_load_2d(sa + kABytes + r * 2048, &map_x, &full[s], kc, r * 16, pol_x);
+            }
         }
-    } else if (threadIdx.x == 32) {
-        // ---- MMA issuer (single thread) ----
-        const uint32_t idesc = idesc_bf16_f32(kBlockM, a.nt);
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % stages;
-            const uint32_t use = static_cast<uint32_t>(kb / stages);
-            mbar_wait(&full[s], use & 1u);
+    } else if (warp == 1) {
+        if (lane == 0 && len > 0) {
+            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = idesc_bf16_f32(kBlockM, a.nt);
+            int i = 0;
+            for (int tile = tile_lo, u = 0; tile <= tile_hi; ++tile, ++u) {
+                const long lo = max(g0, static_cast<long>(tile) * a.nkb);
+                const long hi = min(g1, static_cast<long>(tile + 1) * a.nkb);
+                const int b = u & 1;
+                if (u >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>(((u >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t acc = tmem + static_cast<uint32_t>(b * a.tmem_buf);
+                for (long g = lo; g < hi; ++g, ++i) {
+                    const int s = i % stages;
+                    const uint32_t use = static_cast<uint32_t>(i / stages);
+                    mbar_wait(&full[s], use & 1u);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * stage_bytes);
+                    const uint64_t adesc = sw128_kmajor_desc(sa);
+                    const uint64_t bdesc = sw128_kmajor_desc(sa + kABytes);
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                  (g != lo || k != 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[b]);
+            }
+            stamp(3);
+        }
+    } else {
+        // ---------------- epilogue warps 2..5 ----------------
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;
+        const int tid = threadIdx.x - 64;  // 0..127
+        for (int tile = tile_lo, u = 0; tile <= tile_hi; ++tile, ++u) {
+            const int first = sk_owner(static_cast<long>(tile) * a.nkb, T, P);
+            const int last = sk_owner(static_cast<long>(tile + 1) * a.nkb - 1, T, P);
+            const int nseg = last - first + 1, seg = c - first;
+            const int b = u & 1;
+            mbar_wait(&tfull[b], static_cast<uint32_t>((u >> 1) & 1));
+            __syncwarp();
             tc_fence_after();
-            const uint32_t sa = smem_u32(smem + s * stage_bytes);
-            const uint64_t adesc = sw128_kmajor_desc(sa);
-            const uint64_t bdesc = sw128_kmajor_desc(sa + kABytes);
-#pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k) {
-                // +32 bytes along K inside the 128B swizzle atom = +2 in addr>>4
-                umma_bf16(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-            }
-            umma_commit(&empty[s]);
-        }
-        umma_commit(done);
-    }
-
-    // ---- epilogue: cluster (DSMEM) split-K reduction + fused epilogue ----
-    __syncwarp();
-    mbar_wait(done, 0);
-    __syncwarp();
-    tc_fence_after();
-    const int tid = threadIdx.x;
-    const uint32_t S = static_cast<uint32_t>(a.splits);
-    const uint32_t rank = S > 1 ? cluster_ctarank() : 0u;
-    float* red = reinterpret_cast<float*>(smem);  // [kChunk][128] staging, reuses the ring
-    const uint32_t red_addr = smem_u32(red);
-    constexpr int kChunk = 64;
-    const uint32_t t_lane = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    const GemmEpiParams& e = a.epi;
-    // sum over the cluster's partials of element (t, r) of the current chunk
-    auto csum = [&](int t, int r) -> float {
-        if (S == 1) return red[t * 128 + r];
-        const uint32_t off = static_cast<uint32_t>((t * 128 + r) * 4);
-        // issue all remote loads first (independent), then add in rank order
-        float v[kMaxSplits];
-#pragma unroll
-        for (uint32_t s2 = 0; s2 < kMaxSplits; ++s2)
-            if (s2 < S) v[s2] = ld_dsmem_f32(dsmem_addr(red_addr + off, s2));
-        float acc = 0.0f;
-#pragma unroll
-        for (uint32_t s2 = 0; s2 < kMaxSplits; ++s2)
-            if (s2 < S) acc = __fadd_rn(acc, v[s2]);
-        return acc;
-    };
-    for (int t0 = 0; t0 < a.w; t0 += kChunk) {
-        const int tn = min(kChunk, a.w - t0);
-        for (int c0 = 0; c0 < tn; c0 += 16) {
-            float v[16];
-            tmem_ld16(t_lane + t0 + c0, v);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < tn) red[(c0 + j) * 128 + warp * 32 + lane] = v[j];
-        }
-        if (S > 1) cluster_sync(); else __syncthreads();
-        for (int t = static_cast<int>(rank); t < tn; t += static_cast<int>(S)) {
-            const int tg = t0 + t;  // token index in the pass
-            if (e.kind == kEpiStore) {
-                e.out[static_cast<size_t>(tg) * a.n_out + m0 + tid] = csum(t, tid);
-            } else if (e.kind == kEpiResidual) {
-                float* x = e.out + static_cast<size_t>(tg) * a.n_out + m0 + tid;
-                *x = __fadd_rn(*x, csum(t, tid));
-            } else if (e.kind == kEpiSwiGLU) {
-                if (tid < 64) {
-                    const float g = csum(t, tid), u = csum(t, 64 + tid);
-                    const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-                    e.out_bf[static_cast<size_t>(tg) * (a.n_out / 2) + blockIdx.x * 64 + tid] =
-                        __float2bfloat16_rn(__fmul_rn(silu, u));
-                }
-            } else {  // kEpiQkvRope
-                const ModelDims& md = e.m;
-                const int hd = md.head_dim, half = hd / 2;
-                const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
-                const int pos = e.ps->n_cached + tg;
-                const int page = e.page_table[pos / e.page_size], slot = pos % e.page_size;
-                if (m0 < q_dim + kv_dim) {
-                    if (tid < 64) {
-                        const int hl = tid / half, i = tid % half;
-                        const int r0 = hl * hd + i;
-                        const float av = csum(t, r0), bv = csum(t, r0 + half);
-                        const float c = e.rope_cos[static_cast<size_t>(pos) * half + i];
-                        const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
-                        const float lo = __fmaf_rn(av, c, -__fmul_rn(bv, sn));
-                        const float hi = __fmaf_rn(bv, c, __fmul_rn(av, sn));
-                        const int grow = m0 + r0;
-                        if (grow < q_dim) {
-                            float* qd = e.q_out + static_cast<size_t>(tg) * q_dim + grow;
-                            qd[0] = lo;
-                            qd[half] = hi;
-                        } else {
-                            const int kh = (grow - q_dim) / hd;
-                            __nv_bfloat16* kd =
-                                e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 0, kh, slot) + i;
-                            kd[0] = __float2bfloat16_rn(lo);
-                            kd[half] = __float2bfloat16_rn(hi);
-                        }
+            const uint32_t t_lane =
+                tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * a.tmem_buf);
+            if (nseg == 1) {
+                for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                    const int tn = min(kChunk, a.w - t0);
+                    float v[16];
+                    tmem_ld16(t_lane + t0, v);
+                    if (t0 + kChunk >= a.w) {  // accumulator fully read
+                        tc_fence_before();
+                        mbar_arrive(&tempty[b]);
                     }
-                } else {
-                    const int ve = m0 + tid - q_dim - kv_dim;
-                    e.kv_pool[kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) +
-                              ve % hd] = __float2bfloat16_rn(csum(t, tid));
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < tn) red[j * 128 + row] = v[j];
+                    epi_bar();
+                    scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                    apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                    epi_bar();
+                }
+            } else {
+                float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * a.w * 128;
+                for (int t0 = 0; t0 < a.w; t0 += 16) {
+                    float v[16];
+                    tmem_ld16(t_lane + t0, v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (t0 + j < a.w) part[static_cast<size_t>(t0 + j) * 128 + row] = v[j];
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[b]);
+                __threadfence();
+                epi_bar();
+                if (tid == 0) {
+                    const int prev = atomicAdd(&a.epi.counters[tile], 1);
+                    s_last = (prev == nseg - 1);
+                }
+                epi_bar();
+                if (s_last) {
+                    __threadfence();
+                    const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * a.w * 128;
+                    const size_t seg_stride = static_cast<size_t>(a.w) * 128;
+                    for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                        const int tn = min(kChunk, a.w - t0);
+                        // items = (token, 4-row group); every segment's float4 of an
+                        // item is requested before any add (latency paid once)
+                        for (int it = tid; it < tn * 32; it += kEpiThreads) {
+                            const int t = it >> 5, r4 = (it & 31) * 4;
+                            const float4* src = reinterpret_cast<const float4*>(
+                                base + static_cast<size_t>(t0 + t) * 128 + r4);
+                            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int s0 = 0; s0 < nseg; s0 += 8) {  // 8 segments in flight
+                                float4 v[8];
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if (s0 + j < nseg)
+                                        v[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if (s0 + j < nseg) {
+                                        acc.x = __fadd_rn(acc.x, v[j].x);
+                                        acc.y = __fadd_rn(acc.y, v[j].y);
+                                        acc.z = __fadd_rn(acc.z, v[j].z);
+                                        acc.w = __fadd_rn(acc.w, v[j].w);
+                                    }
+                            }
+                            *reinterpret_cast<float4*>(red + t * 128 + r4) = acc;
+                        }
+                        epi_bar();
+                        scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                        apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                        epi_bar();
+                    }
+                    if (tid == 0) a.epi.counters[tile] = 0;
                 }
             }
         }
-        if (S > 1) cluster_sync(); else __syncthreads();
+        if (tid == 0) stamp(4);
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+    if (warp == 1) {
+        const uint32_t cols = static_cast<uint32_t>(a.tmem_buf * 2);
+        if (cols <= 32) tmem_dealloc<32>(tmem);
+        else if (cols <= 64) tmem_dealloc<64>(tmem);
+        else if (cols <= 128) tmem_dealloc<128>(tmem);
+        else if (cols <= 256) tmem_dealloc<256>(tmem);
+        else tmem_dealloc<512>(tmem);
+    }
+    if (threadIdx.x == 0) stamp(5);
 #endif
 }
 
@@ -239,81 +459,87 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
 }
 
 GemmPlan plan_gemm(int n_out, int k, int nt) {
+    static const int env_stages = getenv("DD_GEMM_STAGES") ? atoi(getenv("DD_GEMM_STAGES")) : 0;
+    static const int env_ctas = getenv("DD_GEMM_CTAS") ? atoi(getenv("DD_GEMM_CTAS")) : 0;
     GemmPlan p{};
-    const int tiles = n_out / kBlockM;
-    const int nkb = k / kBlockK;
+    p.tiles = n_out / kBlockM;
+    p.nkb = k / kBlockK;
+    const long T = static_cast<long>(p.tiles) * p.nkb;
     const uint32_t stage_bytes = kABytes + static_cast<uint32_t>(nt) * 128u;
-    // two CTAs per SM when the ring fits in ~104 KiB, else one
-    int stages = static_cast<int>(104u * 1024u / stage_bytes);
-    int ctas_per_sm = 2;
-    if (stages < 4) {
-        stages = std::min(8, static_cast<int>(220u * 1024u / stage_bytes));
-        ctas_per_sm = 1;
+    const uint32_t fixed = kChunk * 128 * 4 + 64 * 8 + 1024 + 64;
+    const uint32_t budget = 110u * 1024u;
+    int stages = static_cast<int>((budget - fixed) / stage_bytes);
+    int per_sm = 2;  // two persistent CTAs per SM when the ring fits in ~110 KiB
+    if (stages < 3) {
+        stages = static_cast<int>((220u * 1024u - fixed) / stage_bytes);
+        per_sm = 1;
     }
-    stages = std::min(stages, 8);
-    // The split count depends only on the GEMM shape (never on nt), so a token's
-    // fp32 reduction order is identical whatever the pass width: greedy outputs
-    // do not depend on how tokens are batched into passes.
-    const int slots = kNumSMs * 2;
-    // choose split-K maximising wave efficiency, keeping >= 6 k-blocks per CTA
-    int best_s = 1;
-    double best_eff = -1.0;
-    for (int s = 1; s <= kMaxSplits; ++s) {
-        const int kbps = (nkb + s - 1) / s;
-        if (kbps < 6 && s > 1) break;
-        const int real_s = (nkb + kbps - 1) / kbps;
-        const int ctas = tiles * real_s;
-        const int waves = (ctas + slots - 1) / slots;
-        double eff = static_cast<double>(ctas) / (waves * slots);
-        // mild preference for fewer waves (prologue/epilogue cost per CTA)
-        eff -= 0.004 * waves;
-        if (eff > best_eff + 1e-9) {
-            best_eff = eff;
-            best_s = real_s;
-        }
-    }
-    (void)ctas_per_sm;
-    p.kb_per_split = (nkb + best_s - 1) / best_s;
-    p.splits = (nkb + p.kb_per_split - 1) / p.kb_per_split;
+    stages = std::max(2, std::min(stages, 5));
+    if (env_stages > 0) stages = env_stages;
     p.stages = stages;
-    p.smem_bytes = static_cast<int>(stages * stage_bytes + (2 * stages + 1) * 8 + 16 + 1024);
-    p.tiles = tiles;
+    p.smem_bytes = static_cast<int>(stages * stage_bytes + fixed);
+    int buf = 32;
+    while (buf < nt) buf <<= 1;
+    p.tmem_cols = 2 * buf;
+    auto segs = [&](int ctas) {
+        int ms = 1;
+        for (int t = 0; t < p.tiles; ++t) {
+            const int f = sk_owner(static_cast<long>(t) * p.nkb, T, ctas);
+            const int l = sk_owner(static_cast<long>(t + 1) * p.nkb - 1, T, ctas);
+            ms = std::max(ms, l - f + 1);
+        }
+        return ms;
+    };
+    p.ctas = static_cast<int>(std::min<long>(env_ctas > 0 ? env_ctas : kNumSMs * per_sm, T));
+    while (segs(p.ctas) > kMaxSeg) p.ctas = std::max(1, p.ctas * 3 / 4);
+    p.max_seg = segs(p.ctas);
     return p;
 }
 
-cudaError_t launch_gemm(const CUtensorMap* map_w, const CUtensorMap* map_x, int n_out, int k,
+size_t gemm_ws_floats(const GemmPlan& p, int w) {
+    return static_cast<size_t>(p.tiles) * p.max_seg * static_cast<size_t>(w) * 128;
+}
+
+static unsigned long long* g_trace = nullptr;
+void gemm_set_trace(unsigned long long* buf) { g_trace = buf; }
+
+cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, int n_out, int k,
                         int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                         cudaStream_t stream) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              220 * 1024);
-        cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
-    GemmArgs a;
+    GemmArgs a{};
     a.n_out = n_out;
     a.k = k;
     a.w = w;
     a.nt = nt;
-    a.kb_per_split = plan.kb_per_split;
-    a.splits = plan.splits;
+    a.tiles = plan.tiles;
+    a.nkb = plan.nkb;
     a.stages = plan.stages;
+    a.max_seg = plan.max_seg;
+    a.tmem_buf = plan.tmem_cols / 2;
     a.ws = ws;
     a.epi = epi;
+    a.trace = g_trace;
+    static const int env_pf = getenv("DD_GEMM_PREFETCH") ? atoi(getenv("DD_GEMM_PREFETCH")) : 0;
+    a.prefetch = env_pf;
+    static const int env_il = getenv("DD_GEMM_INTERLEAVE") ? atoi(getenv("DD_GEMM_INTERLEAVE")) : 0;
+    a.interleave = env_il;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(plan.tiles, plan.splits, 1);
-    cfg.blockDim = dim3(128, 1, 1);
+    cfg.gridDim = dim3(plan.ctas, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = plan.smem_bytes;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = plan.splits;
-    at[0].val.clusterDim.z = 1;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_skinny_kernel, *map_w, *map_x, a);
+    return cudaLaunchKernelEx(&cfg, gemm_sk_kernel, w_tiled, *map_x, a);
 }
 
 }  // namespace dd

@@ -1,4 +1,4 @@
-// Host interface of the skinny tcgen05 GEMM (see gemm.cu).
+// Host interface of the skinny tcgen05 weight-streaming GEMM (see gemm.cu).
 #pragma once
 
 #include <cuda.h>
@@ -9,8 +9,7 @@
 
 namespace dd {
 
-// Epilogue applied by the last-arriving CTA of each 128-row tile after it has
-// reduced the split-K partials in split order (deterministic).
+// Epilogue applied once per 128-row tile to the fully reduced fp32 result.
 enum GemmEpilogue {
     kEpiStore = 0,     // out[t][row] = y                      (LM-head logits, tests)
     kEpiResidual = 1,  // out[t][row] += y                     (o-proj, down-proj)
@@ -20,7 +19,7 @@ enum GemmEpilogue {
 
 struct GemmEpiParams {
     int kind;
-    int* counters;          // [tiles] zero-initialised; reset by the last CTA
+    int* counters;          // [tiles] zero-initialised; reset by the last segment
     float* out;             // kEpiStore / kEpiResidual: [w][n_out]
     __nv_bfloat16* out_bf;  // kEpiSwiGLU: [w][n_out / 2]
     const PassState* ps;    // kEpiQkvRope
@@ -31,25 +30,43 @@ struct GemmEpiParams {
     const int32_t* page_table;
     int page_size, layer;
     ModelDims m;
+    // Deferred RMSNorm.  W.(x*r*g) == r * (W.(x*g)) with r = rsqrt(mean(x^2)+eps),
+    // so a residual-producing GEMM writes u = bf16(x*g) and, per token, the sum of
+    // squares of its 128 updated rows (ss_out[t][tile]); the consuming GEMM sums
+    // those partials in tile order, forms r per token and scales its fp32
+    // accumulator before its own epilogue.  No normalisation kernel or pass.
+    __nv_bfloat16* u_out;  // kEpiResidual: [w][n_out] bf16(x * gain), or nullptr
+    const float* gain;     // [n_out] RMSNorm gain
+    float* ss_out;         // kEpiResidual: [w][tiles]
+    const float* ss_in;    // consumer: [w][ss_tiles] partials, or nullptr (no scale)
+    int ss_tiles;
+    float eps;
+    int norm_d;            // d of the normalised row
 };
 
 struct GemmArgs {
-    int n_out;         // weight rows (output features), multiple of 128
-    int k;             // reduction length, multiple of 64
-    int w;             // valid tokens (columns stored)
-    int nt;            // padded token count: multiple of 16, <= 256
-    int kb_per_split;  // 64-wide k-blocks per split
-    int splits;
-    int stages;        // smem ring depth
-    float* ws;         // [splits][w][n_out] fp32 partial sums
+    int n_out;      // weight rows (output features), multiple of 128
+    int k;          // reduction length, multiple of 64
+    int w;          // valid tokens
+    int nt;         // padded token count: multiple of 16, <= 256
+    int tiles;      // n_out / 128
+    int nkb;        // k / 64
+    int stages;     // smem ring depth
+    int max_seg;    // max stream-K segments per tile (workspace stride)
+    int tmem_buf;   // TMEM columns per accumulator buffer (2 buffers)
+    int prefetch;   // L2 prefetch distance in k-blocks beyond the ring
+    int interleave; // timing experiment: lockstep-sequential weight addresses
+    float* ws;      // [tiles][max_seg][w][128] fp32 segment partials
     GemmEpiParams epi;
+    unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA, or nullptr
 };
 
 struct GemmPlan {
-    int tiles;
-    int splits;
-    int kb_per_split;
+    int tiles, nkb;
+    int ctas;        // persistent CTAs (one per SM)
     int stages;
+    int max_seg;
+    int tmem_cols;   // allocation (2 buffers)
     int smem_bytes;
 };
 
@@ -59,7 +76,16 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
 
 GemmPlan plan_gemm(int n_out, int k, int nt);
 
-cudaError_t launch_gemm(const CUtensorMap* map_w, const CUtensorMap* map_x, int n_out, int k,
+// workspace floats needed by a plan at width w
+size_t gemm_ws_floats(const GemmPlan& p, int w);
+
+// debug seam: per-CTA timeline of one launch (see dd_debug_gemm_trace)
+void gemm_set_trace(unsigned long long* buf);
+
+// w_tiled: weights in the pre-tiled layout of common.cuh (tiled_offset).
+// Launched with programmatic dependent launch: the kernel streams its first
+// weight stages before waiting on the previous kernel in the stream.
+cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, int n_out, int k,
                         int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                         cudaStream_t stream);
 

@@ -12,17 +12,38 @@
 
 namespace dd {
 
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Small kernels of the pass are launched normally (they start once the
+// preceding GEMM has completed) but trigger launch_dependents immediately, so
+// the following weight-streaming GEMM (launched with programmatic dependent
+// launch) becomes resident and fetches its first weight stages while they run.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+    kernel<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------ weights
-__global__ void init_matrix_kernel(__nv_bfloat16* dst, uint64_t n, uint64_t seed, float amp) {
+// Logical element e = r * cols + c of a generated tensor goes to physical row
+// row0 + r (plain) of a pre-tiled matrix with `tcols` columns.
+__global__ void init_matrix_kernel(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
+                                   uint64_t seed, float amp, uint64_t row0, int tiled) {
+    const uint64_t n = rows * cols;
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        dst[e] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
+        const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
+        const uint64_t r = row0 + e / cols, c = e % cols;
+        dst[tiled ? tiled_offset(r, c, cols) : r * cols + c] = v;
     }
 }
 
 void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64_t seed,
-                        float amp, cudaStream_t s) {
-    init_matrix_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows * cols, seed, amp);
+                        float amp, cudaStream_t s, uint64_t row0, int tiled) {
+    init_matrix_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, row0, tiled);
 }
 
 // Logical row r of a [rows, cols] tensor stored at physical row
@@ -35,7 +56,7 @@ __global__ void init_matrix_il_kernel(__nv_bfloat16* dst, uint64_t rows, uint64_
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t r = e / cols, c = e % cols;
         const uint64_t pr = (r / 64) * 128 + offset + r % 64;
-        dst[pr * cols + c] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
+        dst[tiled_offset(pr, c, cols)] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
     }
 }
 
@@ -56,7 +77,7 @@ __global__ void init_head_kernel(__nv_bfloat16* head, const __nv_bfloat16* emb,
         const uint64_t v = e / d, i = e % d;
         const int32_t t = plant_src ? plant_src[v] : -1;
         if (t >= 0) w = __fmaf_rn(coef, __bfloat162float(emb[static_cast<uint64_t>(t) * d + i]), w);
-        head[e] = __float2bfloat16_rn(w);
+        head[tiled_offset(v, i, d)] = __float2bfloat16_rn(w);
     }
 }
 
@@ -103,20 +124,38 @@ __device__ __forceinline__ void rmsnorm_row(const float* x, const float* gain, i
 // ------------------------------------------------------------ embed + norm
 __global__ void embed_norm_kernel(const PassState* ps, const __nv_bfloat16* emb,
                                   const float* gain, int d, float eps, float* x,
-                                  __nv_bfloat16* h) {
-    __shared__ float red[8];
+                                  __nv_bfloat16* h, float* ss) {
+    // x = E[tok]; deferred RMSNorm producer: h = bf16(x * g) and per-128-row
+    // sums of squares ss[t][d/128] (same tree as the GEMM residual epilogue)
+    pdl_wait();
+    pdl_launch();
     const int t = blockIdx.x;
     const int tok = ps->tokens[t];
-    float* xr = x + static_cast<size_t>(t) * d;
-    for (int i = threadIdx.x; i < d; i += 256)
-        xr[i] = __bfloat162float(emb[static_cast<size_t>(tok) * d + i]);
-    __syncthreads();
-    rmsnorm_row(xr, gain, d, eps, h + static_cast<size_t>(t) * d, red);
+    const int tiles = d / 128;
+    for (int base = 0; base < tiles; base += 2) {  // d % 256 == 0: uniform trip count
+        const int tile = base + (threadIdx.x >> 7);
+        const int i = tile * 128 + (threadIdx.x & 127);
+        const float v = __bfloat162float(emb[static_cast<size_t>(tok) * d + i]);
+        x[static_cast<size_t>(t) * d + i] = v;
+        h[static_cast<size_t>(t) * d + i] = __float2bfloat16_rn(__fmul_rn(v, gain[i]));
+        float sq = __fmul_rn(v, v);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+        __shared__ float part[8][4];
+        const int lw = (threadIdx.x & 127) >> 5, grp = threadIdx.x >> 7;
+        if ((threadIdx.x & 31) == 0) part[grp][lw] = sq;
+        __syncthreads();
+        if ((threadIdx.x & 127) == 0)
+            ss[static_cast<size_t>(t) * tiles + tile] =
+                __fadd_rn(__fadd_rn(part[grp][0], part[grp][1]), __fadd_rn(part[grp][2], part[grp][3]));
+        __syncthreads();
+    }
+    (void)eps;
 }
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
-                       int d, float eps, float* x, __nv_bfloat16* h, cudaStream_t s) {
-    embed_norm_kernel<<<w, 256, 0, s>>>(ps, emb, gain, d, eps, x, h);
+                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s) {
+    launch_pdl(embed_norm_kernel, dim3(w), dim3(256), 0, s, ps, emb, gain, d, eps, x, h, ss);
 }
 
 // ------------------------------------------------------------ attention
@@ -137,6 +176,8 @@ __global__ void __launch_bounds__(kAttnThreads)
     __shared__ float qs[256];
     __shared__ float red[kAttnWarps];
     __shared__ float part[kAttnThreads / 8][64];  // [KG][hd] with KG * hd = 16 * 128
+    pdl_wait();
+    pdl_launch();
     const int head = blockIdx.x, t = blockIdx.y;
     const int pos = ps->n_cached + t;
     const int n_keys = pos + 1;
@@ -260,8 +301,8 @@ void launch_attention(const PassState* ps, int w, const ModelDims& m, const floa
                       int layer, __nv_bfloat16* o, cudaStream_t s) {
     dim3 grid(m.n_heads, w);
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(m.head_dim)));
-    attention_kernel<<<grid, kAttnThreads, g_attn_smem_bytes, s>>>(ps, m, q, kv_pool, page_table,
-                                                                   page_size, layer, scale, o);
+    launch_pdl(attention_kernel, grid, dim3(kAttnThreads), g_attn_smem_bytes, s, ps, m, q, kv_pool,
+               page_table, page_size, layer, scale, o);
 }
 
 // ------------------------------------------------------------ RMSNorm
@@ -269,13 +310,15 @@ void launch_attention(const PassState* ps, int w, const ModelDims& m, const floa
 __global__ void rmsnorm_kernel(const float* x, int d, const float* gain, float eps,
                                __nv_bfloat16* h) {
     __shared__ float red[8];
+    pdl_wait();
+    pdl_launch();
     const int t = blockIdx.x;
     rmsnorm_row(x + static_cast<size_t>(t) * d, gain, d, eps, h + static_cast<size_t>(t) * d, red);
 }
 
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s) {
-    rmsnorm_kernel<<<w, 256, 0, s>>>(x, d, gain, eps, h);
+    launch_pdl(rmsnorm_kernel, dim3(w), dim3(256), 0, s, x, d, gain, eps, h);
 }
 
 // ------------------------------------------------------------ KV compaction

@@ -38,15 +38,16 @@ struct PassState {
 };
 
 // ---------------------------------------------------------------- kernels
+// row0: first physical row; tiled: write the pre-tiled GEMM layout (common.cuh)
 void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64_t seed,
-                        float amp, cudaStream_t s);
+                        float amp, cudaStream_t s, uint64_t row0 = 0, int tiled = 1);
 void launch_init_head(__nv_bfloat16* head, const __nv_bfloat16* emb, const int32_t* plant_src,
                       uint64_t vocab, uint64_t d, uint64_t seed, float amp, float plant_coef,
                       cudaStream_t s);
 void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
-                       int d, float eps, float* x, __nv_bfloat16* h, cudaStream_t s);
+                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s);
 void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                       const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                       int layer, __nv_bfloat16* o, cudaStream_t s);

@@ -85,7 +85,7 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
-    auto gemm = [&](int id, const CUtensorMap* mw, const CUtensorMap* mx,
+    auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
                     const GemmEpiParams& ep) -> cudaError_t {
         int n_out, k;
         gemm_shape(ctx, id, &n_out, &k);
@@ -94,36 +94,43 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         mark(0);
         return r;
     };
-    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, s);
+    const int d_tiles = m.d / 128;
+    // deferred RMSNorm: consumers of h scale by r computed from ss partials
+    e.ss_in = ctx->ss;
+    e.ss_tiles = d_tiles;
+    e.eps = m.eps;
+    e.norm_d = m.d;
+    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, ctx->ss,
+                      s);
     mark(2);
     for (int l = 0; l < m.n_layers; ++l) {
         const LayerW& L = ctx->layers[l];
         GemmEpiParams eq = e;
         eq.kind = kEpiQkvRope;
         eq.layer = l;
-        CK(gemm(kGQkv, &L.map_qkv, &ctx->map_h, eq));
+        CK(gemm(kGQkv, L.qkv, &ctx->map_h, eq));
         launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
                          ctx->o, s);
         mark(1);
-        GemmEpiParams er = e;
+        GemmEpiParams er = e;  // residual add; writes u = bf16(x*g) + ss partials
         er.kind = kEpiResidual;
         er.out = ctx->x;
-        CK(gemm(kGO, &L.map_o, &ctx->map_o, er));
-        launch_rmsnorm(w, ctx->x, m.d, ctx->gain_ones, m.eps, ctx->h, s);
-        mark(2);
+        er.ss_in = nullptr;
+        er.u_out = ctx->h;
+        er.gain = ctx->gain_ones;
+        er.ss_out = ctx->ss;
+        CK(gemm(kGO, L.o, &ctx->map_o, er));
         GemmEpiParams eg = e;
         eg.kind = kEpiSwiGLU;
         eg.out_bf = ctx->a;
-        CK(gemm(kGGu, &L.map_gu, &ctx->map_h, eg));
-        CK(gemm(kGDown, &L.map_d, &ctx->map_a, er));
-        launch_rmsnorm(w, ctx->x, m.d, ctx->gain_ones, m.eps, ctx->h, s);
-        mark(2);
+        CK(gemm(kGGu, L.gu, &ctx->map_h, eg));
+        CK(gemm(kGDown, L.dn, &ctx->map_a, er));
     }
     if (want_logits) {
         GemmEpiParams el = e;
         el.kind = kEpiStore;
         el.out = ctx->logits;
-        CK(gemm(kGHead, &ctx->map_head, &ctx->map_h, el));
+        CK(gemm(kGHead, ctx->head, &ctx->map_h, el));
     }
     CK(cudaGetLastError());
     return DD_OK;
@@ -257,14 +264,7 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
         CK(cudaMalloc(&L.o, sizeof(__nv_bfloat16) * d_ * m.q_dim()));
         CK(cudaMalloc(&L.gu, sizeof(__nv_bfloat16) * 2 * m.ffn * d_));
         CK(cudaMalloc(&L.dn, sizeof(__nv_bfloat16) * d_ * m.ffn));
-        if (make_tmap_bf16(&L.map_qkv, L.qkv, m.qkv_rows(), d_, 128) ||
-            make_tmap_bf16(&L.map_o, L.o, d_, m.q_dim(), 128) ||
-            make_tmap_bf16(&L.map_gu, L.gu, 2 * m.ffn, d_, 128) ||
-            make_tmap_bf16(&L.map_d, L.dn, d_, m.ffn, 128))
-            return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
     }
-    if (make_tmap_bf16(&ctx->map_head, ctx->head, m.vocab, d_, 128))
-        return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
     const int gain_n = std::max(m.d, m.ffn);
     CK(cudaMalloc(&ctx->gain_ones, sizeof(float) * gain_n));
     launch_fill_f32(ctx->gain_ones, gain_n, 1.0f, ctx->stream);
@@ -289,12 +289,13 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
         gemm_shape(ctx, id, &n_out, &k);
         for (int nt = 16; nt <= kMaxPassTokens; nt += 16) {
             const GemmPlan& p = plan_for(ctx, id, nt);
-            ws_floats = std::max(ws_floats, static_cast<size_t>(p.splits) * nt * n_out);
+            ws_floats = std::max(ws_floats, gemm_ws_floats(p, nt));
         }
     }
     CK(cudaMalloc(&ctx->ws, sizeof(float) * ws_floats));
     CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
     CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
+    CK(cudaMalloc(&ctx->ss, sizeof(float) * R * (m.d / 128)));
     CK(cudaMalloc(&ctx->logits, sizeof(float) * R * m.vocab));
 
     // paged KV cache (all pages reserved up front; page table maps logical->physical)
@@ -361,7 +362,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
                    ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
-                   ctx->counters};
+                   ctx->counters, ctx->ss};
     for (void* p : dev)
         if (p) cudaFree(p);
     if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
@@ -385,7 +386,8 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
     const float amp_emb = static_cast<float>(pt.emb_std * std::sqrt(3.0));
     cudaStream_t s = ctx->stream;
     const uint64_t d_ = m.d;
-    launch_init_matrix(ctx->emb, m.vocab, d_, derive_seed(weight_seed, kTensorEmb), amp_emb, s);
+    launch_init_matrix(ctx->emb, m.vocab, d_, derive_seed(weight_seed, kTensorEmb), amp_emb, s, 0,
+                       0);  // gathered, row-major
     int32_t* d_src = nullptr;
     if (pt.any) {
         CK(cudaMalloc(&d_src, sizeof(int32_t) * m.vocab));
@@ -397,11 +399,11 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
     for (int l = 0; l < m.n_layers; ++l) {
         LayerW& L = ctx->layers[l];
         const uint64_t qd = m.q_dim(), kvd = m.kv_dim();
-        launch_init_matrix(L.qkv, qd, d_, derive_seed(weight_seed, tensor_id(l, kWq)), amp_proj, s);
-        launch_init_matrix(L.qkv + qd * d_, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWk)),
-                           amp_proj, s);
-        launch_init_matrix(L.qkv + (qd + kvd) * d_, kvd, d_,
-                           derive_seed(weight_seed, tensor_id(l, kWv)), amp_proj, s);
+        launch_init_matrix(L.qkv, qd, d_, derive_seed(weight_seed, tensor_id(l, kWq)), amp_proj, s, 0);
+        launch_init_matrix(L.qkv, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWk)), amp_proj, s,
+                           qd);
+        launch_init_matrix(L.qkv, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWv)), amp_proj, s,
+                           qd + kvd);
         launch_init_matrix(L.o, d_, qd, derive_seed(weight_seed, tensor_id(l, kWo)), amp_out, s);
         launch_init_matrix_interleaved(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWg)),
                                        amp_proj, 0, s);
@@ -654,24 +656,12 @@ int dd_profile_pass(dd_ctx* ctx, int w, float* ms4) {
     return DD_OK;
 }
 
-int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launches) {
-    if (!ctx || !median_ms || w < 1 || w > kMaxPassTokens || trials < 1)
-        return ctx_fail(ctx, DD_E_ARG, "bad arguments");
-    if (ctx->n_cached + w > ctx->max_seq) return ctx_fail(ctx, DD_E_CAPACITY, "cache full");
-    CK(cudaSetDevice(ctx->device));
+// The GEMM launches of one pass (4 per layer + LM head), back to back; with
+// `trace` each launch records per-CTA stamps at trace + launch * stride.
+static int enqueue_gemm_sequence(dd_ctx* ctx, int w, unsigned long long* trace, size_t stride,
+                                 int* n_launch) {
     const ModelDims& m = ctx->m;
     const int nt = round_nt(w);
-    const int n0 = ctx->n_cached;
-    // pass state for the qkv epilogue positions
-    const int slot = ctx->ps_slot;
-    ctx->ps_slot = (slot + 1) % kPsRing;
-    CK(cudaEventSynchronize(ctx->ps_done[slot]));
-    PassState* hp = ctx->h_ps + slot;
-    hp->n_cached = n0;
-    hp->w = w;
-    for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
-    CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
     GemmEpiParams e{};
     e.counters = ctx->counters;
     e.ps = ctx->d_ps;
@@ -682,48 +672,103 @@ int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launche
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
+    e.ss_in = ctx->ss;
+    e.ss_tiles = m.d / 128;
+    e.eps = m.eps;
+    e.norm_d = m.d;
+    int n = 0;
+    auto one = [&](int id, const __nv_bfloat16* W, const CUtensorMap* mx,
+                   const GemmEpiParams& ep) -> cudaError_t {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        gemm_set_trace(trace ? trace + stride * n : nullptr);
+        ++n;
+        return launch_gemm(W, mx, n_out, k, w, nt, plan_for(ctx, id, nt), ctx->ws, ep, ctx->stream);
+    };
+    for (int l = 0; l < m.n_layers; ++l) {
+        const LayerW& L = ctx->layers[l];
+        GemmEpiParams eq = e;
+        eq.kind = kEpiQkvRope;
+        eq.layer = l;
+        CK(one(kGQkv, L.qkv, &ctx->map_h, eq));
+        GemmEpiParams er = e;
+        er.kind = kEpiResidual;
+        er.out = ctx->x;
+        er.ss_in = nullptr;
+        er.u_out = ctx->h;
+        er.gain = ctx->gain_ones;
+        er.ss_out = ctx->ss;
+        CK(one(kGO, L.o, &ctx->map_o, er));
+        GemmEpiParams eg = e;
+        eg.kind = kEpiSwiGLU;
+        eg.out_bf = ctx->a;
+        CK(one(kGGu, L.gu, &ctx->map_h, eg));
+        CK(one(kGDown, L.dn, &ctx->map_a, er));
+    }
+    GemmEpiParams el = e;
+    el.kind = kEpiStore;
+    el.out = ctx->logits;
+    CK(one(kGHead, ctx->head, &ctx->map_h, el));
+    gemm_set_trace(nullptr);
+    if (n_launch) *n_launch = n;
+    return DD_OK;
+}
+
+static int upload_dummy_pass(dd_ctx* ctx, int w) {
+    const int slot = ctx->ps_slot;
+    ctx->ps_slot = (slot + 1) % kPsRing;
+    CK(cudaEventSynchronize(ctx->ps_done[slot]));
+    PassState* hp = ctx->h_ps + slot;
+    hp->n_cached = ctx->n_cached;
+    hp->w = w;
+    for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
+    CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
+    return DD_OK;
+}
+
+int dd_debug_pass_trace(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_launch,
+                        int* ctas_per_launch) {
+    if (!ctx || !trace || w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_ARG, "bad args");
+    CK(cudaSetDevice(ctx->device));
+    int rc = upload_dummy_pass(ctx, w);
+    if (rc) return rc;
+    int maxc = 0;
+    for (int id = 0; id < kNumGemm; ++id) maxc = std::max(maxc, plan_for(ctx, id, round_nt(w)).ctas);
+    const size_t stride = 8 * static_cast<size_t>(maxc);
+    const size_t need = stride * (4 * ctx->m.n_layers + 1);
+    if (need > max_entries) return ctx_fail(ctx, DD_E_CAPACITY, "trace buffer too small");
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long) * need));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long) * need));
+    rc = enqueue_gemm_sequence(ctx, w, nullptr, 0, nullptr);  // warm-up
+    if (rc) return rc;
+    rc = enqueue_gemm_sequence(ctx, w, d, stride, n_launch);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * need, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *ctas_per_launch = maxc;
+    ctx->last_w = 0;
+    return DD_OK;
+}
+
+int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launches) {
+    if (!ctx || !median_ms || w < 1 || w > kMaxPassTokens || trials < 1)
+        return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    if (ctx->n_cached + w > ctx->max_seq) return ctx_fail(ctx, DD_E_CAPACITY, "cache full");
+    CK(cudaSetDevice(ctx->device));
+    int rc = upload_dummy_pass(ctx, w);
+    if (rc) return rc;
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     std::vector<float> ms;
     int n_launch = 0;
     for (int t = 0; t < trials + 1; ++t) {
-        n_launch = 0;
         CK(cudaEventRecord(a, ctx->stream));
-        for (int l = 0; l < m.n_layers; ++l) {
-            const LayerW& L = ctx->layers[l];
-            int n_out, k;
-            GemmEpiParams eq = e;
-            eq.kind = kEpiQkvRope;
-            eq.layer = l;
-            gemm_shape(ctx, kGQkv, &n_out, &k);
-            CK(launch_gemm(&L.map_qkv, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGQkv, nt),
-                           ctx->ws, eq, ctx->stream));
-            GemmEpiParams er = e;
-            er.kind = kEpiResidual;
-            er.out = ctx->x;
-            gemm_shape(ctx, kGO, &n_out, &k);
-            CK(launch_gemm(&L.map_o, &ctx->map_o, n_out, k, w, nt, plan_for(ctx, kGO, nt), ctx->ws,
-                           er, ctx->stream));
-            GemmEpiParams eg = e;
-            eg.kind = kEpiSwiGLU;
-            eg.out_bf = ctx->a;
-            gemm_shape(ctx, kGGu, &n_out, &k);
-            CK(launch_gemm(&L.map_gu, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGGu, nt),
-                           ctx->ws, eg, ctx->stream));
-            gemm_shape(ctx, kGDown, &n_out, &k);
-            CK(launch_gemm(&L.map_d, &ctx->map_a, n_out, k, w, nt, plan_for(ctx, kGDown, nt),
-                           ctx->ws, er, ctx->stream));
-            n_launch += 4;
-        }
-        GemmEpiParams el = e;
-        el.kind = kEpiStore;
-        el.out = ctx->logits;
-        int n_out, k;
-        gemm_shape(ctx, kGHead, &n_out, &k);
-        CK(launch_gemm(&ctx->map_head, &ctx->map_h, n_out, k, w, nt, plan_for(ctx, kGHead, nt),
-                       ctx->ws, el, ctx->stream));
-        ++n_launch;
+        rc = enqueue_gemm_sequence(ctx, w, nullptr, 0, &n_launch);
+        if (rc) return rc;
         CK(cudaEventRecord(b, ctx->stream));
         CK(cudaEventSynchronize(b));
         float x = 0.0f;
@@ -736,7 +781,6 @@ int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launche
     const size_t n = ms.size();
     *median_ms = n % 2 ? ms[n / 2] : 0.5f * (ms[n / 2 - 1] + ms[n / 2]);
     if (launches) *launches = n_launch;
-    ctx->n_cached = n0;
     ctx->last_w = 0;
     return DD_OK;
 }
@@ -769,17 +813,60 @@ int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n)
     }
     if (n != count) return ctx_fail(ctx, DD_E_ARG, "element count mismatch");
     CK(cudaSetDevice(ctx->device));
-    if (which == 4) {  // stored interleaved in 64-row blocks; return [gate; up]
-        std::vector<uint16_t> tmp(n);
-        CK(cudaMemcpy(tmp.data(), src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
-        for (size_t pr = 0; pr < 2 * static_cast<size_t>(m.ffn); ++pr) {
-            const size_t blk = pr / 128, off = pr % 128;
-            const size_t lr = off < 64 ? blk * 64 + off : m.ffn + blk * 64 + (off - 64);
-            std::memcpy(host + lr * d_, tmp.data() + pr * d_, sizeof(uint16_t) * d_);
-        }
+    if (which == 0) {  // embedding: plain row-major
+        CK(cudaMemcpy(host, src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
         return DD_OK;
     }
-    CK(cudaMemcpy(host, src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
+    // GEMM operands are stored pre-tiled (common.cuh tiled_offset); the fused
+    // gate/up matrix is also interleaved in 64-row blocks.  Return logical layout.
+    std::vector<uint16_t> tmp(n);
+    CK(cudaMemcpy(tmp.data(), src, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost));
+    const size_t cols = (which == 3) ? static_cast<size_t>(m.q_dim())
+                        : (which == 5) ? static_cast<size_t>(m.ffn) : d_;
+    const size_t rows = n / cols;
+    for (size_t pr = 0; pr < rows; ++pr) {
+        size_t lr = pr;
+        if (which == 4) {
+            const size_t blk = pr / 128, off = pr % 128;
+            lr = off < 64 ? blk * 64 + off : m.ffn + blk * 64 + (off - 64);
+        }
+        for (size_t c = 0; c < cols; ++c) host[lr * cols + c] = tmp[tiled_offset(pr, c, cols)];
+    }
+    return DD_OK;
+}
+
+int dd_debug_gemm_trace(dd_ctx* ctx, int which, int w, uint64_t* trace, int max_ctas,
+                        int* n_ctas) {
+    // one launch of GEMM `which` (0 qkv, 1 o, 2 gate/up, 3 down, 4 head) of layer 0
+    if (!ctx || !trace || !n_ctas || w < 1 || w > kMaxPassTokens || which < 0 || which > 4)
+        return ctx_fail(ctx, DD_E_ARG, "bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    const int nt = round_nt(w);
+    const GemmPlan& p = plan_for(ctx, which, nt);
+    const int ctas = p.ctas;
+    if (ctas > max_ctas) return ctx_fail(ctx, DD_E_CAPACITY, "trace buffer too small");
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long) * 8 * ctas));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long) * 8 * ctas));
+    int n_out, k;
+    gemm_shape(ctx, which, &n_out, &k);
+    const LayerW& L = ctx->layers[0];
+    const __nv_bfloat16* W = which == 0 ? L.qkv : which == 1 ? L.o : which == 2 ? L.gu
+                             : which == 3 ? L.dn : ctx->head;
+    const CUtensorMap* mx = which == 1 ? &ctx->map_o : which == 3 ? &ctx->map_a : &ctx->map_h;
+    GemmEpiParams e{};
+    e.kind = kEpiStore;
+    e.counters = ctx->counters;
+    e.out = ctx->ws;  // scratch destination
+    for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+        gemm_set_trace(rep ? d : nullptr);
+        CK(launch_gemm(W, mx, n_out, k, w, nt, p, ctx->ws, e, ctx->stream));
+    }
+    gemm_set_trace(nullptr);
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * 8 * ctas, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *n_ctas = ctas;
     return DD_OK;
 }
 
@@ -797,13 +884,19 @@ int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, 
     CK(cudaMalloc(&dW, sizeof(uint16_t) * n_out * static_cast<size_t>(k)));
     CK(cudaMalloc(&dX, sizeof(uint16_t) * kMaxPassTokens * static_cast<size_t>(k)));
     CK(cudaMemset(dX, 0, sizeof(uint16_t) * kMaxPassTokens * static_cast<size_t>(k)));
-    CK(cudaMemcpy(dW, W, sizeof(uint16_t) * n_out * static_cast<size_t>(k), cudaMemcpyHostToDevice));
+    {
+        std::vector<uint16_t> tiled(static_cast<size_t>(n_out) * k);
+        for (size_t r = 0; r < static_cast<size_t>(n_out); ++r)
+            for (size_t c = 0; c < static_cast<size_t>(k); ++c)
+                tiled[tiled_offset(r, c, k)] = W[r * k + c];
+        CK(cudaMemcpy(dW, tiled.data(), sizeof(uint16_t) * tiled.size(), cudaMemcpyHostToDevice));
+    }
     CK(cudaMemcpy(dX, X, sizeof(uint16_t) * w * static_cast<size_t>(k), cudaMemcpyHostToDevice));
-    CUtensorMap mw, mx;
-    if (make_tmap_bf16(&mw, dW, n_out, k, 128) || make_tmap_bf16(&mx, dX, kMaxPassTokens, k, 16))
+    CUtensorMap mx;
+    if (make_tmap_bf16(&mx, dX, kMaxPassTokens, k, 16))
         return ctx_fail(nullptr, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
     GemmPlan p = plan_gemm(n_out, k, nt);
-    CK(cudaMalloc(&dws, sizeof(float) * p.splits * static_cast<size_t>(w) * n_out));
+    CK(cudaMalloc(&dws, sizeof(float) * gemm_ws_floats(p, w)));
     CK(cudaMalloc(&dY, sizeof(float) * static_cast<size_t>(w) * n_out));
     int* dcnt = nullptr;
     CK(cudaMalloc(&dcnt, sizeof(int) * p.tiles));
@@ -812,7 +905,7 @@ int dd_test_gemm(const uint16_t* W, const uint16_t* X, int n_out, int k, int w, 
     ep.kind = kEpiStore;
     ep.counters = dcnt;
     ep.out = dY;
-    CK(launch_gemm(&mw, &mx, n_out, k, w, nt, p, dws, ep, 0));
+    CK(launch_gemm(static_cast<const __nv_bfloat16*>(dW), &mx, n_out, k, w, nt, p, dws, ep, 0));
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(Y, dY, sizeof(float) * static_cast<size_t>(w) * n_out, cudaMemcpyDeviceToHost));
