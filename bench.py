@@ -61,11 +61,17 @@ def dist_env():
     return ws, rank, local
 
 
-def core_slice(rank: int, world: int):
+def core_slice(rank: int, world: int, max_draft: int = 12):
+    """(target-thread core, draft cores) for stream `rank`: disjoint slices of
+    the host cores; the draft gets at most `max_draft` (on the 16-core B200
+    host 12 draft threads beat 15, which contend with the host's own work)."""
     cpus = sorted(os.sched_getaffinity(0))
     per = max(2, len(cpus) // world)
     mine = cpus[rank * per:(rank + 1) * per] or cpus[-per:]
-    return mine[0], mine[1:] or mine[:1]  # (target thread core, draft cores)
+    draft = mine[1:] or mine[:1]
+    if len(draft) > max_draft:
+        draft = draft[1:1 + max_draft]
+    return mine[0], draft
 
 
 class ClockSampler:

@@ -27,6 +27,7 @@ def lib():
                                                        C.c_uint64, C.c_double, C.c_float,
                                                        C.c_float, C.c_int]
         L.orc_llama_free.argtypes = [C.c_void_p]
+        L.orc_llama_set_quant.argtypes = [C.c_void_p, C.c_int]
         L.orc_llama_len.argtypes = [C.c_void_p]
         L.orc_llama_truncate.argtypes = [C.c_void_p, C.c_int]
         L.orc_llama_tensor.restype = C.POINTER(C.c_uint16)
@@ -43,7 +44,7 @@ class OracleLlama:
     """CPU Llama restatement with the product's synthetic-weight recipe."""
 
     def __init__(self, shape: dict, weight_seed: int, plant: dict | None = None,
-                 max_seq: int = 512, threads: int = 8):
+                 max_seq: int = 512, threads: int = 8, w8a8: bool = False):
         plant = plant or {}
         self.shape = dict(shape)
         self.V = shape["vocab"]
@@ -53,6 +54,8 @@ class OracleLlama:
             shape["vocab"], shape.get("rms_eps", 1e-5), shape.get("rope_theta", 1e4), max_seq,
             weight_seed, plant.get("plant_seed", 0), plant.get("alpha", 0.0),
             plant.get("gain", 0.0), plant.get("emb_std", 0.0), threads)
+        if w8a8:  # the product CPU draft's numerics (draft.cpp)
+            lib().orc_llama_set_quant(self.h, 1)
 
     def forward(self, tokens, last_only: bool = False) -> np.ndarray:
         t = np.ascontiguousarray(tokens, dtype=np.int32)

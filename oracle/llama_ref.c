@@ -139,7 +139,14 @@ static int make_plant(int vocab, int d, uint64_t plant_seed, double alpha, float
 
 /* ------------------------------------------------------------ model */
 typedef struct {
+    int rows, cols;
+    int8_t* q;      /* [rows][cols] */
+    float* scale;   /* [rows] */
+} orc_qmat;
+
+typedef struct {
     uint16_t *qkv, *o, *gu, *dn;
+    orc_qmat qqkv, qo, qgu, qdn; /* W8A8 draft mode */
 } orc_layer;
 
 typedef struct orc_llama {
@@ -151,6 +158,8 @@ typedef struct orc_llama {
     float *rope_cos, *rope_sin;
     int32_t* plant_src;
     int32_t* plant_perm;
+    int quant;      /* 1: W8A8 matmuls (the product CPU draft's numerics) */
+    orc_qmat qhead;
 } orc_llama;
 
 static size_t kv_idx(const orc_llama* m, int layer, int kv, int h, int pos) {
@@ -255,6 +264,92 @@ void orc_llama_free(orc_llama* m) {
     free(m->rope_sin);
     free(m->plant_src);
     free(m);
+}
+
+/* Per-row symmetric int8 weights (scale = max|w|/127, round-half-even) and
+ * per-token int8 activations: restates the product CPU draft
+ * (paper_2503_00784_b200/csrc/draft.cpp quantize / quantize_acts / qdot_rows);
+ * the integer dot products are exact, so logits match bit-for-bit up to the
+ * float epilogue order. */
+static orc_qmat quantize_rows(const uint16_t* w, int rows, int cols) {
+    orc_qmat m;
+    m.rows = rows;
+    m.cols = cols;
+    m.q = (int8_t*)malloc((size_t)rows * cols);
+    m.scale = (float*)malloc(sizeof(float) * rows);
+    for (int r = 0; r < rows; ++r) {
+        const uint16_t* src = w + (size_t)r * cols;
+        float mx = 0.0f;
+        for (int c = 0; c < cols; ++c) {
+            const float a = fabsf(bf2f(src[c]));
+            if (a > mx) mx = a;
+        }
+        const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+        for (int c = 0; c < cols; ++c) {
+            int v = (int)nearbyintf(bf2f(src[c]) / sc);
+            v = v < -127 ? -127 : (v > 127 ? 127 : v);
+            m.q[(size_t)r * cols + c] = (int8_t)v;
+        }
+        m.scale[r] = sc;
+    }
+    return m;
+}
+
+void orc_llama_set_quant(orc_llama* m, int on) {
+    if (!on || m->quant) return;
+    const int qd = m->H * m->hd, kvd = m->Hkv * m->hd;
+    for (int l = 0; l < m->L; ++l) {
+        orc_layer* Ly = &m->layers[l];
+        Ly->qqkv = quantize_rows(Ly->qkv, qd + 2 * kvd, m->d);
+        Ly->qo = quantize_rows(Ly->o, m->d, qd);
+        Ly->qgu = quantize_rows(Ly->gu, 2 * m->F, m->d);
+        Ly->qdn = quantize_rows(Ly->dn, m->d, m->F);
+    }
+    m->qhead = quantize_rows(m->head, m->V, m->d);
+    m->quant = 1;
+}
+
+typedef struct {
+    const orc_qmat* m;
+    const int8_t* xq;
+    const float* xs;
+    int w;
+    float* y;
+} qmm_arg;
+static void qmm_range(void* p, int64_t lo, int64_t hi) {
+    qmm_arg* a = (qmm_arg*)p;
+    const int k = a->m->cols;
+    for (int64_t n = lo; n < hi; ++n)
+        for (int t = 0; t < a->w; ++t) {
+            int64_t dot = 0;
+            const int8_t* wq = a->m->q + (size_t)n * k;
+            const int8_t* xq = a->xq + (size_t)t * k;
+            for (int i = 0; i < k; ++i) dot += (int64_t)wq[i] * xq[i];
+            a->y[(size_t)t * a->m->rows + n] = (float)(int32_t)dot * (a->xs[t] * a->m->scale[n]);
+        }
+}
+/* x: [w][k] float values that are exactly bf16 */
+static void matmul_q(const orc_qmat* m, const float* x, int w, float* y) {
+    const int k = m->cols;
+    int8_t* xq = (int8_t*)malloc((size_t)w * k);
+    float* xs = (float*)malloc(sizeof(float) * w);
+    for (int t = 0; t < w; ++t) {
+        float mx = 0.0f;
+        for (int i = 0; i < k; ++i) {
+            const float a = fabsf(x[(size_t)t * k + i]);
+            if (a > mx) mx = a;
+        }
+        const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+        for (int i = 0; i < k; ++i) {
+            int v = (int)nearbyintf(x[(size_t)t * k + i] / sc);
+            xq[(size_t)t * k + i] = (int8_t)(v < -127 ? -127 : (v > 127 ? 127 : v));
+        }
+        xs[t] = sc;
+    }
+    qmm_arg a = {m, xq, xs, w, y};
+    par_range(m->rows, qmm_range, &a);
+    free(xq);
+    free(xs);
 }
 
 int orc_llama_len(const orc_llama* m) { return m->n_cached; }
@@ -401,7 +496,8 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
     const float scale = (float)(1.0 / sqrt((double)hd));
     for (int l = 0; l < m->L; ++l) {
         const orc_layer* Ly = &m->layers[l];
-        matmul(Ly->qkv, rows, d, h, w, qkv);
+        if (m->quant) matmul_q(&Ly->qqkv, h, w, qkv);
+        else matmul(Ly->qkv, rows, d, h, w, qkv);
         scale_rows(qkv, w, rows, rn);
         for (int t = 0; t < w; ++t) {
             const int pos = n0 + t;
@@ -430,12 +526,14 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
             attn_arg aa = {m, l, n0, w, q, o, scale};
             par_range((int64_t)H * w, attn_range, &aa);
         }
-        matmul(Ly->o, d, qd, o, w, y);
+        if (m->quant) matmul_q(&Ly->qo, o, w, y);
+        else matmul(Ly->o, d, qd, o, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
             rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
         }
-        matmul(Ly->gu, 2 * F, d, h, w, y);
+        if (m->quant) matmul_q(&Ly->qgu, h, w, y);
+        else matmul(Ly->gu, 2 * F, d, h, w, y);
         scale_rows(y, w, 2 * F, rn);
         for (int t = 0; t < w; ++t)
             for (int f = 0; f < F; ++f) {
@@ -443,7 +541,8 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
                 const float silu = g / (1.0f + expf(-g));
                 a[(size_t)t * F + f] = bfr(silu * u);
             }
-        matmul(Ly->dn, d, F, a, w, y);
+        if (m->quant) matmul_q(&Ly->qdn, a, w, y);
+        else matmul(Ly->dn, d, F, a, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
             rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
@@ -451,10 +550,12 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
     }
     if (logits) {
         if (last_only) {
-            matmul(m->head, V, d, h + (size_t)(w - 1) * d, 1, logits);
+            if (m->quant) matmul_q(&m->qhead, h + (size_t)(w - 1) * d, 1, logits);
+            else matmul(m->head, V, d, h + (size_t)(w - 1) * d, 1, logits);
             scale_rows(logits, 1, V, rn + (w - 1));
         } else {
-            matmul(m->head, V, d, h, w, logits);
+            if (m->quant) matmul_q(&m->qhead, h, w, logits);
+            else matmul(m->head, V, d, h, w, logits);
             scale_rows(logits, w, V, rn);
         }
     }

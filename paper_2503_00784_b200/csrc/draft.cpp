@@ -1,4 +1,5 @@
-// CPU draft model: Llama-family forward on pinned host cores (AVX-512 BF16).
+// CPU draft model: Llama-family forward on pinned host cores, W8A8 (per-row
+// int8 weights, per-token int8 activations, AVX-512 VNNI dot products).
 //
 // This is the draft side of DuoDecoding (north star: "the draft model runs on
 // host CPU cores in a concurrent thread").  The reference's draft is a
@@ -64,36 +65,102 @@ void gen(SpinPool& pool, std::vector<uint16_t>& dst, uint64_t offset, uint64_t n
     });
 }
 
-__attribute__((target("avx512f,avx512bw,avx512bf16"))) inline float dot_bf16(const uint16_t* w,
-                                                                            const uint16_t* x,
-                                                                            int k) {
-    __m512 acc0 = _mm512_setzero_ps(), acc1 = _mm512_setzero_ps();
-    int i = 0;
-    for (; i + 64 <= k; i += 64) {
-        acc0 = _mm512_dpbf16_ps(acc0, (__m512bh)_mm512_loadu_si512(w + i),
-                                (__m512bh)_mm512_loadu_si512(x + i));
-        acc1 = _mm512_dpbf16_ps(acc1, (__m512bh)_mm512_loadu_si512(w + i + 32),
-                                (__m512bh)_mm512_loadu_si512(x + i + 32));
-    }
-    for (; i + 32 <= k; i += 32)
-        acc0 = _mm512_dpbf16_ps(acc0, (__m512bh)_mm512_loadu_si512(w + i),
-                                (__m512bh)_mm512_loadu_si512(x + i));
-    float s = _mm512_reduce_add_ps(_mm512_add_ps(acc0, acc1));
-    for (; i < k; ++i) s += bf2f(w[i]) * bf2f(x[i]);
-    return s;
-}
-
-// Y[t][n] = W[n,:] . X[t,:] for rows n split across the pool
-void matmul(SpinPool& pool, const uint16_t* W, int rows, int k, const uint16_t* X, int w,
-            float* Y) {
+// Per-row symmetric int8 quantisation of a bf16 matrix (mirrored bit-for-bit
+// by oracle/llama_ref.c orc_quantize_rows).
+QMat quantize(const std::vector<uint16_t>& w, int rows, int cols, SpinPool& pool) {
+    QMat m;
+    m.rows = rows;
+    m.cols = cols;
+    m.q.resize(static_cast<size_t>(rows) * cols);
+    m.scale.resize(rows);
+    m.rowsum.resize(rows);
     pool.run([&](int tid, int nt) {
         const int lo = static_cast<int>(static_cast<int64_t>(rows) * tid / nt);
         const int hi = static_cast<int>(static_cast<int64_t>(rows) * (tid + 1) / nt);
-        for (int n = lo; n < hi; ++n) {
-            const uint16_t* wr = W + static_cast<size_t>(n) * k;
-            for (int t = 0; t < w; ++t)
-                Y[static_cast<size_t>(t) * rows + n] = dot_bf16(wr, X + static_cast<size_t>(t) * k, k);
+        for (int r = lo; r < hi; ++r) {
+            const uint16_t* src = &w[static_cast<size_t>(r) * cols];
+            float mx = 0.0f;
+            for (int c = 0; c < cols; ++c) mx = std::max(mx, std::fabs(bf2f(src[c])));
+            const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+            int32_t sum = 0;
+            int8_t* dst = &m.q[static_cast<size_t>(r) * cols];
+            for (int c = 0; c < cols; ++c) {
+                int v = static_cast<int>(std::nearbyint(bf2f(src[c]) / sc));
+                v = std::max(-127, std::min(127, v));
+                dst[c] = static_cast<int8_t>(v);
+                sum += v;
+            }
+            m.scale[r] = sc;
+            m.rowsum[r] = sum;
         }
+    });
+    return m;
+}
+
+// Per-token symmetric int8 activation quantisation, stored as u8 = q + 128.
+void quantize_acts(const uint16_t* X, int w, int k, std::vector<uint8_t>& xq,
+                   std::vector<float>& xs) {
+    xq.resize(static_cast<size_t>(w) * k);
+    xs.resize(w);
+    for (int t = 0; t < w; ++t) {
+        const uint16_t* x = X + static_cast<size_t>(t) * k;
+        float mx = 0.0f;
+        for (int i = 0; i < k; ++i) mx = std::max(mx, std::fabs(bf2f(x[i])));
+        const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+        for (int i = 0; i < k; ++i) {
+            int v = static_cast<int>(std::nearbyint(bf2f(x[i]) / sc));
+            v = std::max(-127, std::min(127, v));
+            xq[static_cast<size_t>(t) * k + i] = static_cast<uint8_t>(v + 128);
+        }
+        xs[t] = sc;
+    }
+}
+
+// Y[t][n] = (sum_k xq[t][k] * q[n][k]) * (xs[t] * scale[n]); 8 rows per block
+// so eight independent vpdpbusd chains share each activation load.
+__attribute__((target("avx512f,avx512bw,avx512vnni"))) void qdot_rows(
+    const QMat& m, const uint8_t* xq, const float* xs, int w, int lo, int hi, float* Y) {
+    const int k = m.cols;
+    for (int t = 0; t < w; ++t) {
+        const uint8_t* x = xq + static_cast<size_t>(t) * k;
+        int n = lo;
+        for (; n + 8 <= hi; n += 8) {
+            __m512i acc[8];
+#pragma GCC unroll 8
+            for (int r = 0; r < 8; ++r) acc[r] = _mm512_setzero_si512();
+            for (int i = 0; i < k; i += 64) {
+                const __m512i xv = _mm512_loadu_si512(x + i);
+#pragma GCC unroll 8
+                for (int r = 0; r < 8; ++r)
+                    acc[r] = _mm512_dpbusd_epi32(
+                        acc[r], xv, _mm512_loadu_si512(&m.q[static_cast<size_t>(n + r) * k + i]));
+            }
+#pragma GCC unroll 8
+            for (int r = 0; r < 8; ++r) {
+                const int32_t dot = _mm512_reduce_add_epi32(acc[r]) - 128 * m.rowsum[n + r];
+                Y[static_cast<size_t>(t) * m.rows + n + r] =
+                    static_cast<float>(dot) * (xs[t] * m.scale[n + r]);
+            }
+        }
+        for (; n < hi; ++n) {
+            __m512i acc = _mm512_setzero_si512();
+            for (int i = 0; i < k; i += 64)
+                acc = _mm512_dpbusd_epi32(acc, _mm512_loadu_si512(x + i),
+                                          _mm512_loadu_si512(&m.q[static_cast<size_t>(n) * k + i]));
+            const int32_t dot = _mm512_reduce_add_epi32(acc) - 128 * m.rowsum[n];
+            Y[static_cast<size_t>(t) * m.rows + n] = static_cast<float>(dot) * (xs[t] * m.scale[n]);
+        }
+    }
+}
+
+void matmul(SpinPool& pool, const QMat& m, const uint16_t* X, int w, float* Y,
+            std::vector<uint8_t>& xq, std::vector<float>& xs) {
+    quantize_acts(X, w, m.cols, xq, xs);
+    const int blocks = (m.rows + 7) / 8;
+    pool.run([&](int tid, int nt) {
+        const int lo = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * tid / nt) * 8);
+        const int hi = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * (tid + 1) / nt) * 8);
+        if (lo < hi) qdot_rows(m, xq.data(), xs.data(), w, lo, hi, Y);
     });
 }
 
@@ -178,7 +245,7 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
     const float amp_emb = static_cast<float>(pt.emb_std * std::sqrt(3.0));
     const uint64_t D = static_cast<uint64_t>(d_);
     emb_.resize(static_cast<size_t>(V_) * D);
-    head_.resize(static_cast<size_t>(V_) * D);
+    std::vector<uint16_t> head_bf(static_cast<size_t>(V_) * D);
     gen(*pool_, emb_, 0, V_ * D, derive(weight_seed, 0), amp_emb);
     {
         const uint64_t hs = derive(weight_seed, 1);
@@ -189,24 +256,27 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
                 float w = unit(hs, e) * amp_proj;
                 const int32_t t = pt.any ? pt.src[e / D] : -1;
                 if (t >= 0) w = std::fmaf(pt.coef, bf2f(emb_[static_cast<size_t>(t) * D + e % D]), w);
-                head_[e] = f2bf(w);
+                head_bf[e] = f2bf(w);
             }
         });
+        head_ = quantize(head_bf, V_, d_, *pool_);
     }
     layers_.resize(L_);
     for (int l = 0; l < L_; ++l) {
         DraftLayer& Ly = layers_[l];
-        Ly.qkv.resize(static_cast<size_t>(qd + 2 * kvd) * D);
-        Ly.o.resize(D * qd);
-        Ly.gu.resize(2 * static_cast<size_t>(F_) * D);
-        Ly.dn.resize(D * F_);
-        gen(*pool_, Ly.qkv, 0, qd * D, derive(weight_seed, tensor_id(l, 0)), amp_proj);
-        gen(*pool_, Ly.qkv, qd * D, kvd * D, derive(weight_seed, tensor_id(l, 1)), amp_proj);
-        gen(*pool_, Ly.qkv, (qd + kvd) * D, kvd * D, derive(weight_seed, tensor_id(l, 2)), amp_proj);
-        gen(*pool_, Ly.o, 0, D * qd, derive(weight_seed, tensor_id(l, 3)), amp_out);
-        gen(*pool_, Ly.gu, 0, F_ * D, derive(weight_seed, tensor_id(l, 4)), amp_proj);
-        gen(*pool_, Ly.gu, F_ * D, F_ * D, derive(weight_seed, tensor_id(l, 5)), amp_proj);
-        gen(*pool_, Ly.dn, 0, D * F_, derive(weight_seed, tensor_id(l, 6)), amp_out);
+        std::vector<uint16_t> qkv(static_cast<size_t>(qd + 2 * kvd) * D), o(D * qd),
+            gu(2 * static_cast<size_t>(F_) * D), dn(D * F_);
+        gen(*pool_, qkv, 0, qd * D, derive(weight_seed, tensor_id(l, 0)), amp_proj);
+        gen(*pool_, qkv, qd * D, kvd * D, derive(weight_seed, tensor_id(l, 1)), amp_proj);
+        gen(*pool_, qkv, (qd + kvd) * D, kvd * D, derive(weight_seed, tensor_id(l, 2)), amp_proj);
+        gen(*pool_, o, 0, D * qd, derive(weight_seed, tensor_id(l, 3)), amp_out);
+        gen(*pool_, gu, 0, F_ * D, derive(weight_seed, tensor_id(l, 4)), amp_proj);
+        gen(*pool_, gu, F_ * D, F_ * D, derive(weight_seed, tensor_id(l, 5)), amp_proj);
+        gen(*pool_, dn, 0, D * F_, derive(weight_seed, tensor_id(l, 6)), amp_out);
+        Ly.qkv = quantize(qkv, qd + 2 * kvd, d_, *pool_);
+        Ly.o = quantize(o, d_, qd, *pool_);
+        Ly.gu = quantize(gu, 2 * F_, d_, *pool_);
+        Ly.dn = quantize(dn, d_, F_, *pool_);
     }
     kv_.assign(static_cast<size_t>(L_) * 2 * Hkv_ * max_seq_ * hd_, 0);
     const int half = hd_ / 2;
@@ -273,7 +343,7 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd_)));
     for (int l = 0; l < L_; ++l) {
         const DraftLayer& Ly = layers_[l];
-        matmul(*pool_, Ly.qkv.data(), rows, d_, hb_.data(), w, qkv_.data());
+        matmul(*pool_, Ly.qkv, hb_.data(), w, qkv_.data(), xq_, xs_);
         scale_rn(qkv_.data(), rows);
         for (int t = 0; t < w; ++t) {
             const int pos = n0 + t;
@@ -326,25 +396,25 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
                 for (int i = 0; i < hd_; ++i) ob_[t * qd + head * hd_ + i] = f2bf(acc[i] * inv);
             }
         });
-        matmul(*pool_, Ly.o.data(), d_, qd, ob_.data(), w, y_.data());
+        matmul(*pool_, Ly.o, ob_.data(), w, y_.data(), xq_, xs_);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
         }
-        matmul(*pool_, Ly.gu.data(), 2 * F_, d_, hb_.data(), w, gu_.data());
+        matmul(*pool_, Ly.gu, hb_.data(), w, gu_.data(), xq_, xs_);
         scale_rn(gu_.data(), 2 * F_);
         for (int t = 0; t < w; ++t)
             for (int f = 0; f < F_; ++f) {
                 const float g = gu_[t * 2 * F_ + f], u = gu_[t * 2 * F_ + F_ + f];
                 ab_[t * F_ + f] = f2bf(g / (1.0f + std::exp(-g)) * u);
             }
-        matmul(*pool_, Ly.dn.data(), d_, F_, ab_.data(), w, y_.data());
+        matmul(*pool_, Ly.dn, ab_.data(), w, y_.data(), xq_, xs_);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
         }
     }
-    matmul(*pool_, head_.data(), V_, d_, &hb_[(W - 1) * d_], 1, logits_last);
+    matmul(*pool_, head_, &hb_[(W - 1) * d_], 1, logits_last, xq_, xs_);
     for (int i = 0; i < V_; ++i) logits_last[i] *= rn[W - 1];
     tokens_.insert(tokens_.end(), toks, toks + w);
 }
@@ -438,7 +508,8 @@ int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_pl
                     int n_threads, const int* cpus, int n_cpus, dd_draft** out) {
     if (!desc || !out) return DD_E_ARG;
     *out = nullptr;
-    if (!__builtin_cpu_supports("avx512bf16")) return DD_E_ARG;  // single native path
+    if (!__builtin_cpu_supports("avx512vnni") || !__builtin_cpu_supports("avx512bw"))
+        return DD_E_ARG;  // single native path: AVX-512 VNNI
     const dd_model_desc& d = *desc;
     if (d.n_layers < 1 || d.d_model % 32 || d.ffn_dim % 32 || d.head_dim > 256 || d.max_seq < 2 ||
         d.n_heads % std::max(1, d.n_kv_heads))

@@ -33,8 +33,17 @@ class SpinPool {
     const std::function<void(int, int)>* job_ = nullptr;
 };
 
+// W8A8 weight matrix: per-row symmetric int8 (scale = max|w| / 127) plus the
+// row sums used by the unsigned-activation VNNI trick.
+struct QMat {
+    int rows = 0, cols = 0;
+    std::vector<int8_t> q;        // [rows][cols]
+    std::vector<float> scale;     // [rows]
+    std::vector<int32_t> rowsum;  // [rows] sum of q
+};
+
 struct DraftLayer {
-    std::vector<uint16_t> qkv, o, gu, dn;  // bf16 bits, row-major [out][in]
+    QMat qkv, o, gu, dn;  // row-major [out][in]
 };
 
 // Llama forward on host cores with a KV cache that follows the draft
@@ -59,7 +68,8 @@ class CpuLlama {
     void forward(const int32_t* toks, int w, float* logits_last);
     int L_, d_, H_, Hkv_, hd_, F_, V_, max_seq_;
     float eps_;
-    std::vector<uint16_t> emb_, head_;
+    std::vector<uint16_t> emb_;
+    QMat head_;
     std::vector<DraftLayer> layers_;
     std::vector<uint16_t> kv_;  // [L][2][Hkv][max_seq][hd] bf16
     std::vector<float> rope_cos_, rope_sin_;
@@ -68,6 +78,8 @@ class CpuLlama {
     // scratch
     std::vector<float> x_, qkv_, q_, o_, gu_, a_, y_, logits_tmp_;
     std::vector<uint16_t> hb_, ob_, ab_;
+    std::vector<uint8_t> xq_;  // quantised activations (u8 = q + 128)
+    std::vector<float> xs_;    // per-token activation scales
 };
 
 }  // namespace dd

@@ -96,7 +96,7 @@ def test_sps_and_duo_sampling_run(models, prompt):
 
 def test_draft_logits_vs_oracle(models, prompt):
     _, drf = models
-    orc = OracleLlama(DRAFT, weight_seed=22, plant=PLANT, max_seq=256, threads=8)
+    orc = OracleLlama(DRAFT, weight_seed=22, plant=PLANT, max_seq=256, threads=8, w8a8=True)
     o = orc.forward(prompt, last_only=True)[0]
     g = drf.logits(prompt)
     orc.close()
