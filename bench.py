@@ -37,6 +37,18 @@ import numpy as np  # noqa: E402
 
 SEED_W_TARGET, SEED_W_DRAFT = 1234, 99
 PROMPT_LEN, NEW_TOKENS = 128, 128
+# BASELINE.json configs: config2 (headline) = 128-token prompt, greedy;
+# config3 = 2K-token prompt, temperature 1.0 speculative sampling, up to 4 sequences
+WORKLOADS = {
+    "config2": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4,
+                    desc="config2: Llama-2-7B-shape bf16 target on 1 B200 per rank + "
+                         "Llama-68M-shape draft on pinned host cores, 128-token prompt, "
+                         "128 new tokens, greedy, DuoDecoding"),
+    "config3": dict(prompt_len=2048, greedy=False, temperature=1.0, max_sequences=4,
+                    desc="config3: Llama-2-7B-shape target, dynamic multi-sequence drafting "
+                         "(uncertainty-gated, up to 4 seqs), temperature 1.0 speculative "
+                         "sampling, 2K-token prompt, 128 new tokens"),
+}
 METRIC = ("decode tokens/sec (Llama-2-7B-shape target on B200 + Llama-68M-shape CPU draft, "
           "DuoDecoding, greedy)")
 
@@ -49,8 +61,9 @@ def splitmix(seed: int, m: int) -> int:
     return z ^ (z >> 31)
 
 
-def make_prompt(prompt_seed: int, n: int = PROMPT_LEN, vocab: int = 32000):
+def make_prompt(prompt_seed: int, n: int = None, vocab: int = 32000):
     """token_i = splitmix64(prompt_seed, i) mod V."""
+    n = PROMPT_LEN if n is None else n
     return [splitmix(prompt_seed, i + 1) % vocab for i in range(n)]
 
 
@@ -224,6 +237,9 @@ def run_ours(args):
     from paper_2503_00784_b200 import (DEFAULT_PLANT, SHAPES, Draft, EngineConfig, Target,
                                        calibrate, run_generation)
     plant = dict(DEFAULT_PLANT, alpha=args.alpha)
+    wl = WORKLOADS[args.workload]
+    global PROMPT_LEN
+    PROMPT_LEN = wl["prompt_len"]
     tcore, dcores = core_slice(rank, ws)
     os.sched_setaffinity(0, {tcore})  # target-role thread
     tgt = Target(SHAPES["llama2_7b"], weight_seed=SEED_W_TARGET, plant=plant,
@@ -234,8 +250,9 @@ def run_ours(args):
         budget, coef = args.budget, None
     else:
         coef, budget = calibrate(tgt, drf, probe_len=8, trials=12)
-    cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=args.max_sequences,
-                       max_new_tokens=NEW_TOKENS, greedy=True)
+    cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=wl["max_sequences"],
+                       max_new_tokens=NEW_TOKENS, greedy=wl["greedy"],
+                       temperature=wl["temperature"])
 
     def one(step):
         return run_generation(tgt, drf, make_prompt(1000 * rank + step + 1), cfg)
@@ -262,6 +279,10 @@ def run_ours(args):
     h2d = sum(r.h2d_bytes for r in results) / len(results)
     d2h = sum(r.d2h_bytes for r in results) / len(results)
     widths = [it.width for r in results for it in r.iterations]
+    seq_hist = {}
+    for r in results:
+        for it in r.iterations:
+            seq_hist[it.sequence_count] = seq_hist.get(it.sequence_count, 0) + 1
     tok_per_iter = statistics.mean(it.tokens_processed for r in results for it in r.iterations)
     if dist:
         import torch
@@ -300,13 +321,14 @@ def run_ours(args):
         # same-run GPU baselines: target-only AR and conventional SpS
         base = {}
         for mode, bud in (("vanilla", 2), ("sps", max(2, budget // 2))):
-            c2 = EngineConfig(mode=mode, budget=bud, max_new_tokens=NEW_TOKENS, greedy=True)
+            c2 = EngineConfig(mode=mode, budget=bud, max_new_tokens=NEW_TOKENS,
+                              greedy=wl["greedy"], temperature=wl["temperature"])
             r2 = run_generation(tgt, drf if mode != "vanilla" else None, make_prompt(1), c2)
             base[mode] = {"decode_tps": round(decode_stats(r2) / (first_decode_ms(r2) / 1e3), 1),
                           "tps_reference_style": round(r2.tps, 1),
                           "ttft_ms": round(r2.device_ttft_ms, 2), "budget": bud}
         extra["gpu_baselines"] = base
-        if ws == 1 and not args.no_cpu_baseline:
+        if ws == 1 and not args.no_cpu_baseline and args.workload == "config2":
             thr = os.cpu_count()
             os.sched_setaffinity(0, set(range(os.cpu_count())))
             rate, r, _ = cpu_decode_sample(SHAPES["llama2_7b"], SHAPES["llama_68m"], plant,
@@ -325,13 +347,13 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data":
                 "synthetic: seeded random-init weights (planted shared bigram, alpha recorded), "
                 "splitmix64 prompts",
-            "config": {"workload": "config2: Llama-2-7B-shape bf16 target on 1 B200 per rank + "
-                                   "Llama-68M-shape draft on pinned host cores, 128-token "
-                                   "prompt, 128 new tokens, greedy, DuoDecoding",
+            "config": {"workload": wl["desc"],
                        "model": "llama2_7b target / llama_68m draft", "global_batch": ws,
                        "seq_len": PROMPT_LEN + NEW_TOKENS, "parallelism": f"replicas{ws}",
                        "mode": args.mode, "budget": budget, "calibrated_c": coef,
-                       "max_sequences": args.max_sequences, "alpha": plant["alpha"],
+                       "max_sequences": wl["max_sequences"], "greedy": wl["greedy"],
+                       "temperature": wl["temperature"], "alpha": plant["alpha"],
+                       "seq_hist": seq_hist,
                        "draft_cores": len(dcores),
                        "l2": "weights 13.2 GB >> 126 MB L2: every pass re-streams from HBM"},
             "ttft_p50_ms": round(statistics.median(ttfts), 2),
@@ -365,7 +387,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="duo", choices=["duo", "sps", "vanilla"])
     ap.add_argument("--budget", type=int, default=0, help="0 = calibrate on this box")
-    ap.add_argument("--max-sequences", type=int, default=4)
+    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--cpu-tokens", type=int, default=16)
     ap.add_argument("--ref-tokens", type=int, default=8)

@@ -471,6 +471,43 @@ int CpuLlama::distribution(const float* lg, double temperature, bool greedy, flo
     return bi;
 }
 
+int CpuLlama::sample(const float* q, double u) {
+    const int nt = pool_->size();
+    std::vector<double> sums(nt, 0.0);
+    std::vector<int> last(nt, -1);
+    pool_->run([&](int tid, int n) {
+        const int lo = static_cast<int>(static_cast<int64_t>(V_) * tid / n);
+        const int hi = static_cast<int>(static_cast<int64_t>(V_) * (tid + 1) / n);
+        double acc = 0.0;
+        int ls = -1;
+        for (int i = lo; i < hi; ++i)
+            if (q[i] > 0.0f) {
+                acc += q[i];
+                ls = i;
+            }
+        sums[tid] = acc;
+        last[tid] = ls;
+    });
+    double prefix = 0.0;
+    int last_support = 0;
+    for (int t = 0; t < nt; ++t) {
+        if (last[t] >= 0) last_support = last[t];
+        if (sums[t] > 0.0 && u < prefix + sums[t]) {
+            const int lo = static_cast<int>(static_cast<int64_t>(V_) * t / nt);
+            const int hi = static_cast<int>(static_cast<int64_t>(V_) * (t + 1) / nt);
+            double acc = prefix;
+            for (int i = lo; i < hi; ++i) {
+                if (!(q[i] > 0.0f)) continue;
+                acc += q[i];
+                if (u < acc) return i;
+            }
+            return last[t];
+        }
+        prefix += sums[t];
+    }
+    return last_support;  // u in the rounding slack past the accumulated mass
+}
+
 void CpuLlama::top_k(const float* q, int k, int32_t* out) {
     // partial selection keeping "descending probability, then ascending id"
     // (ranked_tokens, proj/src/distribution.cpp:80-87) without a full sort

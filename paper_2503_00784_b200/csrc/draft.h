@@ -60,6 +60,9 @@ class CpuLlama {
     int distribution(const float* logits, double temperature, bool greedy, float* q);
     // indices of the k largest q (descending, ties ascending id)
     void top_k(const float* q, int k, int32_t* out);
+    // inverse-CDF sample of q with uniform u (distribution.cpp:61-78): pool
+    // chunk sums + a sequential walk of the crossing chunk
+    int sample(const float* q, double u);
     SpinPool& pool() { return *pool_; }
     int cached() const { return static_cast<int>(tokens_.size()); }
     std::string err;

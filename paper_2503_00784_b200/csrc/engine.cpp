@@ -158,7 +158,7 @@ Bundle draft_dynamic(DraftModel& dm, const std::vector<int32_t>& context, int bu
                 dp = d.data();
             }
             const double u = rng.next_uniform();
-            const int t = dm.greedy ? am : sample_f32(dp, V, u);
+            const int t = dm.greedy ? am : dm.m->sample(dp, u);
             seq.tokens.push_back(t);
             seq.dists.push_back(dm.greedy ? std::vector<float>() : std::vector<float>(dp, dp + V));
             ctx.push_back(t);
@@ -283,7 +283,7 @@ struct Runner {
             for (int k = 0; k < budget; ++k) {
                 const int am = dm.dist(c2, q.data());
                 const double u = rng_draft.next_uniform();
-                const int t = cfg.greedy ? am : sample_f32(q.data(), V, u);
+                const int t = cfg.greedy ? am : dm.m->sample(q.data(), u);
                 toks.push_back(t);
                 if (!cfg.greedy) dists.push_back(q);
                 c2.push_back(t);
