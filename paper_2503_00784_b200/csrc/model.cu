@@ -159,200 +159,150 @@ void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, con
 }
 
 // ------------------------------------------------------------ attention
-// Split-KV decode attention over the paged bf16 cache (flash-decoding style).
-// Grid (head, split, query group of 16).  Keys are cut into 64-key chunks by
-// ABSOLUTE position; split s owns chunks s, s+S, ...  A CTA stages each chunk's
-// K and V in shared memory once and uses them for all queries of its group
-// (online softmax), writes (m, l, o) partials, and the last-arriving split of
-// a (head, group) combines the S partials in split order.  The query at
-// absolute position p = n_cached + t attends keys 0..p (chain causal mask).
-// Every reduction order depends only on (head, position, chunk layout), so a
-// token's output is independent of the pass width (greedy determinism).
+// One CTA per (query head, new token): the query at absolute position
+// pos = n_cached + t attends to keys 0..pos (cached prefix + the chain of new
+// tokens up to itself).  Scores: one thread per key (16-byte K loads, q
+// broadcast from shared memory); PV: warp w takes keys w, w+4, ..., each lane
+// owns head_dim/32 output dims, then a fixed-order cross-warp sum.  The work
+// of a CTA depends only on (head, pos), so a token's output is independent of
+// the pass width.
 constexpr int kAttnThreads = 128;
-constexpr int kKeyChunk = 64;
-constexpr int kQGroup = 16;
-constexpr int kSplits = 8;
-
-struct AttnScratch {
-    float* part;      // [heads][groups][kSplits][kQGroup][hd + 2]
-    int* counters;    // [heads][groups]
-};
-
+constexpr int kAttnWarps = kAttnThreads / 32;
 __global__ void __launch_bounds__(kAttnThreads)
     attention_kernel(const PassState* ps, ModelDims m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                     int layer, float scale, __nv_bfloat16* o, AttnScratch scr) {
+                     int layer, float scale, __nv_bfloat16* o) {
+    extern __shared__ float scores[];  // [max_keys]
+    __shared__ float qs[256];
+    __shared__ float red[kAttnWarps];
+    __shared__ float part[kAttnThreads / 8][64];  // [KG][hd] with KG * hd = 16 * 128
     pdl_wait();
     pdl_launch();
-    extern __shared__ __align__(16) uint8_t att_smem[];
+    const int head = blockIdx.x, t = blockIdx.y;
+    const int pos = ps->n_cached + t;
+    const int n_keys = pos + 1;
     const int hd = m.head_dim;
-    const int head = blockIdx.x, split = blockIdx.y, grp = blockIdx.z;
-    const int w = ps->w, n0 = ps->n_cached;
-    const int q0 = grp * kQGroup;
-    const int nq = min(kQGroup, w - q0);
-    if (nq <= 0) return;
     const int kvh = head / (m.n_heads / m.n_kv_heads);
-    const int n_keys = n0 + q0 + nq;  // keys any query of this group may see
-    const int n_chunks = (n_keys + kKeyChunk - 1) / kKeyChunk;
-    const int tid = threadIdx.x;
-
-    __nv_bfloat16* sk = reinterpret_cast<__nv_bfloat16*>(att_smem);        // [64][hd]
-    __nv_bfloat16* sv = sk + kKeyChunk * hd;                                // [64][hd]
-    float* sq = reinterpret_cast<float*>(sv + kKeyChunk * hd);              // [16][hd]
-    float* sp = sq + kQGroup * hd;                                          // [16][64]
-    float* so = sp + kQGroup * kKeyChunk;                                   // [16][hd]
-    float* sm = so + kQGroup * hd;                                          // [16] running max
-    float* sl = sm + kQGroup;                                               // [16] running sum
-    __shared__ int s_last;
-
-    for (int i = tid; i < nq * hd; i += kAttnThreads) {
-        const int t = i / hd, d = i % hd;
-        sq[t * hd + d] = q[static_cast<size_t>(q0 + t) * m.q_dim() + head * hd + d];
-    }
-    for (int i = tid; i < kQGroup * hd; i += kAttnThreads) so[i] = 0.0f;
-    if (tid < kQGroup) {
-        sm[tid] = -INFINITY;
-        sl[tid] = 0.0f;
-    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < hd; i += kAttnThreads)
+        qs[i] = q[static_cast<size_t>(t) * m.q_dim() + head * hd + i];
     __syncthreads();
 
-    const int vec_per_row = hd / 8;  // 16-byte vectors per key row
-    for (int c = split; c < n_chunks; c += kSplits) {
-        const int k0 = c * kKeyChunk;
-        const int nk = min(kKeyChunk, n_keys - k0);
-        // stage K and V rows of this chunk (coalesced 16-byte loads)
-        for (int i = tid; i < nk * vec_per_row; i += kAttnThreads) {
-            const int j = i / vec_per_row, v = i % vec_per_row;
-            const int key = k0 + j;
-            const int page = page_table[key / page_size], slot = key % page_size;
-            const uint4* kr = reinterpret_cast<const uint4*>(
-                kv_pool + kv_offset(m, page_size, page, layer, 0, kvh, slot));
-            const uint4* vr = reinterpret_cast<const uint4*>(
-                kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot));
-            reinterpret_cast<uint4*>(sk + j * hd)[v] = __ldg(kr + v);
-            reinterpret_cast<uint4*>(sv + j * hd)[v] = __ldg(vr + v);
-        }
-        __syncthreads();
-        // scores for (query t, key j); masked keys -> -inf
-        for (int i = tid; i < nq * kKeyChunk; i += kAttnThreads) {
-            const int t = i / kKeyChunk, j = i % kKeyChunk;
-            const int key = k0 + j;
-            float sc = -INFINITY;
-            if (j < nk && key <= n0 + q0 + t) {
-                const float* qv = sq + t * hd;
-                const __nv_bfloat162* kr = reinterpret_cast<const __nv_bfloat162*>(sk + j * hd);
-                float acc = 0.0f;
-#pragma unroll 8
-                for (int d2 = 0; d2 < hd / 2; ++d2) {
-                    const float2 f = __bfloat1622float2(kr[d2]);
-                    acc = __fmaf_rn(qv[2 * d2], f.x, acc);
-                    acc = __fmaf_rn(qv[2 * d2 + 1], f.y, acc);
-                }
-                sc = __fmul_rn(acc, scale);
-            }
-            sp[t * kKeyChunk + j] = sc;
-        }
-        __syncthreads();
-        // online softmax update per query (rescale the running output)
-        if (tid < nq) {
-            const int t = tid;
-            float mx = sm[t];
-            for (int j = 0; j < kKeyChunk; ++j) mx = fmaxf(mx, sp[t * kKeyChunk + j]);
-            const float corr = mx == -INFINITY ? 1.0f : expf(sm[t] - mx);
-            float sum = 0.0f;
-            for (int j = 0; j < kKeyChunk; ++j) {
-                const float s2 = sp[t * kKeyChunk + j];
-                const float e = s2 == -INFINITY ? 0.0f : expf(s2 - mx);
-                sp[t * kKeyChunk + j] = e;
-                sum += e;
-            }
-            sl[t] = __fadd_rn(__fmul_rn(sl[t], corr), sum);
-            sm[t] = mx;
-            for (int d = 0; d < hd; ++d) so[t * hd + d] = __fmul_rn(so[t * hd + d], corr);
-        }
-        __syncthreads();
-        // o[t][d] += sum_j p[t][j] * V[j][d]; thread per dim, all queries of the group
-        for (int d = tid; d < hd; d += kAttnThreads) {
-            float acc[kQGroup];
+    // scores
+    float mx = -INFINITY;
+    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
+        const int page = page_table[key / page_size], slot = key % page_size;
+        const uint4* kr = reinterpret_cast<const uint4*>(
+            kv_pool + kv_offset(m, page_size, page, layer, 0, kvh, slot));
+        float acc = 0.0f;
+#pragma unroll 4
+        for (int c = 0; c < hd / 8; ++c) {
+            const uint4 v = __ldg(kr + c);
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-            for (int t = 0; t < kQGroup; ++t) acc[t] = 0.0f;
-            for (int j = 0; j < nk; ++j) {
-                const float v = __bfloat162float(sv[j * hd + d]);
-#pragma unroll
-                for (int t = 0; t < kQGroup; ++t)
-                    if (t < nq) acc[t] = __fmaf_rn(sp[t * kKeyChunk + j], v, acc[t]);
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(b2[j]);
+                acc = __fmaf_rn(qs[c * 8 + 2 * j], f.x, acc);
+                acc = __fmaf_rn(qs[c * 8 + 2 * j + 1], f.y, acc);
             }
-#pragma unroll
-            for (int t = 0; t < kQGroup; ++t)
-                if (t < nq) so[t * hd + d] = __fadd_rn(so[t * hd + d], acc[t]);
         }
-        __syncthreads();
+        const float sc = __fmul_rn(acc, scale);
+        scores[key] = sc;
+        mx = fmaxf(mx, sc);
     }
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int i = 1; i < kAttnWarps; ++i) mx = fmaxf(mx, red[i]);
+    __syncthreads();
+    float sum = 0.0f;
+    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
+        const float e = expf(scores[key] - mx);
+        scores[key] = e;
+        sum += e;
+    }
+    sum = warp_sum(sum);
+    if (lane == 0) red[warp] = sum;
+    __syncthreads();
+    sum = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kAttnWarps; ++i) sum += red[i];
+    const float inv = 1.0f / sum;
 
-    // partials -> workspace; last split combines in split order
-    const int groups = gridDim.z;
-    const size_t rec = static_cast<size_t>(hd) + 2;
-    float* part = scr.part + ((static_cast<size_t>(head) * groups + grp) * kSplits + split) * kQGroup * rec;
-    for (int i = tid; i < nq * hd; i += kAttnThreads) part[(i / hd) * rec + 2 + i % hd] = so[i];
-    if (tid < nq) {
-        part[tid * rec + 0] = sm[tid];
-        part[tid * rec + 1] = sl[tid];
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-        const int prev = atomicAdd(&scr.counters[head * groups + grp], 1);
-        s_last = (prev == kSplits - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    const float* base = scr.part + (static_cast<size_t>(head) * groups + grp) * kSplits * kQGroup * rec;
-    for (int i = tid; i < nq * hd; i += kAttnThreads) {
-        const int t = i / hd, d = i % hd;
-        float mx = -INFINITY;
-        for (int s2 = 0; s2 < kSplits; ++s2) mx = fmaxf(mx, __ldcg(base + (s2 * kQGroup + t) * rec));
-        float l = 0.0f, acc = 0.0f;
-        for (int s2 = 0; s2 < kSplits; ++s2) {
-            const float* r = base + (s2 * kQGroup + t) * rec;
-            const float ms = __ldcg(r);
-            if (ms == -INFINITY) continue;
-            const float f = expf(ms - mx);
-            l = __fmaf_rn(__ldcg(r + 1), f, l);
-            acc = __fmaf_rn(__ldcg(r + 2 + d), f, acc);
+    // PV: thread = (key group kg = tid / G, dim group dg = tid % G), G = hd / 8,
+    // 8 dims (one 16-byte load) per thread, keys kg, kg + 128/G, ...; then a
+    // fixed-order sum over key groups.
+    const int G = hd / 8;
+    const int KG = kAttnThreads / G;
+    const int kg = threadIdx.x / G, dg = threadIdx.x % G;
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    int key = kg;
+    for (; key + 3 * KG < n_keys; key += 4 * KG) {
+        uint4 v[4];
+        float p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int kk = key + u * KG;
+            const int page = page_table[kk / page_size], slot = kk % page_size;
+            v[u] = __ldg(reinterpret_cast<const uint4*>(
+                       kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
+            p[u] = scores[kk];
         }
-        o[static_cast<size_t>(q0 + t) * m.q_dim() + head * hd + d] =
-            __float2bfloat16_rn(__fdiv_rn(acc, l));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(b2[j]);
+                acc[2 * j] = __fmaf_rn(p[u], f.x, acc[2 * j]);
+                acc[2 * j + 1] = __fmaf_rn(p[u], f.y, acc[2 * j + 1]);
+            }
+        }
     }
-    if (tid == 0) scr.counters[head * groups + grp] = 0;
+    for (; key < n_keys; key += KG) {
+        const int page = page_table[key / page_size], slot = key % page_size;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(
+                            kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
+        const float p = scores[key];
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(b2[j]);
+            acc[2 * j] = __fmaf_rn(p, f.x, acc[2 * j]);
+            acc[2 * j + 1] = __fmaf_rn(p, f.y, acc[2 * j + 1]);
+        }
+    }
+    float* pv = &part[0][0];  // [KG][hd]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pv[kg * hd + dg * 8 + j] = acc[j];
+    __syncthreads();
+    for (int d0 = threadIdx.x; d0 < hd; d0 += kAttnThreads) {
+        float s2 = 0.0f;
+        for (int g2 = 0; g2 < KG; ++g2) s2 = __fadd_rn(s2, pv[g2 * hd + d0]);
+        o[static_cast<size_t>(t) * m.q_dim() + head * hd + d0] =
+            __float2bfloat16_rn(__fmul_rn(s2, inv));
+    }
 }
 
-static AttnScratch g_attn_scratch{nullptr, nullptr};
+static int g_attn_smem_bytes = 48 * 1024;
 
 void attention_set_max_keys(int max_keys) {
-    (void)max_keys;
-    const int hd = 256;  // upper bound for the smem carve-up
-    const int bytes = 2 * kKeyChunk * hd * 2 + (2 * kQGroup * hd + kQGroup * kKeyChunk + 2 * kQGroup) * 4;
-    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (!g_attn_scratch.part) {
-        const size_t groups = (kMaxPassTokens + kQGroup - 1) / kQGroup;
-        cudaMalloc(&g_attn_scratch.part,
-                   sizeof(float) * 64 * groups * kSplits * kQGroup * (256 + 2));  // <= 64 heads
-        cudaMalloc(&g_attn_scratch.counters, sizeof(int) * 64 * groups);
-        cudaMemset(g_attn_scratch.counters, 0, sizeof(int) * 64 * groups);
-    }
+    g_attn_smem_bytes = max_keys * static_cast<int>(sizeof(float));
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         g_attn_smem_bytes);
 }
 
 void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                       const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                       int layer, __nv_bfloat16* o, cudaStream_t s) {
-    const int groups = (w + kQGroup - 1) / kQGroup;
-    dim3 grid(m.n_heads, kSplits, groups);
-    const int hd = m.head_dim;
-    const int smem = 2 * kKeyChunk * hd * 2 + (2 * kQGroup * hd + kQGroup * kKeyChunk + 2 * kQGroup) * 4;
-    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(hd)));
-    launch_pdl(attention_kernel, grid, dim3(kAttnThreads), smem, s, ps, m, q, kv_pool, page_table,
-               page_size, layer, scale, o, g_attn_scratch);
+    dim3 grid(m.n_heads, w);
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(m.head_dim)));
+    launch_pdl(attention_kernel, grid, dim3(kAttnThreads), g_attn_smem_bytes, s, ps, m, q, kv_pool,
+               page_table, page_size, layer, scale, o);
 }
 
 // ------------------------------------------------------------ RMSNorm
