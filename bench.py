@@ -313,7 +313,7 @@ def run_ours(args):
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": (tr.get("dram_bytes_per_pass") if tr else None),
-            "kernel": "gemm_skinny_kernel (tcgen05 + TMA weight streaming, cluster split-K)",
+            "kernel": "gemm_sk_kernel (persistent stream-K tcgen05 + TMA weight streaming)",
             "launches_per_pass": n_launch, "algorithmic_bytes_per_pass": wb,
             "width": w_typ, "gemm_ms_per_pass": round(gemm_ms, 4), "peak_source": peak_src,
             "pass_ms": round(pass_ms, 4),
