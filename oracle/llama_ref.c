@@ -422,6 +422,28 @@ static void matmul(const uint16_t* W, int rows, int k, const float* x, int w, fl
 /* Deferred RMSNorm (mirrors the GPU pass): h = bf16(x * g) and the scale
  * r = 1/sqrt(mean(x^2) + eps) is applied to the consuming GEMM's fp32 output,
  * since W.(x*r*g) == r * (W.(x*g)).  Gains are 1. */
+/* Deterministic exp used by the W8A8 (CPU-draft) numerics: Cody-Waite range
+ * reduction + degree-6 Taylor polynomial, fp32 with fused multiply-adds.  The
+ * product CPU draft (paper_2503_00784_b200/csrc/draft.cpp dd_exp16) runs the
+ * same operations in AVX-512 lanes, so the two agree bit for bit. */
+static float orc_exp_poly(float x) {
+    x = fminf(fmaxf(x, -87.0f), 88.0f);
+    const float n = nearbyintf(x * 1.44269504f);
+    float r = fmaf(n, -0.693145751953125f, x);
+    r = fmaf(n, -1.428606765330187e-06f, r);
+    float p = 1.3888889e-03f;
+    p = fmaf(p, r, 8.3333333e-03f);
+    p = fmaf(p, r, 4.1666667e-02f);
+    p = fmaf(p, r, 1.6666667e-01f);
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    const int32_t e = ((int32_t)n + 127) << 23;
+    float sc;
+    memcpy(&sc, &e, 4);
+    return p * sc;
+}
+
 static float rmsnorm_bf(const float* x, int d, float eps, float* h) {
     float ss = 0.0f;
     for (int i = 0; i < d; ++i) ss = fmaf(x[i], x[i], ss);
@@ -459,9 +481,25 @@ static void attn_range(void* p, int64_t lo, int64_t hi) {
             if (sc[j] > mx) mx = sc[j];
         }
         float sum = 0.0f;
-        for (int j = 0; j < nk; ++j) {
-            sc[j] = expf(sc[j] - mx);
-            sum += sc[j];
+        if (m->quant) {
+            /* the CPU draft's order: 16 lane partials over full 16-key blocks,
+             * lanes summed 0..15, then the tail keys in order */
+            const int nb = nk & ~15;
+            float lanes[16] = {0};
+            for (int j = 0; j < nb; ++j) {
+                sc[j] = orc_exp_poly(sc[j] - mx);
+                lanes[j & 15] += sc[j];
+            }
+            for (int l = 0; l < 16; ++l) sum += lanes[l];
+            for (int j = nb; j < nk; ++j) {
+                sc[j] = orc_exp_poly(sc[j] - mx);
+                sum += sc[j];
+            }
+        } else {
+            for (int j = 0; j < nk; ++j) {
+                sc[j] = expf(sc[j] - mx);
+                sum += sc[j];
+            }
         }
         const float inv = 1.0f / sum;
         for (int i = 0; i < hd; ++i) {
@@ -538,7 +576,7 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
         for (int t = 0; t < w; ++t)
             for (int f = 0; f < F; ++f) {
                 const float g = y[(size_t)t * 2 * F + f], u = y[(size_t)t * 2 * F + F + f];
-                const float silu = g / (1.0f + expf(-g));
+                const float silu = g / (1.0f + (m->quant ? orc_exp_poly(-g) : expf(-g)));
                 a[(size_t)t * F + f] = bfr(silu * u);
             }
         if (m->quant) matmul_q(&Ly->qdn, a, w, y);

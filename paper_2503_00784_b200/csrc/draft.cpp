@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 
 #include "plant.h"
@@ -98,11 +99,11 @@ QMat quantize(const std::vector<uint16_t>& w, int rows, int cols, SpinPool& pool
 }
 
 // Per-token symmetric int8 activation quantisation, stored as u8 = q + 128.
-void quantize_acts(const uint16_t* X, int w, int k, std::vector<uint8_t>& xq,
+void quantize_acts(SpinPool& pool, const uint16_t* X, int w, int k, std::vector<uint8_t>& xq,
                    std::vector<float>& xs) {
     xq.resize(static_cast<size_t>(w) * k);
     xs.resize(w);
-    for (int t = 0; t < w; ++t) {
+    auto one = [&](int t) {
         const uint16_t* x = X + static_cast<size_t>(t) * k;
         float mx = 0.0f;
         for (int i = 0; i < k; ++i) mx = std::max(mx, std::fabs(bf2f(x[i])));
@@ -113,53 +114,84 @@ void quantize_acts(const uint16_t* X, int w, int k, std::vector<uint8_t>& xq,
             xq[static_cast<size_t>(t) * k + i] = static_cast<uint8_t>(v + 128);
         }
         xs[t] = sc;
+    };
+    if (w < 8) {
+        for (int t = 0; t < w; ++t) one(t);
+    } else {
+        pool.run([&](int tid, int nt) {
+            for (int t = tid; t < w; t += nt) one(t);
+        });
     }
 }
 
-// Y[t][n] = (sum_k xq[t][k] * q[n][k]) * (xs[t] * scale[n]); 8 rows per block
-// so eight independent vpdpbusd chains share each activation load.
+// Y[t][n] = (sum_k xq[t][k] * q[n][k]) * (xs[t] * scale[n]) for a block of
+// TB tokens x RB weight rows: TB*RB independent vpdpbusd chains, each
+// activation and weight load shared across the block (the weights of a row
+// block stay in L1 across the token blocks of a prefill).  Integer dots are
+// exact, so the blocking does not change any result.
+template <int TB, int RB>
+__attribute__((target("avx512f,avx512bw,avx512vnni"), always_inline)) inline void qdot_block(
+    const QMat& m, const uint8_t* xq, const float* xs, int t0, int n0, float* Y) {
+    const int k = m.cols;
+    __m512i acc[TB][RB];
+#pragma GCC unroll 8
+    for (int t = 0; t < TB; ++t)
+#pragma GCC unroll 8
+        for (int r = 0; r < RB; ++r) acc[t][r] = _mm512_setzero_si512();
+    for (int i = 0; i < k; i += 64) {
+        __m512i xv[TB];
+#pragma GCC unroll 8
+        for (int t = 0; t < TB; ++t)
+            xv[t] = _mm512_loadu_si512(xq + static_cast<size_t>(t0 + t) * k + i);
+#pragma GCC unroll 8
+        for (int r = 0; r < RB; ++r) {
+            const __m512i wv = _mm512_loadu_si512(&m.q[static_cast<size_t>(n0 + r) * k + i]);
+#pragma GCC unroll 8
+            for (int t = 0; t < TB; ++t) acc[t][r] = _mm512_dpbusd_epi32(acc[t][r], xv[t], wv);
+        }
+    }
+#pragma GCC unroll 8
+    for (int t = 0; t < TB; ++t)
+#pragma GCC unroll 8
+        for (int r = 0; r < RB; ++r) {
+            const int32_t dot = _mm512_reduce_add_epi32(acc[t][r]) - 128 * m.rowsum[n0 + r];
+            Y[static_cast<size_t>(t0 + t) * m.rows + n0 + r] =
+                static_cast<float>(dot) * (xs[t0 + t] * m.scale[n0 + r]);
+        }
+}
+
 __attribute__((target("avx512f,avx512bw,avx512vnni"))) void qdot_rows(
     const QMat& m, const uint8_t* xq, const float* xs, int w, int lo, int hi, float* Y) {
-    const int k = m.cols;
-    for (int t = 0; t < w; ++t) {
-        const uint8_t* x = xq + static_cast<size_t>(t) * k;
+    if (w >= 4) {
+        // prefill: 4 tokens x 6 rows (24 accumulators + 4 activations + 1 weight)
         int n = lo;
-        for (; n + 8 <= hi; n += 8) {
-            __m512i acc[8];
-#pragma GCC unroll 8
-            for (int r = 0; r < 8; ++r) acc[r] = _mm512_setzero_si512();
-            for (int i = 0; i < k; i += 64) {
-                const __m512i xv = _mm512_loadu_si512(x + i);
-#pragma GCC unroll 8
-                for (int r = 0; r < 8; ++r)
-                    acc[r] = _mm512_dpbusd_epi32(
-                        acc[r], xv, _mm512_loadu_si512(&m.q[static_cast<size_t>(n + r) * k + i]));
-            }
-#pragma GCC unroll 8
-            for (int r = 0; r < 8; ++r) {
-                const int32_t dot = _mm512_reduce_add_epi32(acc[r]) - 128 * m.rowsum[n + r];
-                Y[static_cast<size_t>(t) * m.rows + n + r] =
-                    static_cast<float>(dot) * (xs[t] * m.scale[n + r]);
-            }
+        for (; n + 6 <= hi; n += 6) {
+            int t = 0;
+            for (; t + 4 <= w; t += 4) qdot_block<4, 6>(m, xq, xs, t, n, Y);
+            for (; t < w; ++t) qdot_block<1, 6>(m, xq, xs, t, n, Y);
         }
         for (; n < hi; ++n) {
-            __m512i acc = _mm512_setzero_si512();
-            for (int i = 0; i < k; i += 64)
-                acc = _mm512_dpbusd_epi32(acc, _mm512_loadu_si512(x + i),
-                                          _mm512_loadu_si512(&m.q[static_cast<size_t>(n) * k + i]));
-            const int32_t dot = _mm512_reduce_add_epi32(acc) - 128 * m.rowsum[n];
-            Y[static_cast<size_t>(t) * m.rows + n] = static_cast<float>(dot) * (xs[t] * m.scale[n]);
+            int t = 0;
+            for (; t + 4 <= w; t += 4) qdot_block<4, 1>(m, xq, xs, t, n, Y);
+            for (; t < w; ++t) qdot_block<1, 1>(m, xq, xs, t, n, Y);
         }
+        return;
+    }
+    for (int t = 0; t < w; ++t) {
+        int n = lo;
+        for (; n + 8 <= hi; n += 8) qdot_block<1, 8>(m, xq, xs, t, n, Y);
+        for (; n < hi; ++n) qdot_block<1, 1>(m, xq, xs, t, n, Y);
     }
 }
 
 void matmul(SpinPool& pool, const QMat& m, const uint16_t* X, int w, float* Y,
             std::vector<uint8_t>& xq, std::vector<float>& xs) {
-    quantize_acts(X, w, m.cols, xq, xs);
-    const int blocks = (m.rows + 7) / 8;
+    quantize_acts(pool, X, w, m.cols, xq, xs);
+    const int gran = w >= 4 ? 6 : 8;
+    const int blocks = (m.rows + gran - 1) / gran;
     pool.run([&](int tid, int nt) {
-        const int lo = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * tid / nt) * 8);
-        const int hi = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * (tid + 1) / nt) * 8);
+        const int lo = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * tid / nt) * gran);
+        const int hi = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * (tid + 1) / nt) * gran);
         if (lo < hi) qdot_rows(m, xq.data(), xs.data(), w, lo, hi, Y);
     });
 }
@@ -278,7 +310,7 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
         Ly.gu = quantize(gu, 2 * F_, d_, *pool_);
         Ly.dn = quantize(dn, d_, F_, *pool_);
     }
-    kv_.assign(static_cast<size_t>(L_) * 2 * Hkv_ * max_seq_ * hd_, 0);
+    kv_.assign(static_cast<size_t>(L_) * 2 * Hkv_ * ((max_seq_ + 15) & ~15) * hd_, 0);
     const int half = hd_ / 2;
     rope_cos_.resize(static_cast<size_t>(max_seq_) * half);
     rope_sin_.resize(rope_cos_.size());
@@ -315,6 +347,149 @@ bool CpuLlama::logits(const int32_t* ctx, int n, float* out) {
     return true;
 }
 
+namespace {
+// Deterministic exp (Cody-Waite + degree-6 Taylor, fp32 FMA), 16 lanes; the
+// oracle's orc_exp_poly (oracle/llama_ref.c) is the same operation sequence
+// in scalar code, so draft and oracle agree bit for bit.
+__attribute__((target("avx512f"), always_inline)) inline __m512 dd_exp16(__m512 x) {
+    x = _mm512_min_ps(_mm512_max_ps(x, _mm512_set1_ps(-87.0f)), _mm512_set1_ps(88.0f));
+    const __m512 n = _mm512_roundscale_ps(_mm512_mul_ps(x, _mm512_set1_ps(1.44269504f)),
+                                          _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+    __m512 r = _mm512_fmadd_ps(n, _mm512_set1_ps(-0.693145751953125f), x);
+    r = _mm512_fmadd_ps(n, _mm512_set1_ps(-1.428606765330187e-06f), r);
+    __m512 p = _mm512_set1_ps(1.3888889e-03f);
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(8.3333333e-03f));
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(4.1666667e-02f));
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.6666667e-01f));
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(0.5f));
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f));
+    p = _mm512_fmadd_ps(p, r, _mm512_set1_ps(1.0f));
+    const __m512i e = _mm512_slli_epi32(
+        _mm512_add_epi32(_mm512_cvtps_epi32(n), _mm512_set1_epi32(127)), 23);
+    return _mm512_mul_ps(p, _mm512_castsi512_ps(e));
+}
+__attribute__((target("avx512f"))) float dd_exp1(float x) {
+    alignas(64) float t[16];
+    _mm512_store_ps(t, dd_exp16(_mm512_set1_ps(x)));
+    return t[0];
+}
+
+// 16 bf16 -> 16 fp32 (exact)
+__attribute__((target("avx512f,avx512bw"), always_inline)) inline __m512 load_bf16x16(
+    const uint16_t* p) {
+    const __m512i v = _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(p)));
+    return _mm512_castsi512_ps(_mm512_slli_epi32(v, 16));
+}
+
+// One (head, query) of causal attention over keys 0..nk-1.  K is stored in
+// 16-key blocks, dim-major inside a block (kt[pos/16][i][pos%16]) so 16 keys' scores are computed in 16 lanes, each
+// lane accumulating over the head dims in order: exactly the scalar
+// acc = fma(q[i], k[i], acc) chain of the oracle.  PV accumulates over keys in
+// order with the head dims in lanes.  Bit-identical to the scalar loop.
+__attribute__((target("avx512f,avx512bw"))) void attend_one(
+    const float* qv, const uint16_t* kt, const uint16_t* v, int nk, int hd, int max_seq,
+    float scale, std::vector<float>& sc, uint16_t* out) {
+    sc.resize(static_cast<size_t>(nk) + 16);
+    int j = 0;
+    const __m512 vs = _mm512_set1_ps(scale);
+    for (; j + 64 <= nk; j += 64) {  // four independent 16-key chains
+        const uint16_t* kb = kt + static_cast<size_t>(j) * hd;
+        const size_t bs = static_cast<size_t>(hd) * 16;
+        __m512 a0 = _mm512_setzero_ps(), a1 = a0, a2 = a0, a3 = a0;
+        for (int i = 0; i < hd; ++i) {
+            const __m512 qb = _mm512_set1_ps(qv[i]);
+            a0 = _mm512_fmadd_ps(qb, load_bf16x16(kb + i * 16), a0);
+            a1 = _mm512_fmadd_ps(qb, load_bf16x16(kb + bs + i * 16), a1);
+            a2 = _mm512_fmadd_ps(qb, load_bf16x16(kb + 2 * bs + i * 16), a2);
+            a3 = _mm512_fmadd_ps(qb, load_bf16x16(kb + 3 * bs + i * 16), a3);
+        }
+        _mm512_storeu_ps(&sc[j], _mm512_mul_ps(a0, vs));
+        _mm512_storeu_ps(&sc[j + 16], _mm512_mul_ps(a1, vs));
+        _mm512_storeu_ps(&sc[j + 32], _mm512_mul_ps(a2, vs));
+        _mm512_storeu_ps(&sc[j + 48], _mm512_mul_ps(a3, vs));
+    }
+    for (; j + 16 <= nk; j += 16) {
+        const uint16_t* kb = kt + static_cast<size_t>(j) * hd;  // block j/16
+        __m512 acc = _mm512_setzero_ps();
+        for (int i = 0; i < hd; ++i)
+            acc = _mm512_fmadd_ps(_mm512_set1_ps(qv[i]), load_bf16x16(kb + i * 16), acc);
+        _mm512_storeu_ps(&sc[j], _mm512_mul_ps(acc, _mm512_set1_ps(scale)));
+    }
+    for (; j < nk; ++j) {
+        float acc = 0.0f;
+        for (int i = 0; i < hd; ++i)
+            acc = std::fmaf(qv[i], bf2f(kt[static_cast<size_t>(j >> 4) * hd * 16 + i * 16 + (j & 15)]), acc);
+        sc[j] = acc * scale;
+    }
+    // max is order-free; the sum uses the oracle's fixed order: 16 lane
+    // partials over the full 16-key blocks, lanes added 0..15, then the tail
+    const int nb = nk & ~15;
+    float mx = -INFINITY;
+    {
+        __m512 vmx = _mm512_set1_ps(-INFINITY);
+        for (int jj = 0; jj < nb; jj += 16) vmx = _mm512_max_ps(vmx, _mm512_loadu_ps(&sc[jj]));
+        mx = _mm512_reduce_max_ps(vmx);
+        for (int jj = nb; jj < nk; ++jj) mx = std::max(mx, sc[jj]);
+    }
+    float sum = 0.0f;
+    {
+        const __m512 vm = _mm512_set1_ps(mx);
+        __m512 vsum = _mm512_setzero_ps();
+        for (int jj = 0; jj < nb; jj += 16) {
+            const __m512 e = dd_exp16(_mm512_sub_ps(_mm512_loadu_ps(&sc[jj]), vm));
+            _mm512_storeu_ps(&sc[jj], e);
+            vsum = _mm512_add_ps(vsum, e);
+        }
+        alignas(64) float lanes[16];
+        _mm512_store_ps(lanes, vsum);
+        for (int l = 0; l < 16; ++l) sum += lanes[l];
+        for (int jj = nb; jj < nk; ++jj) {
+            sc[jj] = dd_exp1(sc[jj] - mx);
+            sum += sc[jj];
+        }
+    }
+    const float inv = 1.0f / sum;
+    if (hd % 16 == 0 && hd <= 256) {
+        __m512 acc[16];
+        const int nv = hd / 16;
+        for (int c = 0; c < nv; ++c) acc[c] = _mm512_setzero_ps();
+        for (int jj = 0; jj < nk; ++jj) {
+            const __m512 p = _mm512_set1_ps(sc[jj]);
+            const uint16_t* vr = v + static_cast<size_t>(jj) * hd;
+            for (int c = 0; c < nv; ++c) acc[c] = _mm512_fmadd_ps(p, load_bf16x16(vr + 16 * c), acc[c]);
+        }
+        alignas(64) float tmp[256];
+        for (int c = 0; c < nv; ++c) _mm512_store_ps(tmp + 16 * c, acc[c]);
+        for (int i = 0; i < hd; ++i) out[i] = f2bf(tmp[i] * inv);
+    } else {
+        float acc[256];
+        for (int i = 0; i < hd; ++i) acc[i] = 0.0f;
+        for (int jj = 0; jj < nk; ++jj) {
+            const uint16_t* vr = v + static_cast<size_t>(jj) * hd;
+            for (int i = 0; i < hd; ++i) acc[i] = std::fmaf(sc[jj], bf2f(vr[i]), acc[i]);
+        }
+        for (int i = 0; i < hd; ++i) out[i] = f2bf(acc[i] * inv);
+    }
+}
+// a[f] = bf16(silu(g) * u), g = gu[f] * r, u = gu[F + f] * r (oracle order)
+__attribute__((target("avx512f"))) void swiglu_row(const float* gu, float r, int F, uint16_t* a) {
+    const __m512 vr = _mm512_set1_ps(r), one = _mm512_set1_ps(1.0f);
+    alignas(64) float tmp[16];
+    int f = 0;
+    for (; f + 16 <= F; f += 16) {
+        const __m512 g = _mm512_mul_ps(_mm512_loadu_ps(gu + f), vr);
+        const __m512 u = _mm512_mul_ps(_mm512_loadu_ps(gu + F + f), vr);
+        const __m512 e = dd_exp16(_mm512_sub_ps(_mm512_setzero_ps(), g));
+        _mm512_store_ps(tmp, _mm512_mul_ps(_mm512_div_ps(g, _mm512_add_ps(one, e)), u));
+        for (int i = 0; i < 16; ++i) a[f + i] = f2bf(tmp[i]);
+    }
+    for (; f < F; ++f) {
+        const float g = gu[f] * r, u = gu[F + f] * r;
+        a[f] = f2bf(g / (1.0f + dd_exp1(-g)) * u);
+    }
+}
+}  // namespace
+
 void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     const int n0 = static_cast<int>(tokens_.size());
     const int qd = H_ * hd_, kvd = Hkv_ * hd_, rows = qd + 2 * kvd, half = hd_ / 2;
@@ -328,28 +503,44 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     ab_.resize(W * F_);
     y_.resize(W * std::max(d_, 2 * F_));
     std::vector<float> rn(W);
-    auto scale_rn = [&](float* y, int n) {
-        for (int t = 0; t < w; ++t)
-            for (int i = 0; i < n; ++i) y[static_cast<size_t>(t) * n + i] *= rn[t];
+    // per-token elementwise work: on the pool for prefill-sized w
+    auto per_token = [&](const std::function<void(int)>& fn) {
+        if (w < 8) {
+            for (int t = 0; t < w; ++t) fn(t);
+        } else {
+            pool_->run([&](int tid, int nt) {  // contiguous chunks: no false sharing
+                const int lo = w * tid / nt, hi = w * (tid + 1) / nt;
+                for (int t = lo; t < hi; ++t) fn(t);
+            });
+        }
     };
-    for (int t = 0; t < w; ++t) {
+    per_token([&](int t) {
         for (int i = 0; i < d_; ++i)
             x_[t * d_ + i] = bf2f(emb_[static_cast<size_t>(toks[t]) * d_ + i]);
         rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
-    }
-    auto kvp = [&](int l, int kv, int h, int pos) {
-        return &kv_[((((static_cast<size_t>(l) * 2 + kv) * Hkv_ + h) * max_seq_) + pos) * hd_];
+    });
+    const size_t ms16 = static_cast<size_t>((max_seq_ + 15) & ~15);
+    // K in 16-key blocks, dim-major inside a block: [l][h][pos/16][i][16];
+    // V row-major [l][h][pos][i]
+    auto ktp = [&](int l, int h) {
+        return &kv_[((static_cast<size_t>(l) * 2 + 0) * Hkv_ + h) * ms16 * hd_];
+    };
+    auto kt_at = [&](int i, int pos) {
+        return static_cast<size_t>(pos >> 4) * hd_ * 16 + static_cast<size_t>(i) * 16 + (pos & 15);
+    };
+    auto vp = [&](int l, int h, int pos) {
+        return &kv_[(((static_cast<size_t>(l) * 2 + 1) * Hkv_ + h) * ms16 + pos) * hd_];
     };
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd_)));
     for (int l = 0; l < L_; ++l) {
         const DraftLayer& Ly = layers_[l];
         matmul(*pool_, Ly.qkv, hb_.data(), w, qkv_.data(), xq_, xs_);
-        scale_rn(qkv_.data(), rows);
-        for (int t = 0; t < w; ++t) {
+        per_token([&](int t) {
+            float* r = &qkv_[static_cast<size_t>(t) * rows];
+            for (int i = 0; i < rows; ++i) r[i] *= rn[t];
             const int pos = n0 + t;
             const float* cs = &rope_cos_[static_cast<size_t>(pos) * half];
             const float* sn = &rope_sin_[static_cast<size_t>(pos) * half];
-            const float* r = &qkv_[t * rows];
             for (int head = 0; head < H_ + Hkv_; ++head)
                 for (int i = 0; i < half; ++i) {
                     const float av = r[head * hd_ + i], bv = r[head * hd_ + i + half];
@@ -359,60 +550,39 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
                         q_[t * qd + head * hd_ + i] = lo;
                         q_[t * qd + head * hd_ + i + half] = hi;
                     } else {
-                        uint16_t* kd = kvp(l, 0, head - H_, pos);
-                        kd[i] = f2bf(lo);
-                        kd[i + half] = f2bf(hi);
+                        uint16_t* kt = ktp(l, head - H_);
+                        kt[kt_at(i, pos)] = f2bf(lo);
+                        kt[kt_at(i + half, pos)] = f2bf(hi);
                     }
                 }
-            for (int e = 0; e < kvd; ++e) kvp(l, 1, e / hd_, pos)[e % hd_] = f2bf(r[qd + kvd + e]);
-        }
+            for (int e = 0; e < kvd; ++e) vp(l, e / hd_, pos)[e % hd_] = f2bf(r[qd + kvd + e]);
+        });
         pool_->run([&](int tid, int nt) {
             std::vector<float> sc;
-            for (int job = tid; job < H_ * w; job += nt) {
-                const int head = job / w, t = job % w;
-                const int pos = n0 + t, nk = pos + 1, kvh = head / (H_ / Hkv_);
-                const float* qv = &q_[t * qd + head * hd_];
-                sc.resize(nk);
-                float mx = -INFINITY;
-                for (int j = 0; j < nk; ++j) {
-                    const uint16_t* kr = kvp(l, 0, kvh, j);
-                    float acc = 0.0f;
-                    for (int i = 0; i < hd_; ++i) acc = std::fmaf(qv[i], bf2f(kr[i]), acc);
-                    sc[j] = acc * scale;
-                    mx = std::max(mx, sc[j]);
-                }
-                float sum = 0.0f;
-                for (int j = 0; j < nk; ++j) {
-                    sc[j] = std::exp(sc[j] - mx);
-                    sum += sc[j];
-                }
-                const float inv = 1.0f / sum;
-                float acc[256];
-                for (int i = 0; i < hd_; ++i) acc[i] = 0.0f;
-                for (int j = 0; j < nk; ++j) {
-                    const uint16_t* vr = kvp(l, 1, kvh, j);
-                    for (int i = 0; i < hd_; ++i) acc[i] = std::fmaf(sc[j], bf2f(vr[i]), acc[i]);
-                }
-                for (int i = 0; i < hd_; ++i) ob_[t * qd + head * hd_ + i] = f2bf(acc[i] * inv);
+            const int jobs = H_ * w;
+            // balance the causal triangle: long (late) queries first, strided
+            for (int jb = tid; jb < jobs; jb += nt) {
+                const int job = jobs - 1 - jb;
+                const int t = job / H_, head = job % H_;
+                const int pos = n0 + t, kvh = head / (H_ / Hkv_);
+                attend_one(&q_[t * qd + head * hd_], ktp(l, kvh), vp(l, kvh, 0), pos + 1, hd_,
+                           max_seq_, scale, sc, &ob_[t * qd + head * hd_]);
             }
         });
         matmul(*pool_, Ly.o, ob_.data(), w, y_.data(), xq_, xs_);
-        for (int t = 0; t < w; ++t) {
+        per_token([&](int t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
-        }
+        });
         matmul(*pool_, Ly.gu, hb_.data(), w, gu_.data(), xq_, xs_);
-        scale_rn(gu_.data(), 2 * F_);
-        for (int t = 0; t < w; ++t)
-            for (int f = 0; f < F_; ++f) {
-                const float g = gu_[t * 2 * F_ + f], u = gu_[t * 2 * F_ + F_ + f];
-                ab_[t * F_ + f] = f2bf(g / (1.0f + std::exp(-g)) * u);
-            }
+        per_token([&](int t) {
+            swiglu_row(&gu_[static_cast<size_t>(t) * 2 * F_], rn[t], F_, &ab_[static_cast<size_t>(t) * F_]);
+        });
         matmul(*pool_, Ly.dn, ab_.data(), w, y_.data(), xq_, xs_);
-        for (int t = 0; t < w; ++t) {
+        per_token([&](int t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
-        }
+        });
     }
     matmul(*pool_, head_, &hb_[(W - 1) * d_], 1, logits_last, xq_, xs_);
     for (int i = 0; i < V_; ++i) logits_last[i] *= rn[W - 1];

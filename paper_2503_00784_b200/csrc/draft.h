@@ -74,7 +74,7 @@ class CpuLlama {
     std::vector<uint16_t> emb_;
     QMat head_;
     std::vector<DraftLayer> layers_;
-    std::vector<uint16_t> kv_;  // [L][2][Hkv][max_seq][hd] bf16
+    std::vector<uint16_t> kv_;  // K: [L][Hkv][max_seq/16][hd][16] (16-key blocks, dim-major inside), V: [L][Hkv][max_seq][hd]; bf16
     std::vector<float> rope_cos_, rope_sin_;
     std::vector<int32_t> tokens_;  // tokens whose K/V are cached
     std::unique_ptr<SpinPool> pool_;

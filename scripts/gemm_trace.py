@@ -9,10 +9,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2503_00784_b200 import SHAPES, Target, _lib  # noqa: E402
 
 t = Target(SHAPES["llama2_7b"], weight_seed=1, max_seq=512)
-t.prefill(list(range(64)))
+t.prefill(list(range(64)))  # context
 names = ["qkv", "o", "gate_up", "down", "head"]
 for which in range(5):
-    for w in (1, 16):
+    for w in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16").split(",")]:
         buf = (C.c_uint64 * (8 * 4096))()
         n = C.c_int()
         rc = _lib.lib().dd_debug_gemm_trace(t.h, which, w, buf, 4096, C.byref(n))

@@ -39,3 +39,14 @@ def test_draft_logits_match_oracle(draft):
 
 def test_draft_time_token(draft):
     assert draft.time_token(10) > 0.0
+
+
+def test_draft_prefill_bit_exact(draft):
+    """Long prefill (token-blocked VNNI matmuls, 16-lane attention and the
+    deterministic exp) equals the oracle's W8A8 mode bit for bit."""
+    orc = OracleLlama(SHAPE, weight_seed=31, plant=PLANT, max_seq=256, threads=4, w8a8=True)
+    ctx = np.random.default_rng(2).integers(0, SHAPE["vocab"], 230).tolist()
+    o = orc.forward(ctx)
+    for n in (230, 3, 120, 229):
+        assert np.array_equal(draft.logits(ctx[:n]), o[n - 1]), n
+    orc.close()
