@@ -472,11 +472,15 @@ static void attn_range(void* p, int64_t lo, int64_t hi) {
         const int kvh = head / (H / Hkv);
         const float* qv = a->q + (size_t)t * qd + head * hd;
         float* sc = (float*)malloc(sizeof(float) * nk);
+        /* the GPU target feeds bf16(q) to its tensor-core QK^T (attention.cu);
+         * the CPU draft (W8A8 mode) keeps q in fp32 */
+        float qr[256];
+        for (int i = 0; i < hd; ++i) qr[i] = m->quant ? qv[i] : bfr(qv[i]);
         float mx = -INFINITY;
         for (int j = 0; j < nk; ++j) {
             const uint16_t* kr = m->kv + kv_idx(m, l, 0, kvh, j);
             float acc = 0.0f;
-            for (int i = 0; i < hd; ++i) acc = fmaf(qv[i], bf2f(kr[i]), acc);
+            for (int i = 0; i < hd; ++i) acc = fmaf(qr[i], bf2f(kr[i]), acc);
             sc[j] = acc * a->scale;
             if (sc[j] > mx) mx = sc[j];
         }

@@ -1,0 +1,408 @@
+// Split-KV causal attention over the paged bf16 KV cache, on tensor cores
+// (mma.sync m16n8k16 bf16 -> fp32), for every pass width (decode W <= 32 and
+// prefill chunks up to 256 tokens).
+//
+// Grid = (kRanks, query tiles of 16 new tokens, query heads); the kRanks CTAs
+// of one (head, tile) form a thread-block cluster.  Keys are cut into splits
+// of 128 at absolute positions; rank r takes splits r, r + kRanks, ... .  Per
+// split the CTA stages K and V (128 keys) in shared memory with cp.async
+// (16-byte chunks, XOR-swizzled so the fragment reads are conflict-free),
+// then every warp computes the full S = QK^T of the split (16 rows x 128
+// keys) and the online softmax (fp32, exp2 domain) - identical in the four
+// warps - and warp w accumulates O for its quarter of the head dims.  No
+// merge across warps is needed.  Fragments use two permutations:
+//  * QK^T: the head dims are permuted inside each 32-dim chunk so that lane
+//    quad c reads K[key][32ch + 8c .. +8] as one 16-byte chunk (the Q
+//    fragments use the same permutation, so the dot products are unchanged);
+//  * PV: lane group g supplies column g of the warp's n-tiles, mapped to the
+//    NTW contiguous dims w*HD/4 + g*NTW + e, so one 8-byte (4-byte) read per
+//    key feeds every n-tile; pairs are packed with byte permutes.
+// Ranks merge through distributed shared memory (rank order).  Work placement
+// depends only on absolute key positions and query rows are independent, so a
+// token's output does not depend on the pass width (tests/test_gpu_kernels).
+#include "common.cuh"
+#include "model.h"
+
+namespace dd {
+
+namespace {
+
+constexpr int kSplitKeys = 128;
+constexpr int kRanks = 8;  // CTAs per cluster (portable maximum)
+constexpr int kAttnCtaThreads = 128;
+constexpr int kQTile = 16;
+
+__device__ __forceinline__ void pdl_wait_() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// 16-byte global -> shared copy; src_bytes = 0 zero-fills without reading
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// K row `key`, 16-byte chunk `ch` (8 dims) -> swizzled chunk
+__device__ __forceinline__ int k_chunk(int key, int ch) { return ch ^ (key & 7); }
+// V: move key pairs across the 128-byte bank window
+template <int HD>
+__device__ __forceinline__ int v_chunk(int key, int ch) {
+    return ch ^ (((key >> 1) & 3) << (HD == 128 ? 2 : 1));
+}
+
+template <int HD>
+struct AttnSmem {
+    __nv_bfloat16 k[kSplitKeys][HD];
+    __nv_bfloat16 v[kSplitKeys][HD];
+    float res_o[kQTile][HD];  // this CTA's unnormalised O, read by the cluster
+    float res_m[kQTile];
+    float res_l[kQTile];
+};
+
+}  // namespace
+
+#ifdef DD_ATTN_TRACE  // timing harness only (scripts/micro/attn_bench.cu)
+__device__ unsigned long long* g_attn_trace = nullptr;
+#define ATT_STAMP(k)                                                                       \
+    do {                                                                                   \
+        if (g_attn_trace && threadIdx.x == 0) {                                            \
+            unsigned long long t_;                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+            const int b_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);  \
+            if (b_ < 4096) g_attn_trace[b_ * 16 + (k)] = t_;                               \
+        }                                                                                  \
+    } while (0)
+void attention_set_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)); }
+#else
+#define ATT_STAMP(k) \
+    do {             \
+    } while (0)
+#endif
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnCtaThreads)
+    attn_cluster_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
+                        const __nv_bfloat16* __restrict__ kv_pool,
+                        const int32_t* __restrict__ page_table, int page_size, int layer,
+                        float scale_log2, __nv_bfloat16* __restrict__ o) {
+    constexpr int NCH = HD / 32;      // 32-dim chunks of QK^T (2 k-steps each)
+    constexpr int CHK = HD / 8;       // 16-byte chunks per K/V row
+    constexpr int DW = HD / 4;        // output dims per warp
+    constexpr int NTW = DW / 8;       // output n-tiles per warp (4 or 2)
+    constexpr int NJ = kSplitKeys / 8;  // S n-tiles per split (16)
+    extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+    AttnSmem<HD>& sm = *reinterpret_cast<AttnSmem<HD>*>(attn_smem_raw);
+    ATT_STAMP(0);
+    pdl_wait_();
+    pdl_launch_();
+    const int rank = static_cast<int>(cluster_ctarank());
+    const int qt = blockIdx.y, head = blockIdx.z;
+    const int n0 = ps->n_cached, W = ps->w;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, c = lane & 3;
+    const int kvh = head / (md.n_heads / md.n_kv_heads);
+    const int qd = md.q_dim();
+    const int tid = threadIdx.x;
+
+    const bool tile_live = qt * kQTile < W;
+    const int t_hi = min(W, (qt + 1) * kQTile);  // exclusive
+    const int kmax = n0 + t_hi - 1;               // last key any row of the tile may see
+    const int n_split = tile_live ? kmax / kSplitKeys + 1 : 0;
+    const int pos_g = n0 + qt * kQTile + g, pos_g8 = pos_g + 8;  // this lane's two rows
+    const bool v_g = qt * kQTile + g < W, v_g8 = qt * kQTile + g + 8 < W;
+
+    float acc[NTW][4];
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+    float m_g = -INFINITY, m_g8 = -INFINITY, l_g = 0.f, l_g8 = 0.f;
+
+    ATT_STAMP(1);
+    if (rank < n_split) {
+        // Q fragments (bf16, permuted dims), rows g and g + 8
+        uint32_t qa[NCH][4], qb[NCH][4];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            const int d0 = head * HD + ch * 32 + c * 8;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+            if (v_g) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    q + static_cast<size_t>(qt * kQTile + g) * qd + d0);
+                a0 = src[0];
+                a1 = src[1];
+            }
+            if (v_g8) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    q + static_cast<size_t>(qt * kQTile + g + 8) * qd + d0);
+                b0 = src[0];
+                b1 = src[1];
+            }
+            qa[ch][0] = pack_bf16(a0.x, a0.y);
+            qa[ch][1] = pack_bf16(a0.z, a0.w);
+            qa[ch][2] = pack_bf16(a1.x, a1.y);
+            qa[ch][3] = pack_bf16(a1.z, a1.w);
+            qb[ch][0] = pack_bf16(b0.x, b0.y);
+            qb[ch][1] = pack_bf16(b0.z, b0.w);
+            qb[ch][2] = pack_bf16(b1.x, b1.y);
+            qb[ch][3] = pack_bf16(b1.z, b1.w);
+        }
+#pragma unroll 1
+        for (int split = rank; split < n_split; split += kRanks) {
+            const int kb = split * kSplitKeys;
+            // ---- stage the split's K and V (zero-filled past kmax)
+#pragma unroll 4
+            for (int idx = tid; idx < kSplitKeys * CHK; idx += kAttnCtaThreads) {
+                const int kk = idx / CHK, ch = idx % CHK;
+                const int key = kb + kk;
+                const bool ok = key <= kmax;
+                const int kc = ok ? key : 0;
+                const size_t base =
+                    kv_offset(md, page_size, page_table[kc / page_size], layer, 0, kvh, kc % page_size);
+                const __nv_bfloat16* ksrc = kv_pool + base + ch * 8;
+                const __nv_bfloat16* vsrc = kv_pool +
+                    kv_offset(md, page_size, page_table[kc / page_size], layer, 1, kvh, kc % page_size) + ch * 8;
+                cp_async16(&sm.k[kk][k_chunk(kk, ch) * 8], ksrc, ok ? 16u : 0u);
+                cp_async16(&sm.v[kk][v_chunk<HD>(kk, ch) * 8], vsrc, ok ? 16u : 0u);
+            }
+            cp_async_wait_all();
+            __syncthreads();
+            ATT_STAMP(2);
+            // ---- S = Q K^T for the 128 keys (16 n-tiles of 8)
+            float s[NJ][4];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+                const int kk = 8 * j + g;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const uint4 kr = *reinterpret_cast<const uint4*>(&sm.k[kk][k_chunk(kk, 4 * ch + c) * 8]);
+                    const uint32_t a0[4] = {qa[ch][0], qb[ch][0], qa[ch][1], qb[ch][1]};
+                    mma_bf16(s[j], a0, kr.x, kr.y);
+                    const uint32_t a1[4] = {qa[ch][2], qb[ch][2], qa[ch][3], qb[ch][3]};
+                    mma_bf16(s[j], a1, kr.z, kr.w);
+                }
+            }
+            // ---- online softmax (log2 domain), causal mask per row
+            float mx_g = -INFINITY, mx_g8 = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int key = kb + 8 * j + 2 * c + e;
+                    s[j][e] = key <= pos_g ? s[j][e] * scale_log2 : -INFINITY;
+                    s[j][2 + e] = key <= pos_g8 ? s[j][2 + e] * scale_log2 : -INFINITY;
+                    mx_g = fmaxf(mx_g, s[j][e]);
+                    mx_g8 = fmaxf(mx_g8, s[j][2 + e]);
+                }
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                mx_g = fmaxf(mx_g, __shfl_xor_sync(0xffffffffu, mx_g, off));
+                mx_g8 = fmaxf(mx_g8, __shfl_xor_sync(0xffffffffu, mx_g8, off));
+            }
+            const float mn_g = fmaxf(m_g, mx_g), mn_g8 = fmaxf(m_g8, mx_g8);
+            const float base_g = mn_g == -INFINITY ? 0.f : mn_g;
+            const float base_g8 = mn_g8 == -INFINITY ? 0.f : mn_g8;
+            const float cr_g = fast_exp2(m_g - base_g), cr_g8 = fast_exp2(m_g8 - base_g8);
+            m_g = mn_g;
+            m_g8 = mn_g8;
+            l_g *= cr_g;
+            l_g8 *= cr_g8;
+#pragma unroll
+            for (int t = 0; t < NTW; ++t) {
+                acc[t][0] *= cr_g;
+                acc[t][1] *= cr_g;
+                acc[t][2] *= cr_g8;
+                acc[t][3] *= cr_g8;
+            }
+            uint32_t pa[NJ / 2][4];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                const float p0 = fast_exp2(s[j][0] - base_g), p1 = fast_exp2(s[j][1] - base_g);
+                const float p2 = fast_exp2(s[j][2] - base_g8), p3 = fast_exp2(s[j][3] - base_g8);
+                l_g += p0 + p1;
+                l_g8 += p2 + p3;
+                pa[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
+                pa[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
+            }
+            // ---- O[:, warp's dims] += P V
+            const int dbyte = (warp * DW + g * NTW) * 2;  // within the row
+#pragma unroll
+            for (int ks = 0; ks < NJ / 2; ++ks) {
+                uint32_t vw[4][NTW / 2];  // keys 2c, 2c+1, 2c+8, 2c+9: NTW dims each
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int kk = 16 * ks + 2 * c + (r & 1) + (r >> 1) * 8;
+                    const int ch = v_chunk<HD>(kk, dbyte >> 4);
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(&sm.v[kk][0]) + ch * 16 + (dbyte & 15);
+                    if (NTW == 4) {
+                        const uint2 x = *reinterpret_cast<const uint2*>(src);
+                        vw[r][0] = x.x;
+                        vw[r][NTW / 2 - 1] = x.y;
+                    } else {
+                        vw[r][0] = *reinterpret_cast<const uint32_t*>(src);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < NTW; ++e) {
+                    const uint32_t sel = (e & 1) ? 0x7632 : 0x5410;
+                    const uint32_t b0 = __byte_perm(vw[0][e >> 1], vw[1][e >> 1], sel);
+                    const uint32_t b1 = __byte_perm(vw[2][e >> 1], vw[3][e >> 1], sel);
+                    mma_bf16(acc[e], pa[ks], b0, b1);
+                }
+            }
+            __syncthreads();  // the next split overwrites K / V
+        }
+    }
+    ATT_STAMP(3);
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
+        l_g8 += __shfl_xor_sync(0xffffffffu, l_g8, off);
+    }
+    // C fragment column 2c (2c+1) of n-tile e -> dim warp*DW + (2c)*NTW + e
+    const int dcol = warp * DW + 2 * c * NTW;
+    if (n_split <= 1) {  // uniform over the cluster: rank 0 alone finishes
+        if (rank == 0 && n_split == 1) {
+            const float ig = 1.0f / l_g, ig8 = 1.0f / l_g8;
+            const size_t og = static_cast<size_t>(qt * kQTile + g) * qd + head * HD;
+            const size_t og8 = og + static_cast<size_t>(8) * qd;
+#pragma unroll
+            for (int e = 0; e < NTW; ++e) {
+                if (v_g) {
+                    o[og + dcol + e] = __float2bfloat16_rn(acc[e][0] * ig);
+                    o[og + dcol + NTW + e] = __float2bfloat16_rn(acc[e][1] * ig);
+                }
+                if (v_g8) {
+                    o[og8 + dcol + e] = __float2bfloat16_rn(acc[e][2] * ig8);
+                    o[og8 + dcol + NTW + e] = __float2bfloat16_rn(acc[e][3] * ig8);
+                }
+            }
+        }
+        return;
+    }
+    // ---- cluster merge (rank order) through DSMEM; rank r finishes rows r, r + 8
+#pragma unroll
+    for (int e = 0; e < NTW; ++e) {
+        sm.res_o[g][dcol + e] = acc[e][0];
+        sm.res_o[g][dcol + NTW + e] = acc[e][1];
+        sm.res_o[g + 8][dcol + e] = acc[e][2];
+        sm.res_o[g + 8][dcol + NTW + e] = acc[e][3];
+    }
+    if (warp == 0 && c == 0) {
+        sm.res_m[g] = m_g;
+        sm.res_m[g + 8] = m_g8;
+        sm.res_l[g] = l_g;
+        sm.res_l[g + 8] = l_g8;
+    }
+    ATT_STAMP(4);
+    cluster_sync();
+    ATT_STAMP(5);
+    {
+        constexpr int kRowsPerRank = kQTile / kRanks;  // 2
+        constexpr int kThreadsPerRow = kAttnCtaThreads / kRowsPerRank;
+        const int r = rank + kRanks * (tid / kThreadsPerRow);
+        const int t = qt * kQTile + r;
+        if (t < W) {
+            const uint32_t a_m = smem_u32(&sm.res_m[r]), a_l = smem_u32(&sm.res_l[r]);
+            float mj[kRanks], lj[kRanks];
+            const int nr = min(n_split, kRanks);
+#pragma unroll
+            for (int j = 0; j < kRanks; ++j) {
+                mj[j] = j < nr ? ld_dsmem_f32(dsmem_addr(a_m, j)) : -INFINITY;
+                lj[j] = j < nr ? ld_dsmem_f32(dsmem_addr(a_l, j)) : 0.f;
+            }
+            float M = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kRanks; ++j) M = fmaxf(M, mj[j]);
+            float L = 0.f, f[kRanks];
+#pragma unroll
+            for (int j = 0; j < kRanks; ++j) {
+                f[j] = mj[j] == -INFINITY ? 0.f : fast_exp2(mj[j] - M);
+                L += lj[j] * f[j];
+            }
+            const float inv = 1.0f / L;
+            for (int d = tid % kThreadsPerRow; d < HD; d += kThreadsPerRow) {
+                const uint32_t a_o = smem_u32(&sm.res_o[r][d]);
+                float v[kRanks];
+#pragma unroll
+                for (int j = 0; j < kRanks; ++j) v[j] = j < nr ? ld_dsmem_f32(dsmem_addr(a_o, j)) : 0.f;
+                float O = 0.f;
+#pragma unroll
+                for (int j = 0; j < kRanks; ++j) O += v[j] * f[j];
+                o[static_cast<size_t>(t) * qd + head * HD + d] = __float2bfloat16_rn(O * inv);
+            }
+        }
+    }
+    ATT_STAMP(6);
+    cluster_sync();  // keep this CTA's shared memory alive until every rank has read it
+    ATT_STAMP(7);
+}
+
+int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
+                     const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                     int layer, __nv_bfloat16* o, cudaStream_t s) {
+    const int qtiles = (w + kQTile - 1) / kQTile;
+    const float scale_log2 =
+        static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(m.head_dim)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kRanks, qtiles, m.n_heads);
+    cfg.blockDim = dim3(kAttnCtaThreads, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kRanks;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (m.head_dim == 128) {
+        static bool attr = false;
+        cfg.dynamicSmemBytes = sizeof(AttnSmem<128>);
+        if (!attr) {
+            cudaFuncSetAttribute(attn_cluster_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(AttnSmem<128>)));
+            attr = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, attn_cluster_kernel<128>, ps, m, q, kv_pool, page_table,
+                               page_size, layer, scale_log2, o);
+    } else if (m.head_dim == 64) {
+        static bool attr = false;
+        cfg.dynamicSmemBytes = sizeof(AttnSmem<64>);
+        if (!attr) {
+            cudaFuncSetAttribute(attn_cluster_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(AttnSmem<64>)));
+            attr = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, attn_cluster_kernel<64>, ps, m, q, kv_pool, page_table,
+                               page_size, layer, scale_log2, o);
+    } else {
+        return -1;
+    }
+    return e == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace dd

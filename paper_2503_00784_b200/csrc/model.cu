@@ -158,153 +158,6 @@ void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, con
     launch_pdl(embed_norm_kernel, dim3(w), dim3(256), 0, s, ps, emb, gain, d, eps, x, h, ss);
 }
 
-// ------------------------------------------------------------ attention
-// One CTA per (query head, new token): the query at absolute position
-// pos = n_cached + t attends to keys 0..pos (cached prefix + the chain of new
-// tokens up to itself).  Scores: one thread per key (16-byte K loads, q
-// broadcast from shared memory); PV: warp w takes keys w, w+4, ..., each lane
-// owns head_dim/32 output dims, then a fixed-order cross-warp sum.  The work
-// of a CTA depends only on (head, pos), so a token's output is independent of
-// the pass width.
-constexpr int kAttnThreads = 128;
-constexpr int kAttnWarps = kAttnThreads / 32;
-__global__ void __launch_bounds__(kAttnThreads)
-    attention_kernel(const PassState* ps, ModelDims m, const float* q,
-                     const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                     int layer, float scale, __nv_bfloat16* o) {
-    extern __shared__ float scores[];  // [max_keys]
-    __shared__ float qs[256];
-    __shared__ float red[kAttnWarps];
-    __shared__ float part[kAttnThreads / 8][64];  // [KG][hd] with KG * hd = 16 * 128
-    pdl_wait();
-    pdl_launch();
-    const int head = blockIdx.x, t = blockIdx.y;
-    const int pos = ps->n_cached + t;
-    const int n_keys = pos + 1;
-    const int hd = m.head_dim;
-    const int kvh = head / (m.n_heads / m.n_kv_heads);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < hd; i += kAttnThreads)
-        qs[i] = q[static_cast<size_t>(t) * m.q_dim() + head * hd + i];
-    __syncthreads();
-
-    // scores
-    float mx = -INFINITY;
-    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
-        const int page = page_table[key / page_size], slot = key % page_size;
-        const uint4* kr = reinterpret_cast<const uint4*>(
-            kv_pool + kv_offset(m, page_size, page, layer, 0, kvh, slot));
-        float acc = 0.0f;
-#pragma unroll 4
-        for (int c = 0; c < hd / 8; ++c) {
-            const uint4 v = __ldg(kr + c);
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 f = __bfloat1622float2(b2[j]);
-                acc = __fmaf_rn(qs[c * 8 + 2 * j], f.x, acc);
-                acc = __fmaf_rn(qs[c * 8 + 2 * j + 1], f.y, acc);
-            }
-        }
-        const float sc = __fmul_rn(acc, scale);
-        scores[key] = sc;
-        mx = fmaxf(mx, sc);
-    }
-    mx = warp_max(mx);
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    mx = red[0];
-#pragma unroll
-    for (int i = 1; i < kAttnWarps; ++i) mx = fmaxf(mx, red[i]);
-    __syncthreads();
-    float sum = 0.0f;
-    for (int key = threadIdx.x; key < n_keys; key += kAttnThreads) {
-        const float e = expf(scores[key] - mx);
-        scores[key] = e;
-        sum += e;
-    }
-    sum = warp_sum(sum);
-    if (lane == 0) red[warp] = sum;
-    __syncthreads();
-    sum = 0.0f;
-#pragma unroll
-    for (int i = 0; i < kAttnWarps; ++i) sum += red[i];
-    const float inv = 1.0f / sum;
-
-    // PV: thread = (key group kg = tid / G, dim group dg = tid % G), G = hd / 8,
-    // 8 dims (one 16-byte load) per thread, keys kg, kg + 128/G, ...; then a
-    // fixed-order sum over key groups.
-    const int G = hd / 8;
-    const int KG = kAttnThreads / G;
-    const int kg = threadIdx.x / G, dg = threadIdx.x % G;
-    float acc[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-    int key = kg;
-    for (; key + 3 * KG < n_keys; key += 4 * KG) {
-        uint4 v[4];
-        float p[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int kk = key + u * KG;
-            const int page = page_table[kk / page_size], slot = kk % page_size;
-            v[u] = __ldg(reinterpret_cast<const uint4*>(
-                       kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
-            p[u] = scores[kk];
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 f = __bfloat1622float2(b2[j]);
-                acc[2 * j] = __fmaf_rn(p[u], f.x, acc[2 * j]);
-                acc[2 * j + 1] = __fmaf_rn(p[u], f.y, acc[2 * j + 1]);
-            }
-        }
-    }
-    for (; key < n_keys; key += KG) {
-        const int page = page_table[key / page_size], slot = key % page_size;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(
-                            kv_pool + kv_offset(m, page_size, page, layer, 1, kvh, slot)) + dg);
-        const float p = scores[key];
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float2 f = __bfloat1622float2(b2[j]);
-            acc[2 * j] = __fmaf_rn(p, f.x, acc[2 * j]);
-            acc[2 * j + 1] = __fmaf_rn(p, f.y, acc[2 * j + 1]);
-        }
-    }
-    float* pv = &part[0][0];  // [KG][hd]
-#pragma unroll
-    for (int j = 0; j < 8; ++j) pv[kg * hd + dg * 8 + j] = acc[j];
-    __syncthreads();
-    for (int d0 = threadIdx.x; d0 < hd; d0 += kAttnThreads) {
-        float s2 = 0.0f;
-        for (int g2 = 0; g2 < KG; ++g2) s2 = __fadd_rn(s2, pv[g2 * hd + d0]);
-        o[static_cast<size_t>(t) * m.q_dim() + head * hd + d0] =
-            __float2bfloat16_rn(__fmul_rn(s2, inv));
-    }
-}
-
-static int g_attn_smem_bytes = 48 * 1024;
-
-void attention_set_max_keys(int max_keys) {
-    g_attn_smem_bytes = max_keys * static_cast<int>(sizeof(float));
-    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         g_attn_smem_bytes);
-}
-
-void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
-                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                      int layer, __nv_bfloat16* o, cudaStream_t s) {
-    dim3 grid(m.n_heads, w);
-    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(m.head_dim)));
-    launch_pdl(attention_kernel, grid, dim3(kAttnThreads), g_attn_smem_bytes, s, ps, m, q, kv_pool,
-               page_table, page_size, layer, scale, o);
-}
-
 // ------------------------------------------------------------ RMSNorm
 // h[t] = bf16(x[t] * rsqrt(mean(x[t]^2) + eps) * g); one CTA per token row.
 __global__ void rmsnorm_kernel(const float* x, int d, const float* gain, float eps,

@@ -48,10 +48,11 @@ void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
                        int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s);
-void launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
-                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                      int layer, __nv_bfloat16* o, cudaStream_t s);
-void attention_set_max_keys(int max_keys);
+// Split-KV tensor-core attention with a cluster/DSMEM merge (attention.cu);
+// returns 0, or nonzero for an unsupported head_dim / launch failure.
+int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
+                     const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                     int layer, __nv_bfloat16* o, cudaStream_t s);
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s);
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,

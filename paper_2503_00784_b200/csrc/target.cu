@@ -109,8 +109,9 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         eq.kind = kEpiQkvRope;
         eq.layer = l;
         CK(gemm(kGQkv, L.qkv, &ctx->map_h, eq));
-        launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size, l,
-                         ctx->o, s);
+        if (launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table,
+                             ctx->page_size, l, ctx->o, s))
+            return ctx_fail(ctx, DD_E_CUDA, "attention launch failed");
         mark(1);
         GemmEpiParams er = e;  // residual add; writes u = bf16(x*g) + ss partials
         er.kind = kEpiResidual;
@@ -223,10 +224,10 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     if (d.n_layers < 1 || d.d_model % 128 || d.head_dim % 32 || d.head_dim > 256 ||
         d.n_heads % std::max(1, d.n_kv_heads) || d.ffn_dim % 128 || d.vocab % 128 ||
         (d.n_heads * d.head_dim) % 128 || (std::max(1, d.n_kv_heads) * d.head_dim) % 128 ||
-        128 % d.head_dim || d.max_seq < 1)
+        (d.head_dim != 64 && d.head_dim != 128) || d.max_seq < 1)
         return ctx_fail(nullptr, DD_E_ARG,
                         "unsupported shape (d_model, ffn_dim, vocab must be multiples of 128; "
-                        "head_dim 32/64/128; q and kv widths multiples of 128)");
+                        "head_dim 64/128; q and kv widths multiples of 128)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cuda_device)
         return ctx_fail(nullptr, DD_E_CUDA, "no CUDA device available (no CPU fallback exists)");
@@ -307,7 +308,6 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     CK(cudaMalloc(&ctx->page_table, sizeof(int32_t) * ctx->n_pages));
     CK(cudaMemcpy(ctx->page_table, pt.data(), sizeof(int32_t) * ctx->n_pages,
                   cudaMemcpyHostToDevice));
-    attention_set_max_keys(ctx->max_seq);
 
     // RoPE tables in double precision -> fp32 (shared with the oracle)
     const int half = m.head_dim / 2;
