@@ -1,3 +1,4 @@
-mkdir -p gpurun_out
-ncu --set full --clock-control none --import-source on -k regex:attn -s 40 -c 1 -o gpurun_out/attn128_full python scripts/one_pass.py 8 128 > gpurun_out/attn_full.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:attn -s 300 -c 1 -o gpurun_out/attn2k_full python scripts/one_pass.py 8 2048 >> gpurun_out/attn_full.log 2>&1
+timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout -s KILL 120 python scripts/pass_timeline.py 8 128 2>&1 | grep -v cta | tail -12
+timeout -s KILL 120 python scripts/pass_ab.py 1,8,32 128
+DD_PASS_PREFETCH=0 timeout -s KILL 120 python scripts/pass_ab.py 8 128

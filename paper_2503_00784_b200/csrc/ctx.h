@@ -12,6 +12,7 @@
 #include "../../include/duodec_b200.h"
 #include "gemm.h"
 #include "model.h"
+#include "pass.h"
 #include "plant.h"
 
 namespace dd {
@@ -74,6 +75,19 @@ struct dd_ctx {
     int32_t* d_tail = nullptr;
     double* d_probs = nullptr;
     size_t probs_cap = 0;
+
+    // persistent pass kernel (pass.cu)
+    bool use_pass_kernel = true;     // DD_PASS_KERNEL=0: one launch per GEMM / attention
+    int epoch = 0;                   // pass sequence number (flag value)
+    int* pass_flags = nullptr;       // [flags][kFlagReplicas] x 128-byte lines
+    size_t pass_flag_count = 0;
+    float* pass_ws = nullptr;        // 2 x stream-K partials (alternating GEMM phases)
+    int* pass_counters = nullptr;    // 2 x [512] segment arrival counters
+    size_t pass_ws_half = 0;         // floats per half
+    float* attn_part = nullptr;      // attention chunk-group partials
+    int* attn_cnt = nullptr;
+    std::map<int, dd::PassPhase*> pass_phases;  // key: w * 2 + want_logits (device arrays)
+    std::map<int, int> pass_nphases;
 
     int n_cached = 0;
     int last_w = 0;  // width of the last scored pass with logits (0 = none)

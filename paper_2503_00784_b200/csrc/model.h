@@ -33,7 +33,8 @@ constexpr int kMaxPassTokens = 256;
 struct PassState {
     int n_cached;  // tokens already in the KV cache (absolute position of row 0)
     int w;         // tokens in this pass
-    int pad[2];
+    int epoch;     // pass sequence number (dataflow flags of the persistent pass kernel)
+    int pad;
     int32_t tokens[kMaxPassTokens];
 };
 

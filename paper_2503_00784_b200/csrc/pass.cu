@@ -1,0 +1,1077 @@
+// Persistent whole-pass kernel for the target verification pass (sm_100a).
+//
+// One cooperative launch of 148 CTAs (one per SM) runs the whole scored pass:
+// embedding, then per layer QKV GEMM -> attention -> O GEMM -> gate/up GEMM ->
+// down GEMM, then the LM head.  Kernel boundaries are replaced by tile-level
+// dataflow flags in global memory (value = the pass epoch): an output tile's
+// epilogue publishes its flag with release semantics, and the activation
+// producer of the next phase acquires the flag of exactly the tile that feeds
+// the k-block it is about to load.  Weights never depend on activations, so
+// the weight producer streams the next phase's weights into the shared-memory
+// ring while the previous phase drains - the HBM stream does not stop at
+// phase boundaries.
+//
+// Warp roles (256 threads):
+//   warp 0  weight producer: one 16 KiB cp.async.bulk per k-block (pre-tiled,
+//           pre-swizzled weights, evict-first)
+//   warp 1  MMA issuer: tcgen05.mma (M=128 weight rows, N=nt tokens, K=16)
+//           into one of two TMEM accumulators
+//   warp 2  activation producer: waits the producing tile's flag, then TMA
+//           (128B swizzle) of the k-block's activation tile
+//   warp 3  idle
+//   warps 4-7 epilogue (tcgen05.ld; stream-K segment reduction; fused RoPE +
+//           paged-KV append / residual + deferred-RMSNorm / SwiGLU / logits),
+//           the embedding phase and the attention phase.
+// The stream-K partition of each GEMM (gemm_epi.cuh) depends only on its shape,
+// attention work placement only on absolute key positions, and every
+// reduction has a fixed order: a token's logits are identical whatever the
+// pass width.  Deadlock freedom needs all CTAs co-resident: the launch is
+// cooperative with one CTA per SM.
+#include "common.cuh"
+#include "gemm_epi.cuh"
+#include "pass.h"
+
+#include <cstdlib>
+#include <cstring>
+
+namespace dd {
+
+using namespace gemm_dev;
+
+// debug seam: per-CTA progress words in mapped host memory (dd_debug_pass_progress)
+__device__ volatile int* g_pass_dbg = nullptr;
+#define PASS_DBG(slot, val)                                                      \
+    do {                                                                         \
+        if (g_pass_dbg) g_pass_dbg[blockIdx.x * 8 + (slot)] = (val);             \
+    } while (0)
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void pass_put(const PassParams& P, int p, int k, unsigned long long v) {
+    if (P.trace) P.trace[(static_cast<size_t>(blockIdx.x) * P.n_phases + p) * 12 + k] = v;
+}
+__device__ __forceinline__ void pass_stamp(const PassParams& P, int p, int k) {
+    if (P.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[(static_cast<size_t>(blockIdx.x) * P.n_phases + p) * 12 + k] = t;
+    }
+}
+
+namespace {
+
+constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// replica `rep` of flag (base + idx)
+__device__ __forceinline__ int* flag_at(int* flags, int base, int idx, int rep) {
+    return flags + (static_cast<size_t>(base + idx) * kFlagReplicas + rep) * kFlagStride;
+}
+// the replica this CTA polls
+__device__ __forceinline__ int* flag_poll(int* flags, int base, int idx) {
+    return flag_at(flags, base, idx, blockIdx.x % kFlagReplicas);
+}
+__device__ __forceinline__ void st_release_flag(int* flags, int base, int idx, int v);
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_release_flag(int* flags, int base, int idx, int v) {
+    st_release(flag_at(flags, base, idx, 0), v);  // release orders the replicas after the data
+#pragma unroll
+    for (int r = 1; r < kFlagReplicas; ++r)
+        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_at(flags, base, idx, r)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const int* p, int epoch) {
+    while (ld_acquire(p) - epoch < 0) __nanosleep(32);
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- attention
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ void mma_bf16(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ int k_chunk(int key, int ch) { return ch ^ (key & 7); }
+template <int HD>
+__device__ __forceinline__ int v_chunk(int key, int ch) {
+    return ch ^ (((key >> 1) & 3) << (HD == 128 ? 2 : 1));
+}
+
+// One attention item: (head, 16-query tile, chunk group) over 64-key chunks
+// grp, grp + kAttnGroups, ... (absolute positions), run by the 128 epilogue
+// threads.  K and V of a chunk are staged in shared memory (swizzled); every
+// warp computes S = QK^T for the chunk (16 x 64) and the online softmax, and
+// warp w accumulates O for its quarter of the head dims (mma.sync m16n8k16).
+// Groups merge through global partials; the last-arriving group combines them
+// in group order and publishes the (head, tile) flag.
+template <int HD>
+__device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_smem, int* s_bcast,
+                          int head, int qt, int grp, int epoch, int tid) {
+    constexpr int NCH = HD / 32;
+    constexpr int CHK = HD / 8;
+    constexpr int DW = HD / 4;
+    constexpr int NTW = DW / 8;
+    constexpr int NJ = kAttnChunk / 8;
+    const ModelDims& md = P.m;
+    const int n0 = P.ps->n_cached, W = P.ps->w;
+    const int t_hi = min(W, (qt + 1) * 16);
+    const int kmax = n0 + t_hi - 1;
+    const int n_chunks = kmax / kAttnChunk + 1;
+    const int active = min(n_chunks, kAttnGroups);
+    const int warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, c = lane & 3;
+    const int kvh = head / (md.n_heads / md.n_kv_heads);
+    const int qd = md.q_dim();
+    __nv_bfloat16(*ks)[HD] = reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem);
+    __nv_bfloat16(*vs)[HD] = reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + kAttnChunk * HD * 2);
+
+    // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
+    if (tid < 3) {  // q, k and v tiles polled in parallel
+        const int row = tid == 0 ? head * HD : tid == 1 ? qd + kvh * HD : qd + md.kv_dim() + kvh * HD;
+        wait_flag(flag_poll(P.flags, ph.qkv_flag, row / 128), epoch);
+    }
+    epi_bar();
+
+    const int pos_g = n0 + qt * 16 + g, pos_g8 = pos_g + 8;
+    const bool v_g = qt * 16 + g < W, v_g8 = qt * 16 + g + 8 < W;
+    uint32_t qa[NCH][4], qb[NCH][4];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int d0 = head * HD + ch * 32 + c * 8;
+        float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+        if (v_g) {
+            const float4* src = reinterpret_cast<const float4*>(P.q + static_cast<size_t>(qt * 16 + g) * qd + d0);
+            a0 = __ldcg(src);
+            a1 = __ldcg(src + 1);
+        }
+        if (v_g8) {
+            const float4* src = reinterpret_cast<const float4*>(P.q + static_cast<size_t>(qt * 16 + g + 8) * qd + d0);
+            b0 = __ldcg(src);
+            b1 = __ldcg(src + 1);
+        }
+        qa[ch][0] = pack_bf16(a0.x, a0.y);
+        qa[ch][1] = pack_bf16(a0.z, a0.w);
+        qa[ch][2] = pack_bf16(a1.x, a1.y);
+        qa[ch][3] = pack_bf16(a1.z, a1.w);
+        qb[ch][0] = pack_bf16(b0.x, b0.y);
+        qb[ch][1] = pack_bf16(b0.z, b0.w);
+        qb[ch][2] = pack_bf16(b1.x, b1.y);
+        qb[ch][3] = pack_bf16(b1.z, b1.w);
+    }
+    float acc[NTW][4];
+#pragma unroll
+    for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+    float m_g = -INFINITY, m_g8 = -INFINITY, l_g = 0.f, l_g8 = 0.f;
+
+    for (int chunk = grp; chunk < n_chunks; chunk += kAttnGroups) {
+        const int kb = chunk * kAttnChunk;
+        for (int idx = tid; idx < kAttnChunk * CHK; idx += 128) {
+            const int kk = idx / CHK, ch = idx % CHK;
+            const int key = kb + kk;
+            const bool ok = key <= kmax;
+            const int kc = ok ? key : 0;
+            const int page = P.page_table[kc / P.page_size], slot = kc % P.page_size;
+            cp_async16(&ks[kk][k_chunk(kk, ch) * 8],
+                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 0, kvh, slot) + ch * 8,
+                       ok ? 16u : 0u);
+            cp_async16(&vs[kk][v_chunk<HD>(kk, ch) * 8],
+                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot) + ch * 8,
+                       ok ? 16u : 0u);
+        }
+        cp_async_wait_all();
+        epi_bar();
+        float s[NJ][4];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+            const int kk = 8 * j + g;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+                const uint4 kr = *reinterpret_cast<const uint4*>(&ks[kk][k_chunk(kk, 4 * ch + c) * 8]);
+                const uint32_t a0[4] = {qa[ch][0], qb[ch][0], qa[ch][1], qb[ch][1]};
+                mma_bf16(s[j], a0, kr.x, kr.y);
+                const uint32_t a1[4] = {qa[ch][2], qb[ch][2], qa[ch][3], qb[ch][3]};
+                mma_bf16(s[j], a1, kr.z, kr.w);
+            }
+        }
+        float mx_g = -INFINITY, mx_g8 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = kb + 8 * j + 2 * c + e;
+                s[j][e] = key <= pos_g ? s[j][e] * P.scale_log2 : -INFINITY;
+                s[j][2 + e] = key <= pos_g8 ? s[j][2 + e] * P.scale_log2 : -INFINITY;
+                mx_g = fmaxf(mx_g, s[j][e]);
+                mx_g8 = fmaxf(mx_g8, s[j][2 + e]);
+            }
+#pragma unroll
+        for (int off = 1; off <= 2; off <<= 1) {
+            mx_g = fmaxf(mx_g, __shfl_xor_sync(0xffffffffu, mx_g, off));
+            mx_g8 = fmaxf(mx_g8, __shfl_xor_sync(0xffffffffu, mx_g8, off));
+        }
+        const float mn_g = fmaxf(m_g, mx_g), mn_g8 = fmaxf(m_g8, mx_g8);
+        const float base_g = mn_g == -INFINITY ? 0.f : mn_g;
+        const float base_g8 = mn_g8 == -INFINITY ? 0.f : mn_g8;
+        const float cr_g = fast_exp2(m_g - base_g), cr_g8 = fast_exp2(m_g8 - base_g8);
+        m_g = mn_g;
+        m_g8 = mn_g8;
+        l_g *= cr_g;
+        l_g8 *= cr_g8;
+#pragma unroll
+        for (int t = 0; t < NTW; ++t) {
+            acc[t][0] *= cr_g;
+            acc[t][1] *= cr_g;
+            acc[t][2] *= cr_g8;
+            acc[t][3] *= cr_g8;
+        }
+        uint32_t pa[NJ / 2][4];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const float p0 = fast_exp2(s[j][0] - base_g), p1 = fast_exp2(s[j][1] - base_g);
+            const float p2 = fast_exp2(s[j][2] - base_g8), p3 = fast_exp2(s[j][3] - base_g8);
+            l_g += p0 + p1;
+            l_g8 += p2 + p3;
+            pa[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
+            pa[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
+        }
+        const int dbyte = (warp * DW + g * NTW) * 2;
+#pragma unroll
+        for (int kst = 0; kst < NJ / 2; ++kst) {
+            uint32_t vw[4][2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int kk = 16 * kst + 2 * c + (r & 1) + (r >> 1) * 8;
+                const int chn = v_chunk<HD>(kk, dbyte >> 4);
+                const uint8_t* src = reinterpret_cast<const uint8_t*>(&vs[kk][0]) + chn * 16 + (dbyte & 15);
+                if constexpr (NTW == 4) {
+                    const uint2 xv = *reinterpret_cast<const uint2*>(src);
+                    vw[r][0] = xv.x;
+                    vw[r][1] = xv.y;
+                } else {
+                    vw[r][0] = *reinterpret_cast<const uint32_t*>(src);
+                    vw[r][1] = 0;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < NTW; ++e) {
+                const uint32_t sel = (e & 1) ? 0x7632 : 0x5410;
+                const uint32_t b0 = __byte_perm(vw[0][e >> 1], vw[1][e >> 1], sel);
+                const uint32_t b1 = __byte_perm(vw[2][e >> 1], vw[3][e >> 1], sel);
+                mma_bf16(acc[e], pa[kst], b0, b1);
+            }
+        }
+        epi_bar();  // the next chunk overwrites K / V
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
+        l_g8 += __shfl_xor_sync(0xffffffffu, l_g8, off);
+    }
+    const int dcol = warp * DW + 2 * c * NTW;  // C columns 2c / 2c+1 -> dims dcol + e / + NTW + e
+    const int flag_idx = head * 16 + qt;
+    if (active == 1) {
+        const float ig = 1.0f / l_g, ig8 = 1.0f / l_g8;
+        const size_t og = static_cast<size_t>(qt * 16 + g) * qd + head * HD;
+        const size_t og8 = og + static_cast<size_t>(8) * qd;
+#pragma unroll
+        for (int e = 0; e < NTW; ++e) {
+            if (v_g) {
+                P.o[og + dcol + e] = __float2bfloat16_rn(acc[e][0] * ig);
+                P.o[og + dcol + NTW + e] = __float2bfloat16_rn(acc[e][1] * ig);
+            }
+            if (v_g8) {
+                P.o[og8 + dcol + e] = __float2bfloat16_rn(acc[e][2] * ig8);
+                P.o[og8 + dcol + NTW + e] = __float2bfloat16_rn(acc[e][3] * ig8);
+            }
+        }
+        epi_bar();  // every thread's o stores happen-before thread 0's release
+        if (tid == 0) st_release_flag(P.flags, ph.out_flag, flag_idx, epoch);
+        return;
+    }
+    // partials: [head][qt][grp] x (16 rows x (HD + 2)), unnormalised O, m, l
+    constexpr int RS = HD + 2;
+    float* part = P.attn_part + ((static_cast<size_t>(head) * 16 + qt) * kAttnGroups) * 16 * RS;
+    float* mine = part + static_cast<size_t>(grp) * 16 * RS;
+#pragma unroll
+    for (int e = 0; e < NTW; ++e) {
+        mine[g * RS + dcol + e] = acc[e][0];
+        mine[g * RS + dcol + NTW + e] = acc[e][1];
+        mine[(g + 8) * RS + dcol + e] = acc[e][2];
+        mine[(g + 8) * RS + dcol + NTW + e] = acc[e][3];
+    }
+    if (warp == 0 && c == 0) {
+        mine[g * RS + HD] = m_g;
+        mine[g * RS + HD + 1] = l_g;
+        mine[(g + 8) * RS + HD] = m_g8;
+        mine[(g + 8) * RS + HD + 1] = l_g8;
+    }
+    epi_bar();
+    int* cnt = P.attn_cnt + head * 16 + qt;
+    // release this group's partials, acquire the other groups'
+    if (tid == 0) *s_bcast = atom_add_acq_rel(cnt, 1) == active - 1;
+    epi_bar();
+    if (!*s_bcast) return;
+    // last group: combine the active groups in group order; thread = one dim of
+    // 16 / (128 / HD) rows
+    constexpr int kRows = 16 * HD / 128;
+    const int d = tid % HD, r0 = tid / HD, rstep = 128 / HD;
+    float M[kRows], L[kRows], O[kRows];
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) {
+        M[i] = -INFINITY;
+        L[i] = 0.f;
+        O[i] = 0.f;
+    }
+    for (int j = 0; j < active; ++j)
+#pragma unroll
+        for (int i = 0; i < kRows; ++i)
+            M[i] = fmaxf(M[i], __ldcg(part + (static_cast<size_t>(j) * 16 + r0 + i * rstep) * RS + HD));
+    for (int j = 0; j < active; ++j) {
+        float mj[kRows], lj[kRows], oj[kRows];
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const float* row = part + (static_cast<size_t>(j) * 16 + r0 + i * rstep) * RS;
+            mj[i] = __ldcg(row + HD);
+            lj[i] = __ldcg(row + HD + 1);
+            oj[i] = __ldcg(row + d);
+        }
+#pragma unroll
+        for (int i = 0; i < kRows; ++i) {
+            const float f = mj[i] == -INFINITY ? 0.f : fast_exp2(mj[i] - M[i]);
+            L[i] += lj[i] * f;
+            O[i] += oj[i] * f;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kRows; ++i) {
+        const int t = qt * 16 + r0 + i * rstep;
+        if (t < W) P.o[static_cast<size_t>(t) * qd + head * HD + d] = __float2bfloat16_rn(O[i] / L[i]);
+    }
+    epi_bar();
+    if (tid == 0) {
+        *cnt = 0;
+        st_release_flag(P.flags, ph.out_flag, flag_idx, epoch);
+    }
+}
+
+// Embedding of column tile `tile` (128 columns) for every token: x = E[tok],
+// h = bf16(x * g), ss[t][tile] = sum of squares (warp tree, then warps 0..3 in
+// the order ((0+1)+(2+3)) - the residual epilogue's formulation).
+__device__ void embed_tile(const PassParams& P, int tile, int W, float* part /* [4][32] */, int tid) {
+    const int d = P.m.d, tiles = d / 128;
+    const int col = tile * 128 + tid;
+    const int warp = tid >> 5;
+    const float gcol = P.gain[col];
+    for (int t0 = 0; t0 < W; t0 += 32) {
+        const int tn = min(32, W - t0);
+        for (int t = 0; t < tn; ++t) {
+            const int tok = P.ps->tokens[t0 + t];
+            const float v = __bfloat162float(P.emb[static_cast<size_t>(tok) * d + col]);
+            P.x[static_cast<size_t>(t0 + t) * d + col] = v;
+            P.h[static_cast<size_t>(t0 + t) * d + col] = __float2bfloat16_rn(__fmul_rn(v, gcol));
+            float sq = __fmul_rn(v, v);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+            if ((tid & 31) == 0) part[warp * 32 + t] = sq;
+        }
+        epi_bar();
+        if (tid < tn)
+            P.ss[static_cast<size_t>(t0 + tid) * tiles + tile] =
+                __fadd_rn(__fadd_rn(part[tid], part[32 + tid]), __fadd_rn(part[64 + tid], part[96 + tid]));
+        epi_bar();
+    }
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Wait until every producer flag feeding this CTA's k-blocks of a GEMM phase
+// is published.  Run by the whole activation-producer warp: the distinct
+// producer keys of the range form one contiguous (wrapping) run, each lane
+// spins on its own subset of flags (weak L2 loads), then acq_rel fences and a
+// warp sync order every TMA read that follows (plus the generic -> async proxy
+// fence for the TMA engine).
+__device__ void wait_phase_inputs(const PassParams& P, int x_src, int x_flag, int nkb, int g0, int g1,
+                                  int epoch, int qtiles, int lane) {
+    const int hd_shift = P.m.head_dim == 128 ? 7 : 6;
+    auto key_of = [&](int kb) {
+        return x_src == kXNormed ? kb >> 1 : x_src == kXSwiglu ? kb : (kb * 64) >> hd_shift;
+    };
+    const int n_keys = x_src == kXNormed ? nkb >> 1 : x_src == kXSwiglu ? nkb : (nkb * 64) >> hd_shift;
+    const int n = min(g1 - g0, nkb);
+    const int kb0 = g0 % nkb;
+    int k_lo, count;
+    if (n == nkb) {
+        k_lo = 0;
+        count = n_keys;
+    } else {
+        k_lo = key_of(kb0);
+        const int k_hi = key_of((kb0 + n - 1) % nkb);
+        count = (k_hi - k_lo + n_keys) % n_keys + 1;
+    }
+    const int per_key = x_src == kXAttn ? qtiles : 1;
+    for (int i = lane; i < count * per_key; i += 32) {
+        const int key = (k_lo + i / per_key) % n_keys;
+        const int idx = x_src == kXAttn ? key * 16 + i % per_key : key;
+        const int* f = flag_poll(P.flags, x_flag, idx);
+        while (__ldcg(f) - epoch < 0) __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    __syncwarp();
+    fence_proxy_async();  // generic-proxy writes -> the TMA (async proxy) reads that follow
+}
+
+// ---------------------------------------------------------------- fast epilogue
+// Decode-width (W <= 16) epilogue of one 128-row output tile, one output row
+// per thread (row == epilogue thread id == TMEM lane), from registers:
+// v[t] = D[row][t] (already reduced over stream-K segments).  Store and
+// residual epilogues write straight from registers; SwiGLU and RoPE pair rows
+// that live in different warps, so they stage through `red` once.  Phase-level
+// constants (RMSNorm factors, RoPE cos/sin of the W positions, KV pages) come
+// from shared memory, prefetched at phase start.
+struct FastEpi {
+    float rn[kChunk];          // RMSNorm factor per token (consumers of h)
+    float cs[kChunk][64];      // RoPE cos / sin at positions n_cached + t
+    float sn[kChunk][64];
+    int page[kChunk], slot[kChunk];
+    float part[4][kChunk];     // cross-warp sum-of-squares partials
+};
+
+__device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* part, int tile, float* v,
+                                   const float* xv, float gcol, float* red, int tid) {
+    const GemmEpiParams& e = a.epi;
+    const int W = a.w;
+    const int m0 = tile * kBlockM;
+    if (e.ss_in != nullptr) {
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < W) v[t] = __fmul_rn(v[t], fe.rn[t]);
+    }
+    if (e.kind == kEpiStore) {
+        float* dst = e.out + m0 + tid;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < W) dst[static_cast<size_t>(t) * a.n_out] = v[t];
+    } else if (e.kind == kEpiResidual) {
+        float* dst = e.out + m0 + tid;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t) v[t] = t < W ? __fadd_rn(xv[t], v[t]) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < W) dst[static_cast<size_t>(t) * a.n_out] = v[t];
+        if (e.u_out != nullptr) {
+            __nv_bfloat16* u = e.u_out + m0 + tid;
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                if (t < W) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(v[t], gcol));
+                float sq = __fmul_rn(v[t], v[t]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+                if ((tid & 31) == 0) part[(tid >> 5) * kChunk + t] = sq;
+            }
+            epi_bar();
+            if (tid < W) {
+                const float tot = __fadd_rn(__fadd_rn(part[tid], part[kChunk + tid]),
+                                            __fadd_rn(part[2 * kChunk + tid], part[3 * kChunk + tid]));
+                e.ss_out[static_cast<size_t>(tid) * a.tiles + tile] = tot;
+            }
+        }
+    } else {
+        // SwiGLU / RoPE pair rows of different warps: stage once
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < W) red[t * 128 + tid] = v[t];
+        epi_bar();
+        if (e.kind == kEpiSwiGLU) {
+            const int ffn = a.n_out / 2;
+            for (int idx = tid; idx < W * 64; idx += kEpiThreads) {
+                const int t = idx >> 6, f = idx & 63;
+                const float g = red[t * 128 + f], u = red[t * 128 + 64 + f];
+                const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+                e.out_bf[static_cast<size_t>(t) * ffn + tile * 64 + f] = __float2bfloat16_rn(__fmul_rn(silu, u));
+            }
+        } else {  // kEpiQkvRope
+            const ModelDims& md = e.m;
+            const int hd = md.head_dim, half = hd / 2;
+            const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+            if (m0 < q_dim + kv_dim) {
+                for (int idx = tid; idx < W * 64; idx += kEpiThreads) {
+                    const int t = idx >> 6, pr = idx & 63;
+                    const int hl = pr / half, i = pr % half;
+                    const int r0 = hl * hd + i;
+                    const float av = red[t * 128 + r0], bv = red[t * 128 + r0 + half];
+                    const float c = fe.cs[t][i], sn = fe.sn[t][i];
+                    const float lo = __fmaf_rn(av, c, -__fmul_rn(bv, sn));
+                    const float hi = __fmaf_rn(bv, c, __fmul_rn(av, sn));
+                    const int grow = m0 + r0;
+                    if (grow < q_dim) {
+                        float* qd = e.q_out + static_cast<size_t>(t) * q_dim + grow;
+                        qd[0] = lo;
+                        qd[half] = hi;
+                    } else {
+                        const int kh = (grow - q_dim) / hd;
+                        __nv_bfloat16* kd =
+                            e.kv_pool + kv_offset(md, e.page_size, fe.page[t], e.layer, 0, kh, fe.slot[t]) + i;
+                        kd[0] = __float2bfloat16_rn(lo);
+                        kd[half] = __float2bfloat16_rn(hi);
+                    }
+                }
+            } else {
+                for (int idx = tid; idx < W * 128; idx += kEpiThreads) {
+                    const int t = idx >> 7, r = idx & 127;
+                    const int ve = m0 + r - q_dim - kv_dim;
+                    e.kv_pool[kv_offset(md, e.page_size, fe.page[t], e.layer, 1, ve / hd, fe.slot[t]) + ve % hd] =
+                        __float2bfloat16_rn(red[t * 128 + r]);
+                }
+            }
+        }
+    }
+}
+
+// Shared-memory ring position without divisions (the single-thread producer
+// and MMA loops are issue-bound: every instruction per stage counts).
+struct RingPos {
+    int s = 0;         // stage
+    uint32_t ph = 0;   // parity of the current use of stage s
+    uint32_t n = 0;    // stages consumed so far
+    __device__ __forceinline__ void next(int S) {
+        if (++s == S) {
+            s = 0;
+            ph ^= 1u;
+        }
+        ++n;
+    }
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(kPassThreads, 1)
+    pass_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_o,
+                const __grid_constant__ CUtensorMap map_a, const __grid_constant__ PassParams P) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nctas = gridDim.x, c = blockIdx.x;
+    const int S = P.stages, nt = P.nt;
+    const uint32_t b_bytes = static_cast<uint32_t>(nt) * 128u;
+    const uint32_t stage_bytes = kABytes + b_bytes;
+    const int hd = P.m.head_dim;
+    uint8_t* kv_smem = smem + S * stage_bytes;                          // attention K/V chunk
+    float* red = reinterpret_cast<float*>(kv_smem + 2 * kAttnChunk * hd * 2);  // [kChunk][128]
+    uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ int s_last;
+    __shared__ float s_r[kChunk];
+    __shared__ float s_part[4 * 32];
+    __shared__ GemmArgs s_args;
+    __shared__ FastEpi s_fe;
+    __shared__ unsigned long long s_issue[16];  // debug: weight-load issue time per stage
+    __shared__ volatile int s_xready;           // last phase whose activations are ready
+
+    if (threadIdx.x == 0) {
+        s_xready = -1;
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 2);  // weight producer + activation producer
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], kEpiThreads);
+        }
+        fence_barrier_init();
+        tma_prefetch_desc(&map_h);
+        tma_prefetch_desc(&map_o);
+        tma_prefetch_desc(&map_a);
+    }
+    if (warp == 1) {
+        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * 2);
+        if (cols <= 64) tmem_alloc<64>(tmem_slot);
+        else if (cols <= 128) tmem_alloc<128>(tmem_slot);
+        else if (cols <= 256) tmem_alloc<256>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int epoch = P.ps->epoch;
+    const int W = P.ps->w;
+    const int qtiles = (W + 15) / 16;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- weight producer ----------------
+            const uint64_t pol_w = policy_evict_first();
+            // L2 prefetch cursor runs P.prefetch blocks ahead of the ring loads,
+            // across phase boundaries, so HBM keeps streaming while a phase
+            // waits for its activations
+            int pf_p = 0;
+            long pf_g = -1, pf_g1 = -1;
+            const __nv_bfloat16* pf_w = nullptr;
+            uint32_t pf_it = 0;
+            auto pf_advance = [&](uint32_t target) {
+                while (pf_it < target) {
+                    if (pf_g >= pf_g1) {  // next GEMM phase with work
+                        for (; pf_p < P.n_phases; ++pf_p) {
+                            const PassPhase& q = P.phases[pf_p];
+                            if (q.type != kPhGemm) continue;
+                            const long T = static_cast<long>(q.a.tiles) * q.a.nkb;
+                            pf_g = sk_begin(c, T, nctas);
+                            pf_g1 = sk_begin(c + 1, T, nctas);
+                            pf_w = q.w;
+                            if (pf_g < pf_g1) break;
+                        }
+                        if (pf_p >= P.n_phases) return;
+                        ++pf_p;
+                    }
+                    prefetch_l2(pf_w + pf_g * 8192, kABytes);
+                    ++pf_g;
+                    ++pf_it;
+                }
+            };
+            RingPos rp;
+            for (int p = 0; p < P.n_phases; ++p) {
+                const PassPhase& ph = P.phases[p];
+                if (ph.type != kPhGemm) continue;
+                const long T = static_cast<long>(ph.a.tiles) * ph.a.nkb;
+                const int g0 = static_cast<int>(sk_begin(c, T, nctas));
+                const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+                const __nv_bfloat16* src = ph.w + static_cast<size_t>(g0) * 8192;
+                pass_stamp(P, p, 0);
+                for (int g = g0; g < g1; ++g, src += 8192) {
+                    // boundary throttle (experiment): only P.early stages of a phase
+                    // are fetched before its activations are ready
+                    if (P.early >= 0 && g - g0 >= P.early)
+                        while (s_xready < p) __nanosleep(64);
+                    if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
+                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                    mbar_arrive_expect_tx(&full[rp.s], kABytes);
+                    bulk_load(smem + rp.s * stage_bytes, src, kABytes, &full[rp.s], pol_w);
+                    rp.next(S);
+                }
+                pass_stamp(P, p, 11);
+            }
+        }
+    } else if (warp == 2) {
+        // ---------------- activation producer ----------------
+        // (the whole warp polls the input flags; lane 0 feeds the ring)
+        const uint64_t pol_x = policy_evict_last();
+        RingPos rp;
+        const int nbox = nt >> 4;
+        for (int p = 0; p < P.n_phases; ++p) {
+            const PassPhase& ph = P.phases[p];
+            if (ph.type != kPhGemm) continue;
+            const int nkb = ph.a.nkb;
+            const long T = static_cast<long>(ph.a.tiles) * nkb;
+            const int g0 = static_cast<int>(sk_begin(c, T, nctas));
+            const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+            if (g1 <= g0) continue;
+            if (lane == 0) pass_stamp(P, p, 7);
+            wait_phase_inputs(P, ph.x_src, ph.x_flag, nkb, g0, g1, epoch, qtiles, lane);
+            if (lane == 0) {
+                s_xready = p;
+                pass_stamp(P, p, 1);
+                const CUtensorMap* mx = ph.x_map == 0 ? &map_h : ph.x_map == 1 ? &map_o : &map_a;
+                int kb = g0 % nkb;
+                for (int g = g0; g < g1; ++g) {
+                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                    mbar_arrive_expect_tx(&full[rp.s], b_bytes);
+                    uint8_t* sb = smem + rp.s * stage_bytes + kABytes;
+                    for (int r = 0; r < nbox; ++r)
+                        tma_load_2d(sb + r * 2048, mx, &full[rp.s], kb * kBlockK, r * 16, pol_x);
+                    rp.next(S);
+                    if (++kb == nkb) kb = 0;
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = idesc_bf16_f32(kBlockM, nt);
+            RingPos rp;
+            uint32_t u = 0;
+            for (int p = 0; p < P.n_phases; ++p) {
+                const PassPhase& ph = P.phases[p];
+                if (ph.type != kPhGemm) continue;
+                const int nkb = ph.a.nkb;
+                const long T = static_cast<long>(ph.a.tiles) * nkb;
+                const int g0 = static_cast<int>(sk_begin(c, T, nctas));
+                const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+                if (g1 <= g0) continue;
+                const int tile_lo = g0 / nkb, tile_hi = (g1 - 1) / nkb;
+                for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
+                    const int lo = max(g0, tile * nkb);
+                    const int hi = min(g1, (tile + 1) * nkb);
+                    const int b = u & 1;
+                    if (u >= 2) mbar_wait(&tempty[b], ((u >> 1) - 1) & 1u);
+                    tc_fence_after();
+                    const uint32_t acc = tmem + static_cast<uint32_t>(b * P.tmem_buf);
+                    for (int g = lo; g < hi; ++g) {
+                        mbar_wait(&full[rp.s], rp.ph);
+                        tc_fence_after();
+                        const uint32_t sa = smem_u32(smem + rp.s * stage_bytes);
+                        const uint64_t adesc = sw128_kmajor_desc(sa);
+                        const uint64_t bdesc = sw128_kmajor_desc(sa + kABytes);
+#pragma unroll
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                      (g != lo || k != 0) ? 1u : 0u);
+                        umma_commit(&empty[rp.s]);
+                        rp.next(S);
+                    }
+                    umma_commit(&tfull[b]);
+                }
+                pass_stamp(P, p, 2);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue / embedding / attention ----------------
+        const int tid = threadIdx.x - kEpiBase;  // 0..127
+        const int q = warp & 3;                  // TMEM lane quarter
+        const int row = q * 32 + lane;
+        uint32_t u = 0;
+        for (int p = 0; p < P.n_phases; ++p) {
+            const PassPhase& ph = P.phases[p];
+            if (tid == 0) PASS_DBG(4, p);
+            if (ph.type == kPhEmbed) {
+                const int tiles = P.m.d / 128;
+                for (int tile = c; tile < tiles; tile += nctas) {
+                    embed_tile(P, tile, W, s_part, tid);
+                    epi_bar();
+                    if (tid == 0) st_release_flag(P.flags, ph.out_flag, tile, epoch);
+                }
+                if (tid == 0) pass_stamp(P, p, 3);
+                continue;
+            }
+            if (ph.type == kPhAttn) {
+                const int items = P.m.n_heads * qtiles * kAttnGroups;
+                const int n0 = P.ps->n_cached;
+                for (int item = c; item < items; item += nctas) {
+                    const int grp = item % kAttnGroups;
+                    const int qt = (item / kAttnGroups) % qtiles;
+                    const int head = item / (kAttnGroups * qtiles);
+                    const int kmax = n0 + min(W, (qt + 1) * 16) - 1;
+                    if (grp > kmax / kAttnChunk) continue;  // no chunk for this group
+                    if (tid == 0) PASS_DBG(6, p * 100000 + item);
+                    if (hd == 128)
+                        attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);
+                    else
+                        attn_item<64>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);
+                }
+                if (tid == 0) pass_stamp(P, p, 3);
+                continue;
+            }
+            // GEMM epilogue
+            const int nkb = ph.a.nkb;
+            const long T = static_cast<long>(ph.a.tiles) * nkb;
+            const long g0 = sk_begin(c, T, nctas), g1 = sk_begin(c + 1, T, nctas);
+            if (g1 <= g0) continue;
+            if (tid == 0) s_args = ph.a;
+            const bool fast = W <= kChunk;
+            if (fast) {
+                // every producer tile of this phase's input is complete before
+                // the phase-level constants are read (lanes poll in parallel)
+                const int hd_shift = P.m.head_dim == 128 ? 7 : 6;
+                const int n_keys = ph.x_src == kXNormed ? nkb >> 1 : ph.x_src == kXSwiglu ? nkb
+                                                                     : (nkb * 64) >> hd_shift;
+                const int per_key = ph.x_src == kXAttn ? qtiles : 1;
+                for (int i = tid; i < n_keys * per_key; i += kEpiThreads) {
+                    const int key = i / per_key;
+                    const int idx = ph.x_src == kXAttn ? key * 16 + i % per_key : key;
+                    wait_flag(flag_poll(P.flags, ph.x_flag, idx), epoch);
+                }
+                epi_bar();
+                const GemmEpiParams& ep = ph.a.epi;
+                if (ep.ss_in != nullptr && tid < W) {
+                    const float* ssr = ep.ss_in + static_cast<size_t>(tid) * ep.ss_tiles;
+                    float acc = 0.0f;
+                    for (int i0 = 0; i0 < ep.ss_tiles; i0 += 16) {
+                        float v16[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v16[j] = i0 + j < ep.ss_tiles ? __ldcg(ssr + i0 + j) : 0.0f;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (i0 + j < ep.ss_tiles) acc = __fadd_rn(acc, v16[j]);
+                    }
+                    s_fe.rn[tid] = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(ep.norm_d)), ep.eps));
+                }
+                if (ep.kind == kEpiQkvRope) {
+                    const int half = P.m.head_dim / 2;
+                    const int n0 = P.ps->n_cached;
+                    for (int idx = tid; idx < W * half; idx += kEpiThreads) {
+                        const int t = idx / half, i = idx % half;
+                        s_fe.cs[t][i] = ep.rope_cos[static_cast<size_t>(n0 + t) * half + i];
+                        s_fe.sn[t][i] = ep.rope_sin[static_cast<size_t>(n0 + t) * half + i];
+                    }
+                    if (tid < W) {
+                        const int pos = n0 + tid;
+                        s_fe.page[tid] = ep.page_table[pos / ep.page_size];
+                        s_fe.slot[tid] = pos % ep.page_size;
+                    }
+                }
+            }
+            epi_bar();
+            const GemmArgs& a = s_args;
+            const bool resid = a.epi.kind == kEpiResidual;
+            const int tile_lo = static_cast<int>(g0 / nkb), tile_hi = static_cast<int>((g1 - 1) / nkb);
+            for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
+                int nseg, seg;
+                sk_segments(tile, nkb, T, nctas, c, &nseg, &seg);
+                const int b = u & 1;
+                float xv[kChunk];
+                float gcol = 1.0f;
+                if (fast && resid) {  // residual rows of this tile, before the accumulator lands
+#pragma unroll
+                    for (int t = 0; t < kChunk; ++t)
+                        xv[t] = t < W ? __ldcg(a.epi.out + static_cast<size_t>(t) * a.n_out + tile * kBlockM + tid) : 0.0f;
+                    if (a.epi.u_out != nullptr) gcol = a.epi.gain[tile * kBlockM + tid];
+                }
+                mbar_wait(&tfull[b], (u >> 1) & 1u);
+                __syncwarp();
+                tc_fence_after();
+                const uint32_t t_lane =
+                    tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * P.tmem_buf);
+                bool publish = false;
+                if (fast) {
+                    float v[16];
+                    tmem_ld16(t_lane, v);
+                    tc_fence_before();
+                    mbar_arrive(&tempty[b]);
+                    if (nseg == 1) {
+                        fast_tile_epilogue(a, s_fe, s_part, tile, v, xv, gcol, red, tid);
+                        publish = true;
+                    } else {
+                        float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * W * 128;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < W) part[static_cast<size_t>(j) * 128 + row] = v[j];
+                        epi_bar();
+                        if (tid == 0) {  // release this segment's partial, acquire the others'
+                            const int prev = atom_add_acq_rel(&a.epi.counters[tile], 1);
+                            s_last = (prev == nseg - 1);
+                        }
+                        epi_bar();
+                        if (s_last) {
+                            // this thread's row over every segment: all loads in flight, summed
+                            // in segment order
+                            const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * W * 128 + row;
+                            float acc[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
+                            for (int s0 = 0; s0 < nseg; s0 += 4) {
+                                float pv[4][16];
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j)
+                                        pv[k][j] = (s0 + k < nseg && j < W)
+                                                       ? __ldcg(base + (static_cast<size_t>(s0 + k) * W + j) * 128)
+                                                       : 0.0f;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    if (s0 + k < nseg)
+#pragma unroll
+                                        for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], pv[k][j]);
+                            }
+                            fast_tile_epilogue(a, s_fe, s_part, tile, acc, xv, gcol, red, tid);
+                            if (tid == 0) a.epi.counters[tile] = 0;
+                            publish = true;
+                        }
+                    }
+                } else if (nseg == 1) {
+                    for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                        const int tn = min(kChunk, a.w - t0);
+                        float v[16];
+                        tmem_ld16(t_lane + t0, v);
+                        if (t0 + kChunk >= a.w) {
+                            tc_fence_before();
+                            mbar_arrive(&tempty[b]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (j < tn) red[j * 128 + row] = v[j];
+                        epi_bar();
+                        scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                        apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                        epi_bar();
+                    }
+                    publish = true;
+                } else {
+                    float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * a.w * 128;
+                    for (int t0 = 0; t0 < a.w; t0 += 16) {
+                        float v[16];
+                        tmem_ld16(t_lane + t0, v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            if (t0 + j < a.w) part[static_cast<size_t>(t0 + j) * 128 + row] = v[j];
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&tempty[b]);
+                    epi_bar();
+                    if (tid == 0) {  // release this segment's partial, acquire the others'
+                        const int prev = atom_add_acq_rel(&a.epi.counters[tile], 1);
+                        s_last = (prev == nseg - 1);
+                    }
+                    epi_bar();
+                    if (s_last) {
+                        const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * a.w * 128;
+                        const size_t seg_stride = static_cast<size_t>(a.w) * 128;
+                        for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                            const int tn = min(kChunk, a.w - t0);
+                            for (int itm = tid; itm < tn * 32; itm += kEpiThreads) {
+                                const int t = itm >> 5, r4 = (itm & 31) * 4;
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    base + static_cast<size_t>(t0 + t) * 128 + r4);
+                                float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                                for (int s0 = 0; s0 < nseg; s0 += 8) {
+                                    float4 vv[8];
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j)
+                                        if (s0 + j < nseg) vv[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j)
+                                        if (s0 + j < nseg) {
+                                            acc4.x = __fadd_rn(acc4.x, vv[j].x);
+                                            acc4.y = __fadd_rn(acc4.y, vv[j].y);
+                                            acc4.z = __fadd_rn(acc4.z, vv[j].z);
+                                            acc4.w = __fadd_rn(acc4.w, vv[j].w);
+                                        }
+                                }
+                                *reinterpret_cast<float4*>(red + t * 128 + r4) = acc4;
+                            }
+                            epi_bar();
+                            scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                            apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                            epi_bar();
+                        }
+                        if (tid == 0) a.epi.counters[tile] = 0;
+                        publish = true;
+                    }
+                }
+                if (publish) {
+                    epi_bar();  // every epilogue store happens-before the release
+                    if (tid == 0) {
+                        st_release_flag(P.flags, ph.out_flag, tile, epoch);
+                        pass_stamp(P, p, 6);
+                        if (P.trace2) P.trace2[p * 512 + tile] = gtimer();
+                        if (P.poll_mode == 6) {  // debug: when does the store reach L2?
+                            while (ld_relaxed(flag_at(P.flags, ph.out_flag, tile, 0)) != epoch) {}
+                            pass_stamp(P, p, 8);
+                        }
+                    }
+                }
+            }
+            epi_bar();  // s_args reuse by the next phase
+            if (tid == 0) pass_stamp(P, p, 3);
+        }
+    }
+    if (threadIdx.x == 0) PASS_DBG(7, -1);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * 2);
+        if (cols <= 64) tmem_dealloc<64>(tmem);
+        else if (cols <= 128) tmem_dealloc<128>(tmem);
+        else if (cols <= 256) tmem_dealloc<256>(tmem);
+        else tmem_dealloc<512>(tmem);
+    }
+#endif
+}
+
+void* pass_debug_enable(int on) {
+    static int* host = nullptr;
+    if (on && !host) {
+        cudaHostAlloc(&host, sizeof(int) * kNumSMs * 8, cudaHostAllocMapped);
+        memset(host, 0, sizeof(int) * kNumSMs * 8);
+        int* dev = nullptr;
+        cudaHostGetDevicePointer(&dev, host, 0);
+        cudaMemcpyToSymbol(g_pass_dbg, &dev, sizeof(dev));
+    }
+    return host;
+}
+
+size_t pass_attn_part_floats(const ModelDims& m) {
+    return static_cast<size_t>(m.n_heads) * 16 * kAttnGroups * 16 * (m.head_dim + 2);
+}
+size_t pass_attn_cnt_ints(const ModelDims& m) { return static_cast<size_t>(m.n_heads) * 16; }
+
+int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
+    const int stage_bytes = static_cast<int>(kABytes) + nt * 128;
+    const int fixed = 1024 /* align */ + 2 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
+    const int budget = 225 * 1024 - 2048 /* static shared */;
+    static const int cap = getenv("DD_PASS_STAGES") ? atoi(getenv("DD_PASS_STAGES")) : 8;
+    int s = (budget - fixed) / stage_bytes;
+    s = s > cap ? cap : s;
+    if (s < 2) return -1;
+    *stages = s;
+    return fixed + s * stage_bytes;
+}
+
+cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
+                               const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
+                               cudaStream_t s) {
+    static int attr_set = 0;
+    if (attr_set < smem_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes);
+        if (e != cudaSuccess) return e;
+        attr_set = smem_bytes;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kNumSMs, 1, 1);
+    cfg.blockDim = dim3(kPassThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, pass_kernel, map_h, map_o, map_a, p);
+}
+
+}  // namespace dd

@@ -1,0 +1,82 @@
+// Persistent whole-pass kernel (pass.cu): one launch runs the embedding, every
+// layer's QKV / attention / O / gate-up / down and the LM head of a scored
+// pass, with tile-level dataflow flags instead of kernel boundaries.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "gemm.h"
+#include "model.h"
+
+namespace dd {
+
+enum PassPhaseType { kPhEmbed = 0, kPhGemm = 1, kPhAttn = 2 };
+// where a GEMM phase's activation k-block comes from
+enum PassXSrc {
+    kXNormed = 0,  // h (embedding / residual producer): flag of tile kb / 2
+    kXAttn = 1,    // o (attention): flags of head kb * 64 / head_dim, every query tile
+    kXSwiglu = 2,  // a (SwiGLU): flag of gate/up tile kb
+};
+
+struct PassPhase {
+    int type;
+    int x_map;     // 0 = h, 1 = o, 2 = a
+    int x_src;
+    int x_flag;    // flag base of the producing phase
+    int out_flag;  // flag base of this phase's outputs
+    int layer;
+    int qkv_flag;  // attention: flag base of the layer's QKV tiles
+    int pad_;
+    const __nv_bfloat16* w;  // pre-tiled weights (GEMM)
+    GemmArgs a;              // GEMM shape + fused epilogue
+};
+
+struct PassParams {
+    const PassPhase* phases;
+    int n_phases;
+    int stages;
+    int nt;
+    int tmem_buf;
+    int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
+    int poll_mode;  // debug: flag polling variant
+    int early;      // stages a phase may fetch before its activations are ready (-1: no limit)
+    unsigned long long* trace;
+    unsigned long long* trace2;  // debug: per-tile publish times / poll batch times  // debug: [CTA][phase][4] globaltimer stamps, or nullptr
+    const PassState* ps;
+    int* flags;
+    // embedding
+    const __nv_bfloat16* emb;
+    const float* gain;
+    float* x;
+    __nv_bfloat16* h;
+    float* ss;
+    // attention
+    ModelDims m;
+    const float* q;
+    const __nv_bfloat16* kv_pool;
+    const int32_t* page_table;
+    int page_size;
+    float scale_log2;
+    __nv_bfloat16* o;
+    float* attn_part;
+    int* attn_cnt;
+};
+
+constexpr int kPassThreads = 256;
+constexpr int kAttnChunk = 64;    // keys staged per attention step
+constexpr int kAttnGroups = 8;    // chunk groups per (head, query tile)
+constexpr int kFlagStride = 32;   // ints: one 128-byte line per flag replica
+constexpr int kFlagReplicas = 8;  // every flag is published to 8 lines; CTA c polls replica c % 8
+                                  // (148 pollers on one line serialise in its L2 slice)
+
+void* pass_debug_enable(int on);  // mapped host int[148][8] progress words
+size_t pass_attn_part_floats(const ModelDims& m);
+size_t pass_attn_cnt_ints(const ModelDims& m);
+int pass_smem_bytes(const ModelDims& m, int nt, int* stages);
+
+cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
+                               const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
+                               cudaStream_t s);
+
+}  // namespace dd

@@ -18,7 +18,9 @@
 #include "common.cuh"
 #include "ctx.h"
 #include "gemm.h"
+#include "gemm_epi.cuh"
 #include "model.h"
+#include "pass.h"
 
 using namespace dd;
 
@@ -137,7 +139,188 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     return DD_OK;
 }
 
+
+// ------------------------------------------------------------ persistent pass
+namespace {
+
+// max stream-K segments of one tile when T blocks are cut over kNumSMs CTAs
+int pass_max_seg(int tiles, int nkb) {
+    const long T = static_cast<long>(tiles) * nkb;
+    int ms = 1;
+    for (int t = 0; t < tiles; ++t) {
+        const int f = gemm_dev::sk_owner(static_cast<long>(t) * nkb, T, kNumSMs);
+        int nseg, seg;
+        gemm_dev::sk_segments(t, nkb, T, kNumSMs, f, &nseg, &seg);
+        ms = std::max(ms, nseg);
+    }
+    return ms;
+}
+
+int tmem_buf_for(int nt) {
+    int buf = 32;
+    while (buf < nt) buf <<= 1;
+    return buf;
+}
+
+// Phase table of a pass of width w: embed, per layer QKV / attention / O /
+// gate-up / down, then the LM head (when logits are wanted).
+int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** out, int* n_out) {
+    const int key = w * 2 + (want_logits ? 1 : 0);
+    auto it = ctx->pass_phases.find(key);
+    if (it != ctx->pass_phases.end()) {
+        *out = it->second;
+        *n_out = ctx->pass_nphases[key];
+        return DD_OK;
+    }
+    const ModelDims& m = ctx->m;
+    const int nt = round_nt(w);
+    std::vector<PassPhase> ph;
+    GemmEpiParams e{};
+    e.ps = ctx->d_ps;
+    e.rope_cos = ctx->rope_cos;
+    e.rope_sin = ctx->rope_sin;
+    e.q_out = ctx->q;
+    e.kv_pool = ctx->kv_pool;
+    e.page_table = ctx->page_table;
+    e.page_size = ctx->page_size;
+    e.m = m;
+    e.ss_in = ctx->ss;
+    e.ss_tiles = m.d / 128;
+    e.eps = m.eps;
+    e.norm_d = m.d;
+    int gidx = 0;
+    int next_flag = 0;  // flags are packed: each phase reserves exactly its count
+    auto reserve = [&](int n) {
+        const int b = next_flag;
+        next_flag += n;
+        return b;
+    };
+    auto gemm = [&](int id, const __nv_bfloat16* W, int x_map, int x_src, int x_flag,
+                    GemmEpiParams ep, int layer) {
+        PassPhase p{};
+        p.type = kPhGemm;
+        p.x_map = x_map;
+        p.x_src = x_src;
+        p.x_flag = x_flag;
+        p.layer = layer;
+        p.w = W;
+        int n_outr, k;
+        gemm_shape(ctx, id, &n_outr, &k);
+        GemmArgs& a = p.a;
+        a.n_out = n_outr;
+        a.k = k;
+        a.w = w;
+        a.nt = nt;
+        a.tiles = n_outr / 128;
+        a.nkb = k / 64;
+        a.max_seg = pass_max_seg(a.tiles, a.nkb);
+        a.tmem_buf = tmem_buf_for(nt);
+        a.ws = ctx->pass_ws + (gidx & 1) * ctx->pass_ws_half;
+        ep.counters = ctx->pass_counters + (gidx & 1) * 512;
+        a.epi = ep;
+        p.out_flag = reserve(a.tiles);
+        ++gidx;
+        ph.push_back(p);
+        return p.out_flag;
+    };
+    PassPhase pe{};
+    pe.type = kPhEmbed;
+    pe.out_flag = reserve(m.d / 128);
+    ph.push_back(pe);
+    int h_flag = pe.out_flag;  // producer of h (tile = 128 columns)
+    for (int l = 0; l < m.n_layers; ++l) {
+        const LayerW& L = ctx->layers[l];
+        GemmEpiParams eq = e;
+        eq.kind = kEpiQkvRope;
+        eq.layer = l;
+        const int qkv_flag = gemm(kGQkv, L.qkv, 0, kXNormed, h_flag, eq, l);
+        PassPhase pa{};
+        pa.type = kPhAttn;
+        pa.layer = l;
+        pa.qkv_flag = qkv_flag;
+        pa.out_flag = reserve(m.n_heads * 16);
+        ph.push_back(pa);
+        GemmEpiParams er = e;
+        er.kind = kEpiResidual;
+        er.out = ctx->x;
+        er.ss_in = nullptr;
+        er.u_out = ctx->h;
+        er.gain = ctx->gain_ones;
+        er.ss_out = ctx->ss;
+        h_flag = gemm(kGO, L.o, 1, kXAttn, pa.out_flag, er, l);
+        GemmEpiParams eg = e;
+        eg.kind = kEpiSwiGLU;
+        eg.out_bf = ctx->a;
+        const int gu_flag = gemm(kGGu, L.gu, 0, kXNormed, h_flag, eg, l);
+        h_flag = gemm(kGDown, L.dn, 2, kXSwiglu, gu_flag, er, l);
+    }
+    if (want_logits) {
+        GemmEpiParams el = e;
+        el.kind = kEpiStore;
+        el.out = ctx->logits;
+        gemm(kGHead, ctx->head, 0, kXNormed, h_flag, el, m.n_layers);
+    }
+    if (static_cast<size_t>(next_flag) > ctx->pass_flag_count)
+        return ctx_fail(ctx, DD_E_CAPACITY, "pass flag table too small");
+    PassPhase* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(PassPhase) * ph.size()));
+    CK(cudaMemcpy(d, ph.data(), sizeof(PassPhase) * ph.size(), cudaMemcpyHostToDevice));
+    ctx->pass_phases[key] = d;
+    ctx->pass_nphases[key] = static_cast<int>(ph.size());
+    *out = d;
+    *n_out = static_cast<int>(ph.size());
+    return DD_OK;
+}
+
+int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long* trace = nullptr,
+                        unsigned long long* trace2 = nullptr) {
+    const PassPhase* phases = nullptr;
+    int n = 0;
+    int rc = build_pass_phases(ctx, w, want_logits, &phases, &n);
+    if (rc) return rc;
+    const ModelDims& m = ctx->m;
+    PassParams p{};
+    p.phases = phases;
+    p.n_phases = n;
+    p.nt = round_nt(w);
+    p.tmem_buf = tmem_buf_for(p.nt);
+    static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 16;
+    p.prefetch = env_pf;
+    static const int env_pm = getenv("DD_PASS_POLL") ? atoi(getenv("DD_PASS_POLL")) : 0;
+    p.poll_mode = env_pm;
+    static const int env_early = getenv("DD_PASS_EARLY") ? atoi(getenv("DD_PASS_EARLY")) : -1;
+    p.early = env_early;
+    const int smem = pass_smem_bytes(m, p.nt, &p.stages);
+    if (smem < 0) return ctx_fail(ctx, DD_E_ARG, "pass kernel shared memory plan failed");
+    p.ps = ctx->d_ps;
+    p.flags = ctx->pass_flags;
+    p.emb = ctx->emb;
+    p.gain = ctx->gain_ones;
+    p.x = ctx->x;
+    p.h = ctx->h;
+    p.ss = ctx->ss;
+    p.m = m;
+    p.q = ctx->q;
+    p.kv_pool = ctx->kv_pool;
+    p.page_table = ctx->page_table;
+    p.page_size = ctx->page_size;
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.head_dim)));
+    p.o = ctx->o;
+    p.attn_part = ctx->attn_part;
+    p.attn_cnt = ctx->attn_cnt;
+    p.trace = trace;
+    p.trace2 = trace2;
+    CK(launch_pass_kernel(ctx->map_h, ctx->map_o, ctx->map_a, p, smem, ctx->stream));
+    return DD_OK;
+}
+
+}  // namespace
+
 int enqueue_pass(dd_ctx* ctx, int w, bool want_logits, int* kernels) {
+    if (ctx->use_pass_kernel) {
+        if (kernels) *kernels = 1;
+        return enqueue_pass_kernel(ctx, w, want_logits);
+    }
     int n = 0;
     int rc = enqueue_pass_impl(ctx, w, want_logits, [&n](int) { ++n; });
     if (kernels) *kernels = n;
@@ -174,6 +357,7 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
     PassState* hp = ctx->h_ps + slot;
     hp->n_cached = ctx->n_cached;
     hp->w = w;
+    hp->epoch = ++ctx->epoch;
     std::memcpy(hp->tokens, tokens, sizeof(int32_t) * w);
     CK(cudaMemcpyAsync(ctx->d_ps, hp, offsetof(PassState, tokens) + sizeof(int32_t) * w,
                        cudaMemcpyHostToDevice, ctx->stream));
@@ -183,6 +367,12 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
         const int key = w * 2 + (want_logits ? 1 : 0);
         auto it = ctx->graphs.find(key);
         if (it == ctx->graphs.end()) {
+            if (ctx->use_pass_kernel) {  // device phase table: allocated outside the capture
+                const PassPhase* ph = nullptr;
+                int n = 0;
+                int rc = build_pass_phases(ctx, w, want_logits, &ph, &n);
+                if (rc != DD_OK) return rc;
+            }
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             int nk = 0;
@@ -309,6 +499,33 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     CK(cudaMemcpy(ctx->page_table, pt.data(), sizeof(int32_t) * ctx->n_pages,
                   cudaMemcpyHostToDevice));
 
+    // persistent pass kernel scratch
+    {
+        const char* env = getenv("DD_PASS_KERNEL");
+        ctx->use_pass_kernel = !(env && env[0] == '0');
+        // embed + per layer (qkv, attention, o, gate/up, down) + head
+        const size_t per_layer = m.qkv_rows() / 128 + m.n_heads * 16 + m.d / 128 + 2 * m.ffn / 128 + m.d / 128;
+        const size_t n_flags = m.d / 128 + per_layer * m.n_layers + m.vocab / 128;
+        ctx->pass_flag_count = n_flags;
+        const size_t bytes = sizeof(int) * n_flags * kFlagReplicas * kFlagStride;
+        CK(cudaMalloc(&ctx->pass_flags, bytes));
+        CK(cudaMemset(ctx->pass_flags, 0, bytes));
+        size_t half = 0;
+        for (int id = 0; id < kNumGemm; ++id) {
+            int n_out, k;
+            gemm_shape(ctx, id, &n_out, &k);
+            half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(n_out / 128, k / 64) *
+                                      kMaxPassTokens * 128);
+        }
+        ctx->pass_ws_half = half;
+        CK(cudaMalloc(&ctx->pass_ws, sizeof(float) * 2 * half));
+        CK(cudaMalloc(&ctx->pass_counters, sizeof(int) * 2 * 512));
+        CK(cudaMemset(ctx->pass_counters, 0, sizeof(int) * 2 * 512));
+        CK(cudaMalloc(&ctx->attn_part, sizeof(float) * pass_attn_part_floats(m)));
+        CK(cudaMalloc(&ctx->attn_cnt, sizeof(int) * pass_attn_cnt_ints(m)));
+        CK(cudaMemset(ctx->attn_cnt, 0, sizeof(int) * pass_attn_cnt_ints(m)));
+    }
+
     // RoPE tables in double precision -> fp32 (shared with the oracle)
     const int half = m.head_dim / 2;
     std::vector<float> cs(static_cast<size_t>(ctx->max_seq) * half), sn(cs.size());
@@ -350,6 +567,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : ctx->pass_phases) cudaFree(kv.second);
     for (auto& L : ctx->layers) {
         cudaFree(L.qkv);
         cudaFree(L.o);
@@ -362,7 +580,8 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
                    ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
-                   ctx->counters, ctx->ss};
+                   ctx->counters, ctx->ss, ctx->pass_flags, ctx->pass_ws, ctx->pass_counters,
+                   ctx->attn_part, ctx->attn_cnt};
     for (void* p : dev)
         if (p) cudaFree(p);
     if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
@@ -627,6 +846,7 @@ int dd_profile_pass(dd_ctx* ctx, int w, float* ms4) {
     PassState* hp = ctx->h_ps + slot;
     hp->n_cached = n0;
     hp->w = w;
+    hp->epoch = ++ctx->epoch;
     for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
     CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
@@ -721,6 +941,7 @@ static int upload_dummy_pass(dd_ctx* ctx, int w) {
     PassState* hp = ctx->h_ps + slot;
     hp->n_cached = ctx->n_cached;
     hp->w = w;
+    hp->epoch = ++ctx->epoch;
     for (int i = 0; i < w; ++i) hp->tokens[i] = 0;
     CK(cudaMemcpyAsync(ctx->d_ps, hp, sizeof(PassState), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
@@ -867,6 +1088,45 @@ int dd_debug_gemm_trace(dd_ctx* ctx, int which, int w, uint64_t* trace, int max_
     CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * 8 * ctas, cudaMemcpyDeviceToHost));
     cudaFree(d);
     *n_ctas = ctas;
+    return DD_OK;
+}
+
+void* dd_debug_pass_progress(void) { return pass_debug_enable(1); }
+
+// one pass of width w (logits on) with per-CTA, per-phase globaltimer stamps:
+// trace[cta][phase][8] = weight producer start, inputs ready, MMA done,
+// epilogue done, flags polled, acquire fence done, last flag published
+// (0 where a role had no work)
+int dd_debug_pass_timeline(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_phases) {
+    if (!ctx || !trace || !n_phases || w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_ARG, "bad args");
+    CK(cudaSetDevice(ctx->device));
+    const PassPhase* ph = nullptr;
+    int n = 0;
+    int rc = build_pass_phases(ctx, w, true, &ph, &n);
+    if (rc) return rc;
+    const size_t need = static_cast<size_t>(kNumSMs) * n * 12;
+    if (need > max_entries) return ctx_fail(ctx, DD_E_CAPACITY, "trace buffer too small");
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long) * need));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long) * need));
+    const size_t need2 = 200 * 512 + static_cast<size_t>(kNumSMs) * 200 * 4;
+    unsigned long long* d2 = nullptr;
+    CK(cudaMalloc(&d2, sizeof(unsigned long long) * need2));
+    CK(cudaMemset(d2, 0, sizeof(unsigned long long) * need2));
+    for (int rep = 0; rep < 2; ++rep) {
+        rc = upload_dummy_pass(ctx, w);
+        if (rc) return rc;
+        rc = enqueue_pass_kernel(ctx, w, true, rep ? d : nullptr, rep ? d2 : nullptr);
+        if (rc) return rc;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * need, cudaMemcpyDeviceToHost));
+    if (need + need2 <= max_entries)
+        CK(cudaMemcpy(trace + need, d2, sizeof(unsigned long long) * need2, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    cudaFree(d2);
+    *n_phases = n;
+    ctx->last_w = 0;
     return DD_OK;
 }
 
