@@ -1,4 +1,5 @@
-timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout -s KILL 120 python scripts/pass_timeline.py 8 128 2>&1 | grep -v cta | tail -12
-timeout -s KILL 120 python scripts/pass_ab.py 1,8,32 128
-DD_PASS_PREFETCH=0 timeout -s KILL 120 python scripts/pass_ab.py 8 128
+mkdir -p gpurun_out
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:pass_kernel --csv --log-file gpurun_out/pass_launches.csv python scripts/one_pass.py 8 128 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:pass_kernel -s 2 -c 1 -o gpurun_out/pass_full python scripts/one_pass.py 8 128 > gpurun_out/pass_full.log 2>&1
+cuobjdump -sass paper_2503_00784_b200/libduodec_b200.so > gpurun_out/all.sass 2>&1
+ls -la gpurun_out

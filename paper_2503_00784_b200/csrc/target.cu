@@ -316,8 +316,13 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
 
 }  // namespace
 
+// The persistent pass kernel serves decode widths; wide (prefill) passes are
+// compute-heavier and run as one launch per GEMM / attention, whose
+// 2-CTA-per-SM GEMM keeps more tiles in flight for the epilogue-heavy wide case.
+bool use_pass_kernel(const dd_ctx* ctx, int w) { return ctx->use_pass_kernel && w <= gemm_dev::kChunk; }
+
 int enqueue_pass(dd_ctx* ctx, int w, bool want_logits, int* kernels) {
-    if (ctx->use_pass_kernel) {
+    if (use_pass_kernel(ctx, w)) {
         if (kernels) *kernels = 1;
         return enqueue_pass_kernel(ctx, w, want_logits);
     }
@@ -367,7 +372,7 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
         const int key = w * 2 + (want_logits ? 1 : 0);
         auto it = ctx->graphs.find(key);
         if (it == ctx->graphs.end()) {
-            if (ctx->use_pass_kernel) {  // device phase table: allocated outside the capture
+            if (use_pass_kernel(ctx, w)) {  // device phase table: allocated outside the capture
                 const PassPhase* ph = nullptr;
                 int n = 0;
                 int rc = build_pass_phases(ctx, w, want_logits, &ph, &n);
