@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:pass_kernel --csv --log-file gpurun_out/pass_launches.csv python scripts/one_pass.py 8 128 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:pass_kernel -s 2 -c 1 -o gpurun_out/pass_full python scripts/one_pass.py 8 128 > gpurun_out/pass_full.log 2>&1
-cuobjdump -sass paper_2503_00784_b200/libduodec_b200.so > gpurun_out/all.sass 2>&1
-ls -la gpurun_out
+# one_pass 127: prefill 128 (1 pass of 128 -> W=128 GEMMs) then 3 W=127 passes; capture the 3rd GEMM (gate/up layer 0) of the 2nd pass
+ncu --set full --clock-control none --import-source on -k regex:gemm_sk -s 131 -c 1 -o gpurun_out/gemm127 python scripts/one_pass.py 127 128 > gpurun_out/gemm127.log 2>&1
+tail -3 gpurun_out/gemm127.log

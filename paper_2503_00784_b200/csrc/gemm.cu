@@ -66,8 +66,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* tempty = tfull + 2;      // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     __shared__ int s_last;
-    __shared__ float s_r[kChunk];
     __shared__ float s_part[4 * kChunk];
+    __shared__ float s_rn[kMaxPassTokens];  // RMSNorm factor per token of the consumed h
+    __shared__ int s_page[kMaxPassTokens], s_slot[kMaxPassTokens];
 
     unsigned long long* tr =
         a.trace ? a.trace + 8 * static_cast<size_t>(blockIdx.x) : nullptr;
@@ -187,15 +188,58 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     } else {
         // ---------------- epilogue warps 2..5 ----------------
+        // One output row per thread (row == tid == TMEM lane).  Per-token pass
+        // constants (RMSNorm factor of the consumed h, KV page / slot) are built
+        // once per launch, after the previous kernel of the pass completed.
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int row = q * 32 + lane;
         const int tid = threadIdx.x - 64;  // 0..127
+        const GemmEpiParams& ep = a.epi;
+        griddep_wait();
+        for (int t = tid; t < a.w; t += kEpiThreads) {
+            if (ep.ss_in != nullptr) {
+                const float* ssr = ep.ss_in + static_cast<size_t>(t) * ep.ss_tiles;
+                float acc = 0.0f;
+                for (int i0 = 0; i0 < ep.ss_tiles; i0 += 16) {
+                    float v16[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v16[j] = i0 + j < ep.ss_tiles ? __ldcg(ssr + i0 + j) : 0.0f;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (i0 + j < ep.ss_tiles) acc = __fadd_rn(acc, v16[j]);
+                }
+                s_rn[t] = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(ep.norm_d)), ep.eps));
+            }
+            if (ep.kind == kEpiQkvRope) {
+                const int pos = ep.ps->n_cached + t;
+                s_page[t] = ep.page_table[pos / ep.page_size];
+                s_slot[t] = pos % ep.page_size;
+            }
+        }
+        epi_bar();
+        const bool resid = ep.kind == kEpiResidual;
         for (int tile = tile_lo, u = 0; tile <= tile_hi; ++tile, ++u) {
             const int first = sk_owner(static_cast<long>(tile) * a.nkb, T, P);
             const int last = sk_owner(static_cast<long>(tile + 1) * a.nkb - 1, T, P);
             const int nseg = last - first + 1, seg = c - first;
             const int b = u & 1;
+            const float gcol = (resid && ep.u_out != nullptr) ? ep.gain[tile * kBlockM + row] : 1.0f;
+            // residual rows of this tile's chunk (issued before the data is needed)
+            auto load_x = [&](int t0, int tn, float* xv) {
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    xv[j] = (resid && j < tn)
+                                ? __ldcg(ep.out + static_cast<size_t>(t0 + j) * a.n_out + tile * kBlockM + row)
+                                : 0.0f;
+            };
+            auto scale = [&](int t0, int tn, float* v) {
+                if (ep.ss_in == nullptr) return;
+#pragma unroll
+                for (int j = 0; j < kChunk; ++j)
+                    if (j < tn) v[j] = __fmul_rn(v[j], s_rn[t0 + j]);
+            };
             mbar_wait(&tfull[b], static_cast<uint32_t>((u >> 1) & 1));
+            if (tid == 0 && tile == tile_hi) stamp(6);  // this CTA's last accumulator landed
             __syncwarp();
             tc_fence_after();
             const uint32_t t_lane =
@@ -203,18 +247,16 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (nseg == 1) {
                 for (int t0 = 0; t0 < a.w; t0 += kChunk) {
                     const int tn = min(kChunk, a.w - t0);
+                    float xv[kChunk];
+                    load_x(t0, tn, xv);
                     float v[16];
                     tmem_ld16(t_lane + t0, v);
                     if (t0 + kChunk >= a.w) {  // accumulator fully read
                         tc_fence_before();
                         mbar_arrive(&tempty[b]);
                     }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < tn) red[j * 128 + row] = v[j];
-                    epi_bar();
-                    scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                    apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                    scale(t0, tn, v);
+                    chunk_epilogue_rows(a, tile, t0, tn, v, xv, gcol, s_page, s_slot, red, s_part, row, tid);
                     epi_bar();
                 }
             } else {
@@ -237,37 +279,34 @@ __global__ void __launch_bounds__(kThreads, 2)
                 epi_bar();
                 if (s_last) {
                     __threadfence();
-                    const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * a.w * 128;
+                    // this thread's row of every segment, all loads of a chunk in flight,
+                    // summed in segment order
+                    const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * a.w * 128 + row;
                     const size_t seg_stride = static_cast<size_t>(a.w) * 128;
                     for (int t0 = 0; t0 < a.w; t0 += kChunk) {
                         const int tn = min(kChunk, a.w - t0);
-                        // items = (token, 4-row group); every segment's float4 of an
-                        // item is requested before any add (latency paid once)
-                        for (int it = tid; it < tn * 32; it += kEpiThreads) {
-                            const int t = it >> 5, r4 = (it & 31) * 4;
-                            const float4* src = reinterpret_cast<const float4*>(
-                                base + static_cast<size_t>(t0 + t) * 128 + r4);
-                            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                            for (int s0 = 0; s0 < nseg; s0 += 8) {  // 8 segments in flight
-                                float4 v[8];
+                        float xv[kChunk];
+                        load_x(t0, tn, xv);
+                        float v[16];
 #pragma unroll
-                                for (int j = 0; j < 8; ++j)
-                                    if (s0 + j < nseg)
-                                        v[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
+                        for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+                        for (int s0 = 0; s0 < nseg; s0 += 4) {
+                            float pv[4][16];
 #pragma unroll
-                                for (int j = 0; j < 8; ++j)
-                                    if (s0 + j < nseg) {
-                                        acc.x = __fadd_rn(acc.x, v[j].x);
-                                        acc.y = __fadd_rn(acc.y, v[j].y);
-                                        acc.z = __fadd_rn(acc.z, v[j].z);
-                                        acc.w = __fadd_rn(acc.w, v[j].w);
-                                    }
-                            }
-                            *reinterpret_cast<float4*>(red + t * 128 + r4) = acc;
+                            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j)
+                                    pv[k][j] = (s0 + k < nseg && j < tn)
+                                                   ? __ldcg(base + (s0 + k) * seg_stride + static_cast<size_t>(t0 + j) * 128)
+                                                   : 0.0f;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (s0 + k < nseg)
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], pv[k][j]);
                         }
-                        epi_bar();
-                        scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                        apply_epilogue(a, tile, t0, tn, red, tid, s_part);
+                        scale(t0, tn, v);
+                        chunk_epilogue_rows(a, tile, t0, tn, v, xv, gcol, s_page, s_slot, red, s_part, row, tid);
                         epi_bar();
                     }
                     if (tid == 0) a.epi.counters[tile] = 0;

@@ -184,5 +184,113 @@ static __device__ void scale_by_rnorm(const GemmArgs& a, int t0, int tn, float* 
 }
 
 
+
+// Wide-pass epilogue of tokens [t0, t0 + tn) of one 128-row tile with one output
+// row per thread (row == epilogue thread id == TMEM lane): v[j] = D[row][t0 + j],
+// already reduced over stream-K segments and scaled by the RMSNorm factor when
+// the GEMM consumes h.  Store / residual write straight from registers; SwiGLU
+// and RoPE pair rows of different warps and stage through `red` once.  Pass-level
+// per-token constants (KV page and slot of position n_cached + t) come from
+// shared memory.  Same arithmetic as apply_epilogue.
+static __device__ void chunk_epilogue_rows(const GemmArgs& a, int tile, int t0, int tn, const float* v,
+                                           const float* xv, float gcol, const int* s_page,
+                                           const int* s_slot, float* red, float* part, int row, int tid) {
+    const GemmEpiParams& e = a.epi;
+    const int m0 = tile * kBlockM;
+    if (e.kind == kEpiStore) {
+        float* dst = e.out + static_cast<size_t>(t0) * a.n_out + m0 + row;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < tn) dst[static_cast<size_t>(t) * a.n_out] = v[t];
+    } else if (e.kind == kEpiResidual) {
+        float y[kChunk];
+        float* dst = e.out + static_cast<size_t>(t0) * a.n_out + m0 + row;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t) y[t] = t < tn ? __fadd_rn(xv[t], v[t]) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < tn) dst[static_cast<size_t>(t) * a.n_out] = y[t];
+        if (e.u_out != nullptr) {
+            __nv_bfloat16* u = e.u_out + static_cast<size_t>(t0) * a.n_out + m0 + row;
+#pragma unroll
+            for (int t = 0; t < kChunk; ++t) {
+                if (t < tn) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(y[t], gcol));
+                float sq = __fmul_rn(y[t], y[t]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+                if ((row & 31) == 0) part[(row >> 5) * kChunk + t] = sq;
+            }
+            epi_bar();
+            if (tid < tn) {
+                const float tot = __fadd_rn(__fadd_rn(part[tid], part[kChunk + tid]),
+                                            __fadd_rn(part[2 * kChunk + tid], part[3 * kChunk + tid]));
+                e.ss_out[static_cast<size_t>(t0 + tid) * a.tiles + tile] = tot;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < kChunk; ++t)
+            if (t < tn) red[t * 128 + row] = v[t];
+        epi_bar();
+        if (e.kind == kEpiSwiGLU) {
+            const int ffn = a.n_out / 2;
+            for (int idx = tid; idx < tn * 64; idx += kEpiThreads) {
+                const int t = idx >> 6, f = idx & 63;
+                const float g = red[t * 128 + f], uu = red[t * 128 + 64 + f];
+                const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+                e.out_bf[static_cast<size_t>(t0 + t) * ffn + tile * 64 + f] =
+                    __float2bfloat16_rn(__fmul_rn(silu, uu));
+            }
+        } else {  // kEpiQkvRope
+            const ModelDims& md = e.m;
+            const int hd = md.head_dim, half = hd / 2;
+            const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+            const int n_cached = e.ps->n_cached;
+            if (m0 < q_dim + kv_dim) {
+                // the thread's (token, pair) items: cos / sin requested before use
+                constexpr int kItems = kChunk * 64 / kEpiThreads;  // 8
+                float cv[kItems], sv[kItems];
+#pragma unroll
+                for (int k = 0; k < kItems; ++k) {
+                    const int idx = tid + k * kEpiThreads;
+                    const int t = idx >> 6, pr = idx & 63, i = pr % half;
+                    const size_t ro = static_cast<size_t>(n_cached + t0 + t) * half + i;
+                    cv[k] = t < tn ? e.rope_cos[ro] : 0.0f;
+                    sv[k] = t < tn ? e.rope_sin[ro] : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < kItems; ++k) {
+                    const int idx = tid + k * kEpiThreads;
+                    const int t = idx >> 6, pr = idx & 63;
+                    if (t >= tn) continue;
+                    const int hl = pr / half, i = pr % half;
+                    const int r0 = hl * hd + i;
+                    const float av = red[t * 128 + r0], bv = red[t * 128 + r0 + half];
+                    const float lo = __fmaf_rn(av, cv[k], -__fmul_rn(bv, sv[k]));
+                    const float hi = __fmaf_rn(bv, cv[k], __fmul_rn(av, sv[k]));
+                    const int grow = m0 + r0;
+                    if (grow < q_dim) {
+                        float* qd = e.q_out + static_cast<size_t>(t0 + t) * q_dim + grow;
+                        qd[0] = lo;
+                        qd[half] = hi;
+                    } else {
+                        const int kh = (grow - q_dim) / hd;
+                        __nv_bfloat16* kd = e.kv_pool +
+                            kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 0, kh, s_slot[t0 + t]) + i;
+                        kd[0] = __float2bfloat16_rn(lo);
+                        kd[half] = __float2bfloat16_rn(hi);
+                    }
+                }
+            } else {
+                for (int idx = tid; idx < tn * 128; idx += kEpiThreads) {
+                    const int t = idx >> 7, r = idx & 127;
+                    const int ve = m0 + r - q_dim - kv_dim;
+                    e.kv_pool[kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 1, ve / hd, s_slot[t0 + t]) +
+                              ve % hd] = __float2bfloat16_rn(red[t * 128 + r]);
+                }
+            }
+        }
+    }
+}
 }  // namespace gemm_dev
 }  // namespace dd

@@ -11,7 +11,7 @@ from paper_2503_00784_b200 import SHAPES, Target, _lib  # noqa: E402
 
 t = Target(SHAPES["llama2_7b"], weight_seed=1, max_seq=512)
 t.prefill(list(range(16)))
-for w in (1, 16):
+for w in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16").split(",")]:
     N = 8 * 400 * 200
     buf = (C.c_uint64 * N)()
     nl, cpl = C.c_int(), C.c_int()
@@ -28,11 +28,12 @@ for w in (1, 16):
         mm = (v[:, 3] - t0) / 1e3   # last MMA issued
         ep = (v[:, 4] - t0) / 1e3   # epilogue done
         en = (v[:, 5] - t0) / 1e3   # CTA end
-        rows.append((names[i], st.min(), np.median(st), wt.min(), wt.max(), mm.max(), ep.max(), en.max()))
+        ld = (v[:, 6] - t0) / 1e3   # last accumulator landed
+        rows.append((names[i], st.min(), np.median(st), wt.min(), wt.max(), mm.max(), ep.max(), en.max(), ld.max(), np.median(ep - ld), (ep - ld).max()))
     tot = rows[-1][-1] - rows[0][1]
     print(f"w={w} total {tot:.1f} us over {nl.value} launches")
     for r in rows[:10] + rows[-6:]:
-        print("  %-5s start[min,med]=%8.1f %8.1f waitpass[min,max]=%8.1f %8.1f lastmma=%8.1f epi_end=%8.1f end=%8.1f" % r)
+        print("  %-5s start[min,med]=%8.1f %8.1f waitpass[min,max]=%8.1f %8.1f lastmma=%8.1f epi_end=%8.1f end=%8.1f acc_landed=%8.1f epi_after_land[med,max]=%6.1f %6.1f" % r)
     # averages per layer position
     for k, nm in enumerate(["qkv", "o", "gu", "down"]):
         rr = [rows[4 * l + k] for l in range(32)]
