@@ -1,4 +1,3 @@
-mkdir -p gpurun_out
-# one_pass 127: prefill 128 (1 pass of 128 -> W=128 GEMMs) then 3 W=127 passes; capture the 3rd GEMM (gate/up layer 0) of the 2nd pass
-ncu --set full --clock-control none --import-source on -k regex:gemm_sk -s 131 -c 1 -o gpurun_out/gemm127 python scripts/one_pass.py 127 128 > gpurun_out/gemm127.log 2>&1
-tail -3 gpurun_out/gemm127.log
+timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout -s KILL 120 python scripts/pass_ab.py 17,64,127,128 128
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_wide --csv --log-file gpurun_out/wide_launches.csv python scripts/one_pass.py 127 128 > /dev/null 2>&1

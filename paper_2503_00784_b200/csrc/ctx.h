@@ -53,6 +53,9 @@ struct dd_ctx {
     float* ss = nullptr;            // [256][d/128] deferred-RMSNorm sum-of-squares partials
     float* logits = nullptr;        // [256, vocab]
     CUtensorMap map_h, map_o, map_a;
+    CUtensorMap map_h128, map_o128, map_a128;  // 128-row boxes (prefill GEMM)
+    dd::GemmPlan wide_plans[5] = {};
+    float* ws_wide = nullptr;       // prefill GEMM stream-K partials
 
     __nv_bfloat16* kv_pool = nullptr;
     int32_t* page_table = nullptr;

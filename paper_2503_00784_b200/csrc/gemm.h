@@ -89,4 +89,12 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
                         int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                         cudaStream_t stream);
 
+// Prefill GEMM (gemm_wide.cu): tokens on M (<= 128, one TMEM lane each),
+// 256 weight rows on N; map_x128 has 128-row boxes.  n_out % 256 == 0.
+GemmPlan plan_gemm_wide(int n_out, int k);
+size_t gemm_wide_ws_floats(const GemmPlan& p);
+cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
+                             int w, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
+                             cudaStream_t stream);
+
 }  // namespace dd

@@ -1,0 +1,442 @@
+// Prefill GEMM (wide passes, 17..128 new tokens) for sm_100a.
+//
+// The decode GEMM puts 128 weight rows on M and the few tokens on N.  For a
+// prefill chunk that leaves the tensor core reading 8 KiB of shared memory per
+// 128x128x16 MMA, and it runs several times below its peak.  Here the tokens
+// are M (128, one TMEM lane per token) and the weights N = 256 rows, so each
+// 128x256x16 MMA reads 4 KiB of activations + 8 KiB of weights:
+//
+//   D[128 tokens, 256 weight rows] (+)= X[128, K] . Wtile[256, K]^T
+//
+// Same persistent stream-K skeleton as gemm.cu (one CTA per SM, equal
+// contiguous ranges of (256-row tile, k-block), TMEM double buffer of 2 x 256
+// columns, warp-specialised producer / MMA / epilogue).  A 256-row tile is two
+// consecutive pre-tiled 128-row tiles: one stage = two 16 KiB bulk copies of
+// weights + one 128-row TMA box of activations.
+//
+// Epilogue: TMEM lane = token, so each epilogue thread owns one token's 256
+// outputs and every fused epilogue is thread-local: RoPE pairs (i, i + hd/2),
+// SwiGLU gate/up halves and the residual sum of squares of a 128-row tile all
+// sit in the same thread.  Stream-K partials are stored [segment][row][token]
+// (coalesced over threads); the last segment reduces them in segment order.
+#include "common.cuh"
+#include "gemm.h"
+#include "gemm_epi.cuh"
+
+#include <algorithm>
+
+namespace dd {
+
+namespace {
+
+using gemm_dev::kABytes;
+using gemm_dev::kBlockK;
+using gemm_dev::sk_begin;
+using gemm_dev::sk_segments;
+
+constexpr int kWideM = 128;        // tokens per tile (TMEM lanes)
+constexpr int kWideThreads = 192;  // producer, MMA, 4 epilogue warps
+constexpr uint32_t kXBytes = kWideM * kBlockK * 2;  // 16 KiB of activations
+// NW = weight rows per tile (256, or 128 for the d_model-output GEMMs, whose
+// 32 row tiles would otherwise be split over ~9 stream-K segments each)
+template <int NW>
+struct WideCfg {
+    static constexpr int kHalves = NW / 128;
+    static constexpr uint32_t kWBytes = kHalves * kABytes;
+    static constexpr uint32_t kStageBytes = kWBytes + kXBytes;
+};
+
+__device__ __forceinline__ void wide_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// 16 consecutive weight-row columns [c0, c0 + 16) of this thread's token
+// (partials are [segment][row][token])
+__device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* part_base, int nseg,
+                                          size_t seg_stride, bool from_tmem, float* v) {
+    if (from_tmem) {
+        tmem_ld16(t_lane + c0, v);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+    for (int s0 = 0; s0 < nseg; s0 += 4) {
+        float pv[4][16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                pv[k][j] = s0 + k < nseg ? __ldcg(part_base + (s0 + k) * seg_stride + (c0 + j) * kWideM) : 0.0f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (s0 + k < nseg)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], pv[k][j]);
+    }
+}
+
+}  // namespace
+
+template <int NW>
+__global__ void __launch_bounds__(kWideThreads, 1)
+    gemm_wide_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap map_x,
+                     GemmArgs a) {
+    constexpr int kWideN = NW;
+    constexpr int kHalves = WideCfg<NW>::kHalves;
+    constexpr uint32_t kWBytes = WideCfg<NW>::kWBytes;
+    constexpr uint32_t kStageBytes = WideCfg<NW>::kStageBytes;
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int P = gridDim.x, c = blockIdx.x;
+    const int tiles = a.n_out / kWideN;  // NW-row tiles
+    const long T = static_cast<long>(tiles) * a.nkb;
+    const long g0 = sk_begin(c, T, P), g1 = sk_begin(c + 1, T, P);
+    const int len = static_cast<int>(g1 - g0);
+    const int S = a.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ int s_last;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map_x);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<2 * NW>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    const int tile_lo = len > 0 ? static_cast<int>(g0 / a.nkb) : 0;
+    const int tile_hi = len > 0 ? static_cast<int>((g1 - 1) / a.nkb) : -1;
+
+    if (warp == 0) {
+        if (lane == 0 && len > 0) {
+            // ---------------- producer ----------------
+            const uint64_t pol_w = policy_evict_first();
+            const uint64_t pol_x = policy_evict_last();
+            const int nkb = a.nkb;
+            auto wsrc = [&](long g, int half) {
+                const long tile = g / nkb, kb = g % nkb;
+                return w_tiled + (static_cast<size_t>(kHalves * tile + half) * nkb + kb) * 8192;
+            };
+            // weights do not depend on the previous kernel: the first S stages are
+            // requested before griddepcontrol.wait, the activations after it
+            const int pre = min(S, len);
+            for (int i = 0; i < pre; ++i) {
+                uint8_t* st = smem + i * kStageBytes;
+                mbar_arrive_expect_tx(&full[i], kStageBytes);
+#pragma unroll
+                for (int hh = 0; hh < kHalves; ++hh)
+                    bulk_load(st + hh * kABytes, wsrc(g0 + i, hh), kABytes, &full[i], pol_w);
+            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            int s = 0;
+            uint32_t ph = 0;
+            int kb = static_cast<int>(g0 % nkb);
+            for (int i = 0; i < len; ++i) {
+                uint8_t* st = smem + s * kStageBytes;
+                if (i >= pre) {
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+                    for (int hh = 0; hh < kHalves; ++hh)
+                        bulk_load(st + hh * kABytes, wsrc(g0 + i, hh), kABytes, &full[s], pol_w);
+                }
+                tma_load_2d(st + kWBytes, &map_x, &full[s], kb * kBlockK, 0, pol_x);
+                if (++kb == nkb) kb = 0;
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && len > 0) {
+            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = idesc_bf16_f32(kWideM, kWideN);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int tile = tile_lo, u = 0; tile <= tile_hi; ++tile, ++u) {
+                const long lo = max(g0, static_cast<long>(tile) * a.nkb);
+                const long hi = min(g1, static_cast<long>(tile + 1) * a.nkb);
+                const int b = u & 1;
+                if (u >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>(((u >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t acc = tmem + static_cast<uint32_t>(b * kWideN);
+                for (long g = lo; g < hi; ++g) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t sw = smem_u32(smem + s * kStageBytes);
+                    const uint64_t bdesc = sw128_kmajor_desc(sw);             // weights: N = 256
+                    const uint64_t adesc = sw128_kmajor_desc(sw + kWBytes);   // tokens:  M = 128
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (g != lo || k != 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                umma_commit(&tfull[b]);
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2..5: thread = token ----------------
+        const int q = warp & 3;
+        const int tok = q * 32 + lane;  // TMEM lane
+        const int tid = threadIdx.x - 64;
+        const GemmEpiParams& e = a.epi;
+        const bool valid = tok < a.w;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        // pass-level constants of this thread's token
+        float rn = 1.0f;
+        if (e.ss_in != nullptr && valid) {
+            const float* ssr = e.ss_in + static_cast<size_t>(tok) * e.ss_tiles;
+            float acc = 0.0f;
+            for (int i0 = 0; i0 < e.ss_tiles; i0 += 16) {
+                float v16[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v16[j] = i0 + j < e.ss_tiles ? __ldcg(ssr + i0 + j) : 0.0f;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (i0 + j < e.ss_tiles) acc = __fadd_rn(acc, v16[j]);
+            }
+            rn = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(e.norm_d)), e.eps));
+        }
+        int page = 0, slot = 0, pos = 0;
+        if (e.kind == kEpiQkvRope) {
+            pos = e.ps->n_cached + tok;
+            page = e.page_table[pos / e.page_size];
+            slot = pos % e.page_size;
+        }
+        const int tiles128 = a.n_out / 128;
+        for (int tile = tile_lo, u = 0; tile <= tile_hi; ++tile, ++u) {
+            int nseg, seg;
+            sk_segments(tile, a.nkb, T, P, c, &nseg, &seg);
+            const int b = u & 1;
+            mbar_wait(&tfull[b], static_cast<uint32_t>((u >> 1) & 1));
+            __syncwarp();
+            tc_fence_after();
+            const uint32_t t_lane = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * kWideN);
+            const size_t seg_stride = static_cast<size_t>(kWideN) * kWideM;
+            float* tile_part = a.ws + static_cast<size_t>(tile) * a.max_seg * seg_stride;
+            bool from_tmem = true;
+            if (nseg > 1) {
+                // this segment's partial: [row][token], coalesced over threads
+                float* mine = tile_part + seg * seg_stride + tok;
+                for (int c0 = 0; c0 < kWideN; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(t_lane + c0, v);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) mine[(c0 + j) * kWideM] = v[j];
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[b]);
+                __threadfence();
+                wide_bar();
+                if (tid == 0) s_last = atomicAdd(&e.counters[tile], 1) == nseg - 1;
+                wide_bar();
+                if (!s_last) continue;
+                __threadfence();
+                from_tmem = false;
+            }
+            const float* pbase = tile_part + tok;
+            const int m0 = tile * kWideN;
+            if (e.kind == kEpiStore || e.kind == kEpiResidual) {
+                for (int h = 0; h < kHalves; ++h) {  // 128-row halves (ss tiles)
+                    float ss = 0.0f;
+                    for (int c0 = h * 128; c0 < h * 128 + 128; c0 += 16) {
+                        float v[16];
+                        load_cols(t_lane, c0, pbase, nseg, seg_stride, from_tmem, v);
+                        if (e.ss_in != nullptr)
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rn);
+                        if (!valid) continue;
+                        float* dst = e.out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
+                        if (e.kind == kEpiResidual) {
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4) {
+                                const float4 x = __ldcg(reinterpret_cast<const float4*>(dst + j));
+                                v[j] = __fadd_rn(x.x, v[j]);
+                                v[j + 1] = __fadd_rn(x.y, v[j + 1]);
+                                v[j + 2] = __fadd_rn(x.z, v[j + 2]);
+                                v[j + 3] = __fadd_rn(x.w, v[j + 3]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        if (e.kind == kEpiResidual && e.u_out != nullptr) {
+                            __nv_bfloat16* uo = e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                uo[j] = __float2bfloat16_rn(__fmul_rn(v[j], e.gain[m0 + c0 + j]));
+                                ss = __fmaf_rn(v[j], v[j], ss);
+                            }
+                        }
+                    }
+                    if (e.kind == kEpiResidual && e.u_out != nullptr && valid)
+                        e.ss_out[static_cast<size_t>(tok) * tiles128 + kHalves * tile + h] = ss;
+                }
+            } else if (e.kind == kEpiSwiGLU) {
+                const int ffn = a.n_out / 2;
+                for (int h = 0; h < kHalves; ++h)
+                    for (int k = 0; k < 4; ++k) {
+                        float g[16], up[16];
+                        load_cols(t_lane, h * 128 + 16 * k, pbase, nseg, seg_stride, from_tmem, g);
+                        load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nseg, seg_stride, from_tmem, up);
+                        if (!valid) continue;
+                        __nv_bfloat16* dst = e.out_bf + static_cast<size_t>(tok) * ffn + (kHalves * tile + h) * 64 + 16 * k;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const float gv = __fmul_rn(g[j], rn), uv = __fmul_rn(up[j], rn);
+                            const float silu = __fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv)));
+                            dst[j] = __float2bfloat16_rn(__fmul_rn(silu, uv));
+                        }
+                    }
+            } else {  // kEpiQkvRope
+                const ModelDims& md = e.m;
+                const int hd = md.head_dim, half = hd / 2;
+                const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+                for (int h = 0; h < kHalves; ++h) {
+                    const int r0 = m0 + h * 128;  // first weight row of this 128-row half
+                    if (r0 < q_dim + kv_dim) {
+                        // pairs (i, i + half) of every head in the half
+                        for (int hb = 0; hb < 128; hb += hd)
+                            for (int i0 = 0; i0 < half; i0 += 16) {
+                                float lo_v[16], hi_v[16];
+                                load_cols(t_lane, h * 128 + hb + i0, pbase, nseg, seg_stride, from_tmem, lo_v);
+                                load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nseg, seg_stride, from_tmem, hi_v);
+                                if (!valid) continue;
+                                const int grow = r0 + hb;  // first row of the head
+                                float* qd = grow < q_dim ? e.q_out + static_cast<size_t>(tok) * q_dim + grow : nullptr;
+                                __nv_bfloat16* kd =
+                                    grow < q_dim ? nullptr
+                                                 : e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 0,
+                                                                         (grow - q_dim) / hd, slot);
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) {
+                                    const int i = i0 + j;
+                                    const float av = __fmul_rn(lo_v[j], rn), bv = __fmul_rn(hi_v[j], rn);
+                                    const float cs = e.rope_cos[static_cast<size_t>(pos) * half + i];
+                                    const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
+                                    const float lo = __fmaf_rn(av, cs, -__fmul_rn(bv, sn));
+                                    const float hi = __fmaf_rn(bv, cs, __fmul_rn(av, sn));
+                                    if (qd) {
+                                        qd[i] = lo;
+                                        qd[i + half] = hi;
+                                    } else {
+                                        kd[i] = __float2bfloat16_rn(lo);
+                                        kd[i + half] = __float2bfloat16_rn(hi);
+                                    }
+                                }
+                            }
+                    } else {
+                        for (int c0 = 0; c0 < 128; c0 += 16) {
+                            float v[16];
+                            load_cols(t_lane, h * 128 + c0, pbase, nseg, seg_stride, from_tmem, v);
+                            if (!valid) continue;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const int ve = r0 + c0 + j - q_dim - kv_dim;
+                                e.kv_pool[kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd] =
+                                    __float2bfloat16_rn(__fmul_rn(v[j], rn));
+                            }
+                        }
+                    }
+                }
+            }
+            if (from_tmem) {
+                tc_fence_before();
+                mbar_arrive(&tempty[b]);
+            } else {
+                wide_bar();
+                if (tid == 0) e.counters[tile] = 0;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<2 * NW>(tmem);
+#endif
+}
+
+GemmPlan plan_gemm_wide(int n_out, int k) {
+    GemmPlan p{};
+    // 128-row tiles when 256-row tiles would leave fewer than 64 of them
+    const int nw = (n_out % 256 == 0 && n_out / 256 >= 64) ? 256 : 128;
+    p.tiles = n_out / nw;
+    p.nkb = k / kBlockK;
+    const long T = static_cast<long>(p.tiles) * p.nkb;
+    const uint32_t stage = (nw == 256 ? WideCfg<256>::kStageBytes : WideCfg<128>::kStageBytes);
+    p.stages = nw == 256 ? 4 : 6;
+    p.smem_bytes = static_cast<int>(p.stages * stage + 1024 + 64 * 8);
+    p.tmem_cols = 2 * nw;
+    p.ctas = static_cast<int>(std::min<long>(kNumSMs, T));
+    int ms = 1;
+    for (int t = 0; t < p.tiles; ++t) {
+        const int f = gemm_dev::sk_owner(static_cast<long>(t) * p.nkb, T, p.ctas);
+        int nseg, seg;
+        sk_segments(t, p.nkb, T, p.ctas, f, &nseg, &seg);
+        ms = std::max(ms, nseg);
+    }
+    p.max_seg = ms;
+    return p;
+}
+
+size_t gemm_wide_ws_floats(const GemmPlan& p) {
+    return static_cast<size_t>(p.tiles) * p.max_seg * (p.tmem_cols / 2) * kWideM;
+}
+
+cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
+                             int w, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
+                             cudaStream_t stream) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(gemm_wide_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(gemm_wide_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr_set = true;
+    }
+    GemmArgs a{};
+    a.n_out = n_out;
+    a.k = k;
+    a.w = w;
+    a.nt = kWideM;
+    a.tiles = plan.tiles;
+    a.nkb = plan.nkb;
+    a.stages = plan.stages;
+    a.max_seg = plan.max_seg;
+    a.tmem_buf = plan.tmem_cols / 2;
+    a.ws = ws;
+    a.epi = epi;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(plan.ctas, 1, 1);
+    cfg.blockDim = dim3(kWideThreads, 1, 1);
+    cfg.dynamicSmemBytes = plan.smem_bytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (plan.tmem_cols == 512) return cudaLaunchKernelEx(&cfg, gemm_wide_kernel<256>, w_tiled, *map_x128, a);
+    return cudaLaunchKernelEx(&cfg, gemm_wide_kernel<128>, w_tiled, *map_x128, a);
+}
+
+}  // namespace dd

@@ -87,12 +87,21 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
+    // prefill widths (17..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu)
+    const bool wide = w > 16 && w <= 128 && ctx->ws_wide != nullptr;
     auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
                     const GemmEpiParams& ep) -> cudaError_t {
         int n_out, k;
         gemm_shape(ctx, id, &n_out, &k);
-        const GemmPlan& p = plan_for(ctx, id, nt);
-        cudaError_t r = launch_gemm(mw, mx, n_out, k, w, nt, p, ctx->ws, ep, s);
+        cudaError_t r;
+        if (wide) {
+            const CUtensorMap* m128 = mx == &ctx->map_h ? &ctx->map_h128
+                                      : mx == &ctx->map_o ? &ctx->map_o128 : &ctx->map_a128;
+            r = launch_gemm_wide(mw, m128, n_out, k, w, ctx->wide_plans[id], ctx->ws_wide, ep, s);
+        } else {
+            const GemmPlan& p = plan_for(ctx, id, nt);
+            r = launch_gemm(mw, mx, n_out, k, w, nt, p, ctx->ws, ep, s);
+        }
         mark(0);
         return r;
     };
@@ -477,7 +486,10 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     CK(cudaMemset(ctx->a, 0, sizeof(__nv_bfloat16) * R * m.ffn));
     if (make_tmap_bf16(&ctx->map_h, ctx->h, R, d_, 16) ||
         make_tmap_bf16(&ctx->map_o, ctx->o, R, m.q_dim(), 16) ||
-        make_tmap_bf16(&ctx->map_a, ctx->a, R, m.ffn, 16))
+        make_tmap_bf16(&ctx->map_a, ctx->a, R, m.ffn, 16) ||
+        make_tmap_bf16(&ctx->map_h128, ctx->h, R, d_, 128) ||
+        make_tmap_bf16(&ctx->map_o128, ctx->o, R, m.q_dim(), 128) ||
+        make_tmap_bf16(&ctx->map_a128, ctx->a, R, m.ffn, 128))
         return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
     size_t ws_floats = 0;
     for (int id = 0; id < kNumGemm; ++id) {
@@ -489,6 +501,20 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
         }
     }
     CK(cudaMalloc(&ctx->ws, sizeof(float) * ws_floats));
+    {
+        // tokens-on-M prefill GEMM: every shape must split into 256-row tiles
+        bool ok = true;
+        size_t wide_floats = 0;
+        for (int id = 0; id < kNumGemm; ++id) {
+            int n_out, k;
+            gemm_shape(ctx, id, &n_out, &k);
+            ok = ok && n_out % 128 == 0;
+            if (!ok) break;
+            ctx->wide_plans[id] = plan_gemm_wide(n_out, k);
+            wide_floats = std::max(wide_floats, gemm_wide_ws_floats(ctx->wide_plans[id]));
+        }
+        if (ok) CK(cudaMalloc(&ctx->ws_wide, sizeof(float) * wide_floats));
+    }
     CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
     CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
     CK(cudaMalloc(&ctx->ss, sizeof(float) * R * (m.d / 128)));
@@ -585,7 +611,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->ws, ctx->logits, ctx->kv_pool, ctx->page_table, ctx->rope_cos,
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
                    ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
-                   ctx->counters, ctx->ss, ctx->pass_flags, ctx->pass_ws, ctx->pass_counters,
+                   ctx->counters, ctx->ss, ctx->ws_wide, ctx->pass_flags, ctx->pass_ws, ctx->pass_counters,
                    ctx->attn_part, ctx->attn_cnt};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -646,8 +672,9 @@ int dd_prefill(dd_ctx* ctx, const int32_t* tokens, int n) {
     if (!ctx || (!tokens && n > 0) || n < 0) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
     if (!ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
     CK(cudaSetDevice(ctx->device));
-    for (int i = 0; i < n; i += kMaxPassTokens) {
-        const int w = std::min(kMaxPassTokens, n - i);
+    constexpr int kPrefillChunk = 128;  // the tokens-on-M GEMM's tile height
+    for (int i = 0; i < n; i += kPrefillChunk) {
+        const int w = std::min(kPrefillChunk, n - i);
         int rc = run_pass(ctx, tokens + i, w, false);
         if (rc != DD_OK) return rc;
     }
