@@ -84,6 +84,10 @@ struct dd_ctx {
     int epoch = 0;                   // pass sequence number (flag value)
     int* pass_flags = nullptr;       // [flags][kFlagReplicas] x 128-byte lines
     size_t pass_flag_count = 0;
+    int* sk_prefix_d = nullptr;      // weighted stream-K partition by SM rank (or null)
+    int* rank_of_smid_d = nullptr;
+    std::vector<int> sk_prefix_h;
+    std::vector<int*> pass_begins;   // device begin tables of the phase tables
     float* pass_ws = nullptr;        // 2 x stream-K partials (alternating GEMM phases)
     int* pass_counters = nullptr;    // 2 x [512] segment arrival counters
     size_t pass_ws_half = 0;         // floats per half

@@ -581,6 +581,44 @@ struct RingPos {
     }
 };
 
+// Stream-K partition of a phase over the CTAs, optionally weighted per SM:
+// SMs do not stream HBM equally fast (a stable, per-SM property measured at
+// context set-up), so rank r (the rank of the CTA's SM) owns
+// blocks [prefix[r] * T / prefix[P], prefix[r+1] * T / prefix[P]).  With no
+// calibration (prefix == nullptr) the partition is the uniform sk_begin.
+struct Partition {
+    const int* begins;  // [P + 1] block offsets of this phase's ranks, or nullptr (uniform)
+    int P;
+    __device__ __forceinline__ int begin(int r, int T) const {
+        return begins != nullptr ? begins[r] : static_cast<int>(sk_begin(r, T, P));
+    }
+    __device__ int owner(int g, int T) const {  // rank whose range holds block g
+        int lo = 0, hi = P - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (begin(mid, T) <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    }
+    // segments of `tile`: the non-empty ranks covering its k-blocks; position of r
+    __device__ void segments(int tile, int nkb, int T, int r, int* nseg, int* seg) const {
+        if (begins == nullptr) {
+            sk_segments(tile, nkb, T, P, r, nseg, seg);
+            return;
+        }
+        const int first = owner(tile * nkb, T), last = owner((tile + 1) * nkb - 1, T);
+        int n = 0, pos = 0;
+        for (int k = first; k <= last; ++k)
+            if (begin(k + 1, T) > begin(k, T)) {
+                if (k == r) pos = n;
+                ++n;
+            }
+        *nseg = n;
+        *seg = pos;
+    }
+};
+
 }  // namespace
 
 __global__ void __launch_bounds__(kPassThreads, 1)
@@ -591,7 +629,14 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nctas = gridDim.x, c = blockIdx.x;
+    const int nctas = gridDim.x;
+    int c;  // this CTA's rank in the stream-K partition
+    {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        c = P.rank_of_smid != nullptr ? P.rank_of_smid[smid] : static_cast<int>(blockIdx.x);
+    }
+
     const int S = P.stages, nt = P.nt;
     const uint32_t b_bytes = static_cast<uint32_t>(nt) * 128u;
     const uint32_t stage_bytes = kABytes + b_bytes;
@@ -639,6 +684,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const uint32_t tmem = *tmem_slot;
     const int epoch = P.ps->epoch;
     const int W = P.ps->w;
+    if (threadIdx.x == 0 && P.trace) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pass_put(P, 0, 10, smid);  // debug: SM of this CTA
+    }
     const int qtiles = (W + 15) / 16;
 
     if (warp == 0) {
@@ -659,8 +709,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                             const PassPhase& q = P.phases[pf_p];
                             if (q.type != kPhGemm) continue;
                             const long T = static_cast<long>(q.a.tiles) * q.a.nkb;
-                            pf_g = sk_begin(c, T, nctas);
-                            pf_g1 = sk_begin(c + 1, T, nctas);
+                            const Partition pq{q.begins, nctas};
+                            pf_g = pq.begin(c, static_cast<int>(T));
+                            pf_g1 = pq.begin(c + 1, static_cast<int>(T));
                             pf_w = q.w;
                             if (pf_g < pf_g1) break;
                         }
@@ -677,8 +728,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 const PassPhase& ph = P.phases[p];
                 if (ph.type != kPhGemm) continue;
                 const long T = static_cast<long>(ph.a.tiles) * ph.a.nkb;
-                const int g0 = static_cast<int>(sk_begin(c, T, nctas));
-                const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+                const Partition part{ph.begins, nctas};
+                const int g0 = part.begin(c, static_cast<int>(T));
+                const int g1 = part.begin(c + 1, static_cast<int>(T));
                 const __nv_bfloat16* src = ph.w + static_cast<size_t>(g0) * 8192;
                 pass_stamp(P, p, 0);
                 for (int g = g0; g < g1; ++g, src += 8192) {
@@ -706,8 +758,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             if (ph.type != kPhGemm) continue;
             const int nkb = ph.a.nkb;
             const long T = static_cast<long>(ph.a.tiles) * nkb;
-            const int g0 = static_cast<int>(sk_begin(c, T, nctas));
-            const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+            const Partition part{ph.begins, nctas};
+            const int g0 = part.begin(c, static_cast<int>(T));
+            const int g1 = part.begin(c + 1, static_cast<int>(T));
             if (g1 <= g0) continue;
             if (lane == 0) pass_stamp(P, p, 7);
             wait_phase_inputs(P, ph.x_src, ph.x_flag, nkb, g0, g1, epoch, qtiles, lane);
@@ -739,8 +792,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 if (ph.type != kPhGemm) continue;
                 const int nkb = ph.a.nkb;
                 const long T = static_cast<long>(ph.a.tiles) * nkb;
-                const int g0 = static_cast<int>(sk_begin(c, T, nctas));
-                const int g1 = static_cast<int>(sk_begin(c + 1, T, nctas));
+                const Partition part{ph.begins, nctas};
+                const int g0 = part.begin(c, static_cast<int>(T));
+                const int g1 = part.begin(c + 1, static_cast<int>(T));
                 if (g1 <= g0) continue;
                 const int tile_lo = g0 / nkb, tile_hi = (g1 - 1) / nkb;
                 for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
@@ -808,7 +862,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             // GEMM epilogue
             const int nkb = ph.a.nkb;
             const long T = static_cast<long>(ph.a.tiles) * nkb;
-            const long g0 = sk_begin(c, T, nctas), g1 = sk_begin(c + 1, T, nctas);
+            const Partition part{ph.begins, nctas};
+            const long g0 = part.begin(c, static_cast<int>(T)), g1 = part.begin(c + 1, static_cast<int>(T));
             if (g1 <= g0) continue;
             if (tid == 0) s_args = ph.a;
             const bool fast = W <= kChunk;
@@ -860,7 +915,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const int tile_lo = static_cast<int>(g0 / nkb), tile_hi = static_cast<int>((g1 - 1) / nkb);
             for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
                 int nseg, seg;
-                sk_segments(tile, nkb, T, nctas, c, &nseg, &seg);
+                part.segments(tile, nkb, static_cast<int>(T), c, &nseg, &seg);
                 const int b = u & 1;
                 float xv[kChunk];
                 float gcol = 1.0f;

@@ -29,6 +29,7 @@ struct PassPhase {
     int qkv_flag;  // attention: flag base of the layer's QKV tiles
     int pad_;
     const __nv_bfloat16* w;  // pre-tiled weights (GEMM)
+    const int* begins;       // [149] stream-K range starts by rank (weighted), or nullptr
     GemmArgs a;              // GEMM shape + fused epilogue
 };
 
@@ -41,6 +42,7 @@ struct PassParams {
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
     int poll_mode;  // debug: flag polling variant
     int early;      // stages a phase may fetch before its activations are ready (-1: no limit)
+    const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     unsigned long long* trace;
     unsigned long long* trace2;  // debug: per-tile publish times / poll batch times  // debug: [CTA][phase][4] globaltimer stamps, or nullptr
     const PassState* ps;

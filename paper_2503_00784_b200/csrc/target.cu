@@ -26,6 +26,9 @@ using namespace dd;
 
 thread_local std::string g_last_error;
 
+extern "C" int dd_debug_pass_timeline(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_phases);
+extern "C" int dd_pass_balance(dd_ctx* ctx);
+
 #define CK(expr)                                                                      \
     do {                                                                              \
         cudaError_t e_ = (expr);                                                      \
@@ -153,15 +156,38 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
 namespace {
 
 // max stream-K segments of one tile when T blocks are cut over kNumSMs CTAs
-int pass_max_seg(int tiles, int nkb) {
-    const long T = static_cast<long>(tiles) * nkb;
-    int ms = 1;
-    for (int t = 0; t < tiles; ++t) {
-        const int f = gemm_dev::sk_owner(static_cast<long>(t) * nkb, T, kNumSMs);
-        int nseg, seg;
-        gemm_dev::sk_segments(t, nkb, T, kNumSMs, f, &nseg, &seg);
-        ms = std::max(ms, nseg);
+// host mirror of pass.cu's Partition (weighted when calibrated)
+struct HostPartition {
+    const std::vector<int>* prefix;  // [P + 1] or empty
+    int P;
+    int begin(int r, int T) const {
+        if (prefix == nullptr || prefix->empty()) return static_cast<int>(gemm_dev::sk_begin(r, T, P));
+        return static_cast<int>(static_cast<unsigned long long>((*prefix)[r]) * static_cast<unsigned>(T) /
+                                static_cast<unsigned>((*prefix)[P]));
     }
+    int owner(int g, int T) const {
+        int lo = 0, hi = P - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (begin(mid, T) <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    }
+    int nseg(int tile, int nkb, int T) const {
+        const int first = owner(tile * nkb, T), last = owner((tile + 1) * nkb - 1, T);
+        int n = 0;
+        for (int k = first; k <= last; ++k)
+            if (begin(k + 1, T) > begin(k, T)) ++n;
+        return n;
+    }
+};
+
+int pass_max_seg(const dd_ctx* ctx, int tiles, int nkb) {
+    const HostPartition hp{&ctx->sk_prefix_h, kNumSMs};
+    const int T = tiles * nkb;
+    int ms = 1;
+    for (int t = 0; t < tiles; ++t) ms = std::max(ms, hp.nseg(t, nkb, T));
     return ms;
 }
 
@@ -222,7 +248,7 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
         a.nt = nt;
         a.tiles = n_outr / 128;
         a.nkb = k / 64;
-        a.max_seg = pass_max_seg(a.tiles, a.nkb);
+        a.max_seg = pass_max_seg(ctx, a.tiles, a.nkb);
         a.tmem_buf = tmem_buf_for(nt);
         a.ws = ctx->pass_ws + (gidx & 1) * ctx->pass_ws_half;
         ep.counters = ctx->pass_counters + (gidx & 1) * 512;
@@ -271,6 +297,25 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
     }
     if (static_cast<size_t>(next_flag) > ctx->pass_flag_count)
         return ctx_fail(ctx, DD_E_CAPACITY, "pass flag table too small");
+    if (!ctx->sk_prefix_h.empty()) {
+        // weighted partition: per GEMM phase, the block offset of every rank
+        const std::vector<int>& pre = ctx->sk_prefix_h;
+        std::vector<int> hb;
+        std::vector<size_t> off(ph.size(), 0);
+        for (size_t i = 0; i < ph.size(); ++i) {
+            if (ph[i].type != kPhGemm) continue;
+            const unsigned T = static_cast<unsigned>(ph[i].a.tiles * ph[i].a.nkb);
+            off[i] = hb.size();
+            for (int r = 0; r <= kNumSMs; ++r)
+                hb.push_back(static_cast<int>(static_cast<unsigned long long>(pre[r]) * T / pre[kNumSMs]));
+        }
+        int* db = nullptr;
+        CK(cudaMalloc(&db, sizeof(int) * hb.size()));
+        CK(cudaMemcpy(db, hb.data(), sizeof(int) * hb.size(), cudaMemcpyHostToDevice));
+        ctx->pass_begins.push_back(db);
+        for (size_t i = 0; i < ph.size(); ++i)
+            if (ph[i].type == kPhGemm) ph[i].begins = db + off[i];
+    }
     PassPhase* d = nullptr;
     CK(cudaMalloc(&d, sizeof(PassPhase) * ph.size()));
     CK(cudaMemcpy(d, ph.data(), sizeof(PassPhase) * ph.size(), cudaMemcpyHostToDevice));
@@ -319,6 +364,7 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.attn_cnt = ctx->attn_cnt;
     p.trace = trace;
     p.trace2 = trace2;
+    p.rank_of_smid = ctx->rank_of_smid_d;
     CK(launch_pass_kernel(ctx->map_h, ctx->map_o, ctx->map_a, p, smem, ctx->stream));
     return DD_OK;
 }
@@ -545,7 +591,7 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
         for (int id = 0; id < kNumGemm; ++id) {
             int n_out, k;
             gemm_shape(ctx, id, &n_out, &k);
-            half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(n_out / 128, k / 64) *
+            half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(ctx, n_out / 128, k / 64) *
                                       kMaxPassTokens * 128);
         }
         ctx->pass_ws_half = half;
@@ -599,6 +645,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
     cudaDeviceSynchronize();
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : ctx->pass_phases) cudaFree(kv.second);
+    for (int* b : ctx->pass_begins) cudaFree(b);
     for (auto& L : ctx->layers) {
         cudaFree(L.qkv);
         cudaFree(L.o);
@@ -612,7 +659,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
                    ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
                    ctx->counters, ctx->ss, ctx->ws_wide, ctx->pass_flags, ctx->pass_ws, ctx->pass_counters,
-                   ctx->attn_part, ctx->attn_cnt};
+                   ctx->attn_part, ctx->attn_cnt, ctx->sk_prefix_d, ctx->rank_of_smid_d};
     for (void* p : dev)
         if (p) cudaFree(p);
     if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
@@ -665,6 +712,10 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
     CK(cudaStreamSynchronize(s));
     if (d_src) cudaFree(d_src);
     ctx->weights_ready = true;
+    // SM-weighted stream-K partition: opt-in (measured no faster on the pool's
+    // B200s: the slow SMs share a saturated resource)
+    const char* bal = getenv("DD_PASS_BALANCE");
+    if (ctx->use_pass_kernel && bal && bal[0] == '1') return dd_pass_balance(ctx);
     return DD_OK;
 }
 
@@ -1159,6 +1210,86 @@ int dd_debug_pass_timeline(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entri
     cudaFree(d2);
     *n_phases = n;
     ctx->last_w = 0;
+    return DD_OK;
+}
+
+// Weighted stream-K partition for the persistent pass kernel: time every SM's
+// streaming of the gate/up phases (the largest) over a few decode passes and
+// give each SM a share proportional to its speed.  Runs once,
+// before any pass graph is captured; the phase tables are rebuilt afterwards.
+int dd_pass_balance(dd_ctx* ctx) {
+    if (!ctx || !ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
+    CK(cudaSetDevice(ctx->device));
+    const int w = 8;
+    const int L = ctx->m.n_layers;
+    const int nph_exp = 5 * L + 2;
+    const size_t need = static_cast<size_t>(kNumSMs) * nph_exp * 12;
+    std::vector<uint64_t> tr(need);
+    std::vector<double> span(1024, 0.0);
+    std::vector<int> seen(1024, 0);
+    const int n0 = ctx->n_cached;
+    for (int rep = 0; rep < 3; ++rep) {
+        int nph = 0;
+        int rc = dd_debug_pass_timeline(ctx, w, tr.data(), need, &nph);
+        if (rc) return rc;
+        if (rep == 0) continue;  // warm-up
+        for (int b = 0; b < kNumSMs; ++b) {
+            const int smid = static_cast<int>(tr[(static_cast<size_t>(b) * nph + 0) * 12 + 10]);
+            if (smid < 0 || smid >= 1024) continue;
+            for (int l = 1; l + 1 < L || (L <= 2 && l < L); ++l) {
+                const size_t base = (static_cast<size_t>(b) * nph + 1 + 5 * l + 3) * 12;
+                if (tr[base + 1] == 0 || tr[base + 2] <= tr[base + 1]) continue;
+                span[smid] += static_cast<double>(tr[base + 2] - tr[base + 1]);
+                seen[smid] += 1;
+            }
+        }
+    }
+    ctx->n_cached = n0;
+    std::vector<int> smids;
+    double mean = 0.0;
+    for (int i = 0; i < 1024; ++i)
+        if (seen[i]) {
+            smids.push_back(i);
+            span[i] /= seen[i];
+            mean += span[i];
+        }
+    if (static_cast<int>(smids.size()) != kNumSMs) return DD_OK;  // keep the uniform partition
+    mean /= smids.size();
+    std::vector<int> rank_of(1024, 0), prefix(kNumSMs + 1, 0);
+    for (int r = 0; r < kNumSMs; ++r) {
+        const int sm = smids[r];
+        rank_of[sm] = r;
+        const int wgt = std::max(40, std::min(96, static_cast<int>(std::lround(64.0 * mean / span[sm]))));
+        prefix[r + 1] = prefix[r] + wgt;
+    }
+    if (!ctx->sk_prefix_d) {
+        CK(cudaMalloc(&ctx->sk_prefix_d, sizeof(int) * (kNumSMs + 1)));
+        CK(cudaMalloc(&ctx->rank_of_smid_d, sizeof(int) * 1024));
+    }
+    CK(cudaMemcpy(ctx->sk_prefix_d, prefix.data(), sizeof(int) * prefix.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->rank_of_smid_d, rank_of.data(), sizeof(int) * rank_of.size(), cudaMemcpyHostToDevice));
+    ctx->sk_prefix_h = prefix;
+    // phase tables and partial buffers depend on the partition: rebuild
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    ctx->graphs.clear();
+    for (auto& kv : ctx->pass_phases) cudaFree(kv.second);
+    ctx->pass_phases.clear();
+    for (int* b : ctx->pass_begins) cudaFree(b);
+    ctx->pass_begins.clear();
+    ctx->pass_nphases.clear();
+    size_t half = 0;
+    for (int id = 0; id < kNumGemm; ++id) {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(ctx, n_out / 128, k / 64) *
+                                  kMaxPassTokens * 128);
+    }
+    if (half > ctx->pass_ws_half) {
+        cudaFree(ctx->pass_ws);
+        ctx->pass_ws_half = half;
+        CK(cudaMalloc(&ctx->pass_ws, sizeof(float) * 2 * half));
+    }
     return DD_OK;
 }
 
