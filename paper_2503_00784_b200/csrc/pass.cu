@@ -156,8 +156,33 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     const int g = lane >> 2, c = lane & 3;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
     const int qd = md.q_dim();
-    __nv_bfloat16(*ks)[HD] = reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem);
-    __nv_bfloat16(*vs)[HD] = reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + kAttnChunk * HD * 2);
+    // two K/V chunk buffers: chunk i + 1 is staged while chunk i is computed
+    constexpr int kBufBytes = 2 * kAttnChunk * HD * 2;
+    auto ks_of = [&](int b) {
+        return reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + b * kBufBytes);
+    };
+    auto vs_of = [&](int b) {
+        return reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + b * kBufBytes + kAttnChunk * HD * 2);
+    };
+    auto stage = [&](int chunk, int b) {
+        __nv_bfloat16(*ks)[HD] = ks_of(b);
+        __nv_bfloat16(*vs)[HD] = vs_of(b);
+        const int kb = chunk * kAttnChunk;
+        for (int idx = tid; idx < kAttnChunk * CHK; idx += 128) {
+            const int kk = idx / CHK, ch = idx % CHK;
+            const int key = kb + kk;
+            const bool ok = key <= kmax;
+            const int kc = ok ? key : 0;
+            const int page = P.page_table[kc / P.page_size], slot = kc % P.page_size;
+            cp_async16(&ks[kk][k_chunk(kk, ch) * 8],
+                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 0, kvh, slot) + ch * 8,
+                       ok ? 16u : 0u);
+            cp_async16(&vs[kk][v_chunk<HD>(kk, ch) * 8],
+                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot) + ch * 8,
+                       ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 
     // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
     if (tid < 3) {  // q, k and v tiles polled in parallel
@@ -165,6 +190,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
         wait_flag(flag_poll(P.flags, ph.qkv_flag, row / 128), epoch);
     }
     epi_bar();
+    stage(grp, 0);  // the first chunk's K / V are in flight while Q is loaded
 
     const int pos_g = n0 + qt * 16 + g, pos_g8 = pos_g + 8;
     const bool v_g = qt * 16 + g < W, v_g8 = qt * 16 + g + 8 < W;
@@ -197,23 +223,18 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
     float m_g = -INFINITY, m_g8 = -INFINITY, l_g = 0.f, l_g8 = 0.f;
 
-    for (int chunk = grp; chunk < n_chunks; chunk += kAttnGroups) {
+    for (int i = 0, chunk = grp; chunk < n_chunks; ++i, chunk += kAttnGroups) {
         const int kb = chunk * kAttnChunk;
-        for (int idx = tid; idx < kAttnChunk * CHK; idx += 128) {
-            const int kk = idx / CHK, ch = idx % CHK;
-            const int key = kb + kk;
-            const bool ok = key <= kmax;
-            const int kc = ok ? key : 0;
-            const int page = P.page_table[kc / P.page_size], slot = kc % P.page_size;
-            cp_async16(&ks[kk][k_chunk(kk, ch) * 8],
-                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 0, kvh, slot) + ch * 8,
-                       ok ? 16u : 0u);
-            cp_async16(&vs[kk][v_chunk<HD>(kk, ch) * 8],
-                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot) + ch * 8,
-                       ok ? 16u : 0u);
+        const int b = i & 1;
+        if (chunk + kAttnGroups < n_chunks) {
+            stage(chunk + kAttnGroups, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        cp_async_wait_all();
         epi_bar();
+        __nv_bfloat16(*ks)[HD] = ks_of(b);
+        __nv_bfloat16(*vs)[HD] = vs_of(b);
         float s[NJ][4];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
@@ -295,7 +316,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
                 mma_bf16(acc[e], pa[kst], b0, b1);
             }
         }
-        epi_bar();  // the next chunk overwrites K / V
+        epi_bar();  // buffer b is refilled by the stage issued in the next iteration
     }
 #pragma unroll
     for (int off = 1; off <= 2; off <<= 1) {
@@ -642,7 +663,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const uint32_t stage_bytes = kABytes + b_bytes;
     const int hd = P.m.head_dim;
     uint8_t* kv_smem = smem + S * stage_bytes;                          // attention K/V chunk
-    float* red = reinterpret_cast<float*>(kv_smem + 2 * kAttnChunk * hd * 2);  // [kChunk][128]
+    float* red = reinterpret_cast<float*>(kv_smem + 4 * kAttnChunk * hd * 2);  // [kChunk][128]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -1096,7 +1117,7 @@ size_t pass_attn_cnt_ints(const ModelDims& m) { return static_cast<size_t>(m.n_h
 
 int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
     const int stage_bytes = static_cast<int>(kABytes) + nt * 128;
-    const int fixed = 1024 /* align */ + 2 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
+    const int fixed = 1024 /* align */ + 4 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
     const int budget = 225 * 1024 - 2048 /* static shared */;
     static const int cap = getenv("DD_PASS_STAGES") ? atoi(getenv("DD_PASS_STAGES")) : 8;
     int s = (budget - fixed) / stage_bytes;
