@@ -1,3 +1,4 @@
-timeout -s KILL 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout -s KILL 120 python scripts/pass_ab.py 1,8,16 2048
-timeout -s KILL 120 python scripts/pass_ab.py 1,8,16 128
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 python bench.py --workload config3 --no-cpu-baseline --steps 3 > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+cat gpurun_out/bench.json gpurun_out/bench_c3.json

@@ -122,3 +122,60 @@ def test_kv_truncate_rollback(tiny_pair):
     b = tgt.logits(0, 1)
     assert np.array_equal(a, b)
     assert tgt.kv_len() == len(ctx) + 3
+
+
+@pytest.mark.parametrize("w", [1, 8, 16, 17, 40, 128, 200])
+def test_tiny_pass_logits_all_paths(tiny_pair, w):
+    """Every pass width vs the oracle: decode widths run the persistent pass
+    kernel, 17..128 the tokens-on-M prefill GEMM, wider the per-launch GEMM."""
+    tgt, orc = tiny_pair
+    rng = np.random.default_rng(100 + w)
+    ctx = rng.integers(0, TINY["vocab"], 33).tolist()
+    new = rng.integers(0, TINY["vocab"], w).tolist()
+    tgt.truncate(0)
+    orc.truncate(0)
+    tgt.prefill(ctx)
+    orc.forward(ctx)
+    tgt.score(new)
+    g = tgt.logits(0, w)
+    o = orc.forward(new)
+    rel = np.abs(g - o).max() / np.abs(o).max()
+    assert rel < 2e-3, f"W={w}: relative logit error {rel}"
+
+
+def test_long_context_attention_vs_oracle(tiny_pair):
+    """A context of 300 keys: several 64-key chunks per chunk group (double-
+    buffered staging) and a multi-group merge, against the oracle."""
+    tgt, orc = tiny_pair
+    rng = np.random.default_rng(21)
+    ctx = rng.integers(0, TINY["vocab"], 300).tolist()
+    new = rng.integers(0, TINY["vocab"], 6).tolist()
+    tgt.truncate(0)
+    orc.truncate(0)
+    tgt.prefill(ctx)
+    orc.forward(ctx)
+    tgt.score(new)
+    g = tgt.logits(0, len(new))
+    o = orc.forward(new)
+    rel = np.abs(g - o).max() / np.abs(o).max()
+    assert rel < 2e-3, f"relative logit error {rel}"
+
+
+def test_pass_kernel_matches_per_launch_path(tiny_pair, monkeypatch):
+    """The persistent pass kernel and the one-launch-per-GEMM path agree."""
+    tgt, _ = tiny_pair
+    monkeypatch.setenv("DD_PASS_KERNEL", "0")
+    ref = Target(TINY, weight_seed=11, plant=PLANT, max_seq=512)
+    rng = np.random.default_rng(33)
+    ctx = rng.integers(0, TINY["vocab"], 50).tolist()
+    new = rng.integers(0, TINY["vocab"], 9).tolist()
+    out = []
+    for t in (tgt, ref):
+        t.truncate(0)
+        t.prefill(ctx)
+        t.score(new)
+        out.append(t.logits(0, len(new)))
+    ref.close()
+    rel = np.abs(out[0] - out[1]).max() / np.abs(out[1]).max()
+    assert rel < 1e-3, f"relative difference {rel}"
+    assert (out[0].argmax(-1) == out[1].argmax(-1)).all()
