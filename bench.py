@@ -330,13 +330,20 @@ def run_ours(args):
             "pass_ms": round(pass_ms, 4), "peak_source": peak_src}
         # same-run GPU baselines: target-only AR and conventional SpS
         base = {}
+        # same statistic as the headline: medians over the timed steps' prompts
+        n_base = min(3, args.steps)
         for mode, bud in (("vanilla", 2), ("sps", max(2, budget // 2))):
             c2 = EngineConfig(mode=mode, budget=bud, max_new_tokens=NEW_TOKENS,
                               greedy=wl["greedy"], temperature=wl["temperature"])
-            r2 = run_generation(tgt, drf if mode != "vanilla" else None, make_prompt(1), c2)
-            base[mode] = {"decode_tps": round(decode_stats(r2) / (first_decode_ms(r2) / 1e3), 1),
-                          "tps_reference_style": round(r2.tps, 1),
-                          "ttft_ms": round(r2.device_ttft_ms, 2), "budget": bud}
+            rs = [run_generation(tgt, drf if mode != "vanilla" else None,
+                                 make_prompt(1000 * rank + args.warmup + i + 1), c2)
+                  for i in range(n_base)]
+            base[mode] = {
+                "decode_tps": round(statistics.median(
+                    decode_stats(r2) / (first_decode_ms(r2) / 1e3) for r2 in rs), 1),
+                "tps_reference_style": round(statistics.median(r2.tps for r2 in rs), 1),
+                "ttft_ms": round(statistics.median(r2.device_ttft_ms for r2 in rs), 2),
+                "budget": bud, "runs": n_base}
         extra["gpu_baselines"] = base
         if ws == 1 and not args.no_cpu_baseline and args.workload == "config2":
             thr = os.cpu_count()

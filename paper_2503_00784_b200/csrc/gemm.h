@@ -93,6 +93,8 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
 // 256 weight rows on N; map_x128 has 128-row boxes.  n_out % 256 == 0.
 GemmPlan plan_gemm_wide(int n_out, int k);
 size_t gemm_wide_ws_floats(const GemmPlan& p);
+// debug seam: per-CTA stamps of every following wide launch at buf + launch * 8 * 148
+void gemm_wide_set_trace(unsigned long long* buf);
 cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
                              int w, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                              cudaStream_t stream);

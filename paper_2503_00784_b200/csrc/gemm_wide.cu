@@ -48,9 +48,10 @@ struct WideCfg {
 
 __device__ __forceinline__ void wide_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// 16 consecutive weight-row columns [c0, c0 + 16) of this thread's token
-// (partials are [segment][row][token])
-__device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* part_base, int nseg,
+// 16 consecutive weight-row columns [c0, c0 + 16) of this thread's token, from
+// TMEM or summed (segment order) from the stream-K partials, which are stored
+// [segment][col / 4][token][4]: one float4 per thread per 4 columns, coalesced.
+__device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* part_tok, int nseg,
                                           size_t seg_stride, bool from_tmem, float* v) {
     if (from_tmem) {
         tmem_ld16(t_lane + c0, v);
@@ -59,18 +60,45 @@ __device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* 
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = 0.0f;
     for (int s0 = 0; s0 < nseg; s0 += 4) {
-        float pv[4][16];
+        float4 pv[4][4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                pv[k][j] = s0 + k < nseg ? __ldcg(part_base + (s0 + k) * seg_stride + (c0 + j) * kWideM) : 0.0f;
+            for (int q4 = 0; q4 < 4; ++q4)
+                pv[k][q4] = s0 + k < nseg
+                                ? __ldcg(reinterpret_cast<const float4*>(part_tok + (s0 + k) * seg_stride +
+                                                                         static_cast<size_t>((c0 >> 2) + q4) * kWideM * 4))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (s0 + k < nseg)
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], pv[k][j]);
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    v[4 * q4] = __fadd_rn(v[4 * q4], pv[k][q4].x);
+                    v[4 * q4 + 1] = __fadd_rn(v[4 * q4 + 1], pv[k][q4].y);
+                    v[4 * q4 + 2] = __fadd_rn(v[4 * q4 + 2], pv[k][q4].z);
+                    v[4 * q4 + 3] = __fadd_rn(v[4 * q4 + 3], pv[k][q4].w);
+                }
     }
+}
+
+__device__ __forceinline__ uint32_t bf2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+// 16 bf16 (32 bytes, 16-byte aligned) from fp32
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v) {
+    uint4 a, b;
+    a.x = bf2(v[0], v[1]);
+    a.y = bf2(v[2], v[3]);
+    a.z = bf2(v[4], v[5]);
+    a.w = bf2(v[6], v[7]);
+    b.x = bf2(v[8], v[9]);
+    b.y = bf2(v[10], v[11]);
+    b.z = bf2(v[12], v[13]);
+    b.w = bf2(v[14], v[15]);
+    reinterpret_cast<uint4*>(dst)[0] = a;
+    reinterpret_cast<uint4*>(dst)[1] = b;
 }
 
 }  // namespace
@@ -101,8 +129,17 @@ __global__ void __launch_bounds__(kWideThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     __shared__ int s_last;
+    unsigned long long* tr = a.trace ? a.trace + 8 * static_cast<size_t>(blockIdx.x) : nullptr;
+    auto stamp = [&](int i) {
+        if (tr) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tr[i] = t;
+        }
+    };
 
     if (threadIdx.x == 0) {
+        stamp(0);
         tma_prefetch_desc(&map_x);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -145,6 +182,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                     bulk_load(st + hh * kABytes, wsrc(g0 + i, hh), kABytes, &full[i], pol_w);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
+            stamp(2);
             int s = 0;
             uint32_t ph = 0;
             int kb = static_cast<int>(g0 % nkb);
@@ -195,6 +233,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                 }
                 umma_commit(&tfull[b]);
             }
+            stamp(3);
         }
     } else {
         // ---------------- epilogue warps 2..5: thread = token ----------------
@@ -231,6 +270,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
             sk_segments(tile, a.nkb, T, P, c, &nseg, &seg);
             const int b = u & 1;
             mbar_wait(&tfull[b], static_cast<uint32_t>((u >> 1) & 1));
+            if (tid == 0 && tile == tile_hi) stamp(6);
             __syncwarp();
             tc_fence_after();
             const uint32_t t_lane = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * kWideN);
@@ -239,12 +279,14 @@ __global__ void __launch_bounds__(kWideThreads, 1)
             bool from_tmem = true;
             if (nseg > 1) {
                 // this segment's partial: [row][token], coalesced over threads
-                float* mine = tile_part + seg * seg_stride + tok;
+                float* mine = tile_part + seg * seg_stride + static_cast<size_t>(tok) * 4;
                 for (int c0 = 0; c0 < kWideN; c0 += 16) {
                     float v[16];
                     tmem_ld16(t_lane + c0, v);
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) mine[(c0 + j) * kWideM] = v[j];
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        *reinterpret_cast<float4*>(mine + static_cast<size_t>((c0 >> 2) + q4) * kWideM * 4) =
+                            make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
                 }
                 tc_fence_before();
                 mbar_arrive(&tempty[b]);
@@ -256,7 +298,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                 __threadfence();
                 from_tmem = false;
             }
-            const float* pbase = tile_part + tok;
+            const float* pbase = tile_part + static_cast<size_t>(tok) * 4;
             const int m0 = tile * kWideN;
             if (e.kind == kEpiStore || e.kind == kEpiResidual) {
                 for (int h = 0; h < kHalves; ++h) {  // 128-row halves (ss tiles)
@@ -283,12 +325,13 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                         for (int j = 0; j < 16; j += 4)
                             *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                         if (e.kind == kEpiResidual && e.u_out != nullptr) {
-                            __nv_bfloat16* uo = e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
+                            float uv[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
-                                uo[j] = __float2bfloat16_rn(__fmul_rn(v[j], e.gain[m0 + c0 + j]));
+                                uv[j] = __fmul_rn(v[j], e.gain[m0 + c0 + j]);
                                 ss = __fmaf_rn(v[j], v[j], ss);
                             }
+                            store_bf16x16(e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0, uv);
                         }
                     }
                     if (e.kind == kEpiResidual && e.u_out != nullptr && valid)
@@ -302,13 +345,16 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                         load_cols(t_lane, h * 128 + 16 * k, pbase, nseg, seg_stride, from_tmem, g);
                         load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nseg, seg_stride, from_tmem, up);
                         if (!valid) continue;
-                        __nv_bfloat16* dst = e.out_bf + static_cast<size_t>(tok) * ffn + (kHalves * tile + h) * 64 + 16 * k;
+                        float av[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const float gv = __fmul_rn(g[j], rn), uv = __fmul_rn(up[j], rn);
-                            const float silu = __fdiv_rn(gv, __fadd_rn(1.0f, expf(-gv)));
-                            dst[j] = __float2bfloat16_rn(__fmul_rn(silu, uv));
+                            // fast exp / divide: prefill-only activations (the decode
+                            // epilogue keeps the IEEE forms the oracle mirrors)
+                            const float silu = __fdividef(gv, 1.0f + __expf(-gv));
+                            av[j] = __fmul_rn(silu, uv);
                         }
+                        store_bf16x16(e.out_bf + static_cast<size_t>(tok) * ffn + (kHalves * tile + h) * 64 + 16 * k, av);
                     }
             } else {  // kEpiQkvRope
                 const ModelDims& md = e.m;
@@ -325,26 +371,30 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                                 load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nseg, seg_stride, from_tmem, hi_v);
                                 if (!valid) continue;
                                 const int grow = r0 + hb;  // first row of the head
-                                float* qd = grow < q_dim ? e.q_out + static_cast<size_t>(tok) * q_dim + grow : nullptr;
-                                __nv_bfloat16* kd =
-                                    grow < q_dim ? nullptr
-                                                 : e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 0,
-                                                                         (grow - q_dim) / hd, slot);
+                                float lo16[16], hi16[16];
 #pragma unroll
                                 for (int j = 0; j < 16; ++j) {
                                     const int i = i0 + j;
                                     const float av = __fmul_rn(lo_v[j], rn), bv = __fmul_rn(hi_v[j], rn);
                                     const float cs = e.rope_cos[static_cast<size_t>(pos) * half + i];
                                     const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
-                                    const float lo = __fmaf_rn(av, cs, -__fmul_rn(bv, sn));
-                                    const float hi = __fmaf_rn(bv, cs, __fmul_rn(av, sn));
-                                    if (qd) {
-                                        qd[i] = lo;
-                                        qd[i + half] = hi;
-                                    } else {
-                                        kd[i] = __float2bfloat16_rn(lo);
-                                        kd[i + half] = __float2bfloat16_rn(hi);
+                                    lo16[j] = __fmaf_rn(av, cs, -__fmul_rn(bv, sn));
+                                    hi16[j] = __fmaf_rn(bv, cs, __fmul_rn(av, sn));
+                                }
+                                if (grow < q_dim) {
+                                    float* qd = e.q_out + static_cast<size_t>(tok) * q_dim + grow + i0;
+#pragma unroll
+                                    for (int q4 = 0; q4 < 4; ++q4) {
+                                        reinterpret_cast<float4*>(qd)[q4] =
+                                            make_float4(lo16[4 * q4], lo16[4 * q4 + 1], lo16[4 * q4 + 2], lo16[4 * q4 + 3]);
+                                        reinterpret_cast<float4*>(qd + half)[q4] =
+                                            make_float4(hi16[4 * q4], hi16[4 * q4 + 1], hi16[4 * q4 + 2], hi16[4 * q4 + 3]);
                                     }
+                                } else {
+                                    __nv_bfloat16* kd = e.kv_pool +
+                                        kv_offset(md, e.page_size, page, e.layer, 0, (grow - q_dim) / hd, slot) + i0;
+                                    store_bf16x16(kd, lo16);
+                                    store_bf16x16(kd + half, hi16);
                                 }
                             }
                     } else {
@@ -352,12 +402,11 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                             float v[16];
                             load_cols(t_lane, h * 128 + c0, pbase, nseg, seg_stride, from_tmem, v);
                             if (!valid) continue;
+                            float vv[16];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const int ve = r0 + c0 + j - q_dim - kv_dim;
-                                e.kv_pool[kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd] =
-                                    __float2bfloat16_rn(__fmul_rn(v[j], rn));
-                            }
+                            for (int j = 0; j < 16; ++j) vv[j] = __fmul_rn(v[j], rn);
+                            const int ve = r0 + c0 - q_dim - kv_dim;  // 16 dims of one kv head
+                            store_bf16x16(e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd, vv);
                         }
                     }
                 }
@@ -371,9 +420,11 @@ __global__ void __launch_bounds__(kWideThreads, 1)
             }
         }
     }
+    if (threadIdx.x == 64) stamp(4);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<2 * NW>(tmem);
+    if (threadIdx.x == 0) stamp(5);
 #endif
 }
 
@@ -388,7 +439,9 @@ GemmPlan plan_gemm_wide(int n_out, int k) {
     p.stages = nw == 256 ? 4 : 6;
     p.smem_bytes = static_cast<int>(p.stages * stage + 1024 + 64 * 8);
     p.tmem_cols = 2 * nw;
-    p.ctas = static_cast<int>(std::min<long>(kNumSMs, T));
+    // the 4096-output GEMMs have only 32 row tiles: fewer CTAs keep their
+    // stream-K segments per tile (and the last arriver's reduction) short
+    p.ctas = static_cast<int>(std::min<long>(p.tiles >= 64 ? kNumSMs : 64, T));
     int ms = 1;
     for (int t = 0; t < p.tiles; ++t) {
         const int f = gemm_dev::sk_owner(static_cast<long>(t) * p.nkb, T, p.ctas);
@@ -402,6 +455,13 @@ GemmPlan plan_gemm_wide(int n_out, int k) {
 
 size_t gemm_wide_ws_floats(const GemmPlan& p) {
     return static_cast<size_t>(p.tiles) * p.max_seg * (p.tmem_cols / 2) * kWideM;
+}
+
+static unsigned long long* g_wide_trace = nullptr;
+static size_t g_wide_trace_launch = 0;
+void gemm_wide_set_trace(unsigned long long* buf) {
+    g_wide_trace = buf;
+    g_wide_trace_launch = 0;
 }
 
 cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
@@ -425,6 +485,7 @@ cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* ma
     a.tmem_buf = plan.tmem_cols / 2;
     a.ws = ws;
     a.epi = epi;
+    a.trace = g_wide_trace ? g_wide_trace + (g_wide_trace_launch++) * 8 * kNumSMs : nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.ctas, 1, 1);
     cfg.blockDim = dim3(kWideThreads, 1, 1);

@@ -90,8 +90,9 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
-    // prefill widths (17..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu)
-    const bool wide = w > 16 && w <= 128 && ctx->ws_wide != nullptr;
+    // prefill widths (49..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu);
+    // narrower passes are faster on the skinny stream-K GEMM (measured crossover)
+    const bool wide = w > 48 && w <= 128 && ctx->ws_wide != nullptr;
     auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
                     const GemmEpiParams& ep) -> cudaError_t {
         int n_out, k;
@@ -1175,6 +1176,34 @@ int dd_debug_gemm_trace(dd_ctx* ctx, int which, int w, uint64_t* trace, int max_
 }
 
 void* dd_debug_pass_progress(void) { return pass_debug_enable(1); }
+
+// one prefill-width pass (17..128 tokens, per-launch path) with per-CTA stamps of
+// its wide GEMM launches: trace[launch][cta][8]
+int dd_debug_prefill_trace(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_launch) {
+    if (!ctx || !trace || !n_launch || w <= 48 || w > 128) return ctx_fail(ctx, DD_E_ARG, "bad args");
+    CK(cudaSetDevice(ctx->device));
+    const size_t need = static_cast<size_t>(4 * ctx->m.n_layers + 1) * 8 * kNumSMs;
+    if (need > max_entries) return ctx_fail(ctx, DD_E_CAPACITY, "trace buffer too small");
+    unsigned long long* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(unsigned long long) * need));
+    CK(cudaMemset(d, 0, sizeof(unsigned long long) * need));
+    int rc = upload_dummy_pass(ctx, w);
+    if (rc) return rc;
+    rc = enqueue_pass_impl(ctx, w, true, [](int) {});  // warm-up
+    if (rc) return rc;
+    rc = upload_dummy_pass(ctx, w);
+    if (rc) return rc;
+    gemm_wide_set_trace(d);
+    rc = enqueue_pass_impl(ctx, w, true, [](int) {});
+    gemm_wide_set_trace(nullptr);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * need, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    *n_launch = 4 * ctx->m.n_layers + 1;
+    ctx->last_w = 0;
+    return DD_OK;
+}
 
 // one pass of width w (logits on) with per-CTA, per-phase globaltimer stamps:
 // trace[cta][phase][8] = weight producer start, inputs ready, MMA done,
