@@ -147,14 +147,20 @@ int dd_verify_probs(dd_ctx* ctx, const double* p_rows, const int32_t* tail_token
 /* Median device time (CUDA events) of a scored pass of width w. */
 int dd_time_pass(dd_ctx* ctx, int w, int trials, float* median_ms);
 
-/* Per-kernel device time breakdown of one pass of width w (ms, by class:
- * 0 gemm, 1 attention, 2 epilogues/norms, 3 total). */
+/* Per-kernel device time breakdown of one pass of width w on the per-launch
+ * path (ms, by class: 0 gemm, 1 attention, 2 epilogues/norms, 3 total). */
 int dd_profile_pass(dd_ctx* ctx, int w, float* ms4);
 
-/* Device time of the GEMM launches of one pass of width w (the 4 per layer
- * plus the LM head, back to back, fused epilogues included), median of
- * `trials`; the weight-streaming roofline of the dominant kernel. */
+/* Device time of the per-launch path's GEMM launches of one pass of width w
+ * (4 per layer plus the LM head, back to back, fused epilogues included),
+ * median of `trials`. */
 int dd_time_gemms(dd_ctx* ctx, int w, int trials, float* median_ms, int* launches);
+
+/* Weighted stream-K partition of the persistent pass kernel: times every SM's
+ * weight streaming over a few decode passes and gives each SM a share
+ * proportional to its speed (opt-in: DD_PASS_BALANCE=1 runs it from
+ * dd_weights_init). Must precede the first scored pass. */
+int dd_pass_balance(dd_ctx* ctx);
 
 /* Algorithmic weight bytes streamed by one pass (excludes the gathered
  * embedding), for the roofline. */
@@ -179,6 +185,21 @@ int dd_debug_gemm_trace(dd_ctx* ctx, int which, int w, uint64_t* trace, int max_
  * 8 * ctas_per_launch u64 per launch). */
 int dd_debug_pass_trace(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_launch,
                         int* ctas_per_launch);
+
+/* Debug: one decode pass (w <= 16) of the persistent pass kernel with per-CTA,
+ * per-phase globaltimer stamps, trace[cta][phase][12] (weight producer start,
+ * inputs ready, MMA done, epilogue done, ..., last flag published, ...,
+ * smid in slot 10 of phase 0), followed when max_entries allows by per-tile
+ * publish times; n_phases = embed + 5 per layer + head. */
+int dd_debug_pass_timeline(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_phases);
+
+/* Debug: one prefill pass (49..128 tokens) with per-CTA stamps of its
+ * tokens-on-M GEMM launches, trace[launch][148][8]. */
+int dd_debug_prefill_trace(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entries, int* n_launch);
+
+/* Debug: mapped host int[148][8] of per-CTA progress words of the pass kernel
+ * (hang diagnosis; pointer stays valid for the process). */
+void* dd_debug_pass_progress(void);
 
 /* ------------------------------------------------------------ CPU draft */
 int dd_draft_create(const dd_model_desc* desc, uint64_t weight_seed, const dd_plant_desc* plant,

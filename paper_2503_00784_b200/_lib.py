@@ -93,6 +93,12 @@ SIGNATURES = {
     "dd_test_gemm": (C.c_int, [_u16p, _u16p, C.c_int, C.c_int, C.c_int, _f32p]),
     "dd_debug_pass_trace": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
                                       C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "dd_pass_balance": (C.c_int, [_vp]),
+    "dd_debug_pass_timeline": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
+                                         C.POINTER(C.c_int)]),
+    "dd_debug_prefill_trace": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_size_t,
+                                         C.POINTER(C.c_int)]),
+    "dd_debug_pass_progress": (C.c_void_p, []),
     "dd_debug_gemm_trace": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_uint64), C.c_int,
                                       C.POINTER(C.c_int)]),
     "dd_draft_create": (C.c_int, [C.POINTER(ModelDesc), C.c_uint64, C.POINTER(PlantDesc), C.c_int,
