@@ -314,6 +314,20 @@ struct Runner {
         std::thread worker;
         const bool threaded = cfg.threaded != 0;
         if (threaded) {
+            // The worker must start on its own core: a thread inherits its creator's
+            // affinity, and the creator (the target-role thread, typically pinned to
+            // one core) spins in wait_reply, so a worker born on that core would only
+            // run after a scheduler tick (~ms of lost draft time in iteration 1, i.e.
+            // TTFT).  Create it with the draft core's affinity instead.
+            cpu_set_t saved;
+            const bool pin = !draft->cpus.empty() &&
+                             pthread_getaffinity_np(pthread_self(), sizeof(saved), &saved) == 0;
+            if (pin) {
+                cpu_set_t set;
+                CPU_ZERO(&set);
+                CPU_SET(draft->cpus[0], &set);
+                pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+            }
             worker = std::thread([&] {
                 if (!draft->cpus.empty()) {  // the worker is pool thread 0
                     cpu_set_t set;
@@ -329,6 +343,7 @@ struct Runner {
                     ch.failed.store(true, std::memory_order_release);
                 }
             });
+            if (pin) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
         }
         try {
             while (verified.size() - prompt_len < static_cast<size_t>(cfg.max_new_tokens)) {

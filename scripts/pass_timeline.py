@@ -68,3 +68,6 @@ order = np.argsort(m)
 print("slowest CTAs:", order[-12:], "fastest:", order[:12])
 sm = np.round(m, 1)
 print("even/odd CTA mean:", sm[::2].mean(), sm[1::2].mean(), " first/second half:", sm[:74].mean(), sm[74:].mean())
+for k, nm in ((0, "qkv"), (2, "o"), (3, "gu"), (4, "dn")):
+    sp = [np.nanmax(a[:, 1 + 5 * l + k, 2]) - np.nanmin(a[:, 1 + 5 * l + k, 1]) for l in range(1, 31)]
+    print(f"  {nm} inputs(min)->mma_done(max) {np.mean(sp):.1f} us")
