@@ -1,4 +1,2 @@
-timeout -s KILL 300 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout -s KILL 120 python scripts/pass_ab.py 32,64,127 128
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; python -c "
-import json; d=json.load(open('gpurun_out/bench.json')); print(d['value'], d['ttft_p50_ms'], d['gpu_baselines'], d['roofline']['frac'], d['config']['budget'])"
+ncu --set full --clock-control none --import-source on -k regex:gemm_wide -s 130 -c 1 -o gpurun_out/wide_gu2 python scripts/one_pass.py 127 128 > gpurun_out/wide.log 2>&1
+tail -1 gpurun_out/wide.log

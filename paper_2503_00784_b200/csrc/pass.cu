@@ -961,24 +961,31 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                         fast_tile_epilogue(a, s_fe, s_part, tile, v, xv, gcol, red, tid);
                         publish = true;
                     } else {
-                        float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * W * 128;
+                        // Segment 0 (the tile's first k-blocks) sits at the END of its
+                        // CTA's range, so it finishes last: it is the designated reducer.
+                        // The others store their partial and bump the tile counter with a
+                        // fire-and-forget release; the reducer waits for them (normally
+                        // already done), adds them in segment order to its own registers.
+                        if (seg != 0) {
+                            float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * W * 128;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (j < W) part[static_cast<size_t>(j) * 128 + row] = v[j];
-                        epi_bar();
-                        if (tid == 0) {  // release this segment's partial, acquire the others'
-                            const int prev = atom_add_acq_rel(&a.epi.counters[tile], 1);
-                            s_last = (prev == nseg - 1);
-                        }
-                        epi_bar();
-                        if (s_last) {
-                            // this thread's row over every segment: all loads in flight, summed
-                            // in segment order
+                            for (int j = 0; j < 16; ++j)
+                                if (j < W) part[static_cast<size_t>(j) * 128 + row] = v[j];
+                            epi_bar();  // every partial store happens-before the release
+                            if (tid == 0)
+                                asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
+                                             ::"l"(&a.epi.counters[tile]) : "memory");
+                        } else {
+                            if (tid == 0) {
+                                while (ld_acquire(&a.epi.counters[tile]) < nseg - 1) __nanosleep(32);
+                                a.epi.counters[tile] = 0;
+                            }
+                            epi_bar();
                             const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * W * 128 + row;
                             float acc[16];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) acc[j] = 0.0f;
-                            for (int s0 = 0; s0 < nseg; s0 += 4) {
+                            for (int j = 0; j < 16; ++j) acc[j] = v[j];
+                            for (int s0 = 1; s0 < nseg; s0 += 4) {
                                 float pv[4][16];
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
@@ -994,7 +1001,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                         for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], pv[k][j]);
                             }
                             fast_tile_epilogue(a, s_fe, s_part, tile, acc, xv, gcol, red, tid);
-                            if (tid == 0) a.epi.counters[tile] = 0;
                             publish = true;
                         }
                     }
