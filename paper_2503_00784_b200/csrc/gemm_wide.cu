@@ -48,38 +48,56 @@ struct WideCfg {
 
 __device__ __forceinline__ void wide_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// 16 consecutive weight-row columns [c0, c0 + 16) of this thread's token, from
-// TMEM or summed (segment order) from the stream-K partials, which are stored
-// [segment][col / 4][token][4]: one float4 per thread per 4 columns, coalesced.
-__device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* part_tok, int nseg,
-                                          size_t seg_stride, bool from_tmem, float* v) {
-    if (from_tmem) {
-        tmem_ld16(t_lane + c0, v);
-        return;
-    }
+// 16 consecutive weight-row columns [c0, c0 + 16) of this thread's token.
+template <int NCH, int KS>
+__device__ __forceinline__ void load_cols_n(uint32_t t_lane, int c0, const float* part_tok, int nseg,
+                                            size_t seg_stride, float (*v)[16]) {
+    // NCH consecutive 16-column chunks: this CTA's own segment (segment 0, the
+    // designated reducer) from TMEM plus the other segments' partials
+    // ([segment][col / 4][token][4]) in segment order.  Every partial load is
+    // issued before the TMEM loads (whose wait is a compiler barrier), so one
+    // round trip covers all NCH chunks of up to KS segments.
+    for (int s0 = 1; s0 < nseg || s0 == 1; s0 += KS) {
+        float4 pv[KS][NCH][4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-    for (int s0 = 0; s0 < nseg; s0 += 4) {
-        float4 pv[4][4];
+        for (int k = 0; k < KS; ++k)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+            for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-                pv[k][q4] = s0 + k < nseg
-                                ? __ldcg(reinterpret_cast<const float4*>(part_tok + (s0 + k) * seg_stride +
-                                                                         static_cast<size_t>((c0 >> 2) + q4) * kWideM * 4))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q4 = 0; q4 < 4; ++q4)
+                    pv[k][ch][q4] = s0 + k < nseg
+                                        ? __ldcg(reinterpret_cast<const float4*>(
+                                              part_tok + (s0 + k) * seg_stride +
+                                              static_cast<size_t>(((c0 + 16 * ch) >> 2) + q4) * kWideM * 4))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (s0 == 1) {
+            uint32_t r[NCH][16];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+            for (int ch = 0; ch < NCH; ++ch) tmem_ld16_async(t_lane + c0 + 16 * ch, r[ch]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[ch][j] = __uint_as_float(r[ch][j]);
+        }
+#pragma unroll
+        for (int k = 0; k < KS; ++k)
             if (s0 + k < nseg)
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    v[4 * q4] = __fadd_rn(v[4 * q4], pv[k][q4].x);
-                    v[4 * q4 + 1] = __fadd_rn(v[4 * q4 + 1], pv[k][q4].y);
-                    v[4 * q4 + 2] = __fadd_rn(v[4 * q4 + 2], pv[k][q4].z);
-                    v[4 * q4 + 3] = __fadd_rn(v[4 * q4 + 3], pv[k][q4].w);
-                }
+                for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        v[ch][4 * q4] = __fadd_rn(v[ch][4 * q4], pv[k][ch][q4].x);
+                        v[ch][4 * q4 + 1] = __fadd_rn(v[ch][4 * q4 + 1], pv[k][ch][q4].y);
+                        v[ch][4 * q4 + 2] = __fadd_rn(v[ch][4 * q4 + 2], pv[k][ch][q4].z);
+                        v[ch][4 * q4 + 3] = __fadd_rn(v[ch][4 * q4 + 3], pv[k][ch][q4].w);
+                    }
+        if (nseg <= 1) break;
     }
+}
+__device__ __forceinline__ void load_cols(uint32_t t_lane, int c0, const float* part_tok, int nseg,
+                                          size_t seg_stride, float* v) {
+    load_cols_n<1, 4>(t_lane, c0, part_tok, nseg, seg_stride, reinterpret_cast<float(*)[16]>(v));
 }
 
 __device__ __forceinline__ uint32_t bf2(float lo, float hi) {
@@ -276,62 +294,91 @@ __global__ void __launch_bounds__(kWideThreads, 1)
             const uint32_t t_lane = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * kWideN);
             const size_t seg_stride = static_cast<size_t>(kWideN) * kWideM;
             float* tile_part = a.ws + static_cast<size_t>(tile) * a.max_seg * seg_stride;
-            bool from_tmem = true;
+            int nsum = 1;  // segments summed into this tile (>1: this CTA is the reducer)
             if (nseg > 1) {
-                // this segment's partial: [row][token], coalesced over threads
-                float* mine = tile_part + seg * seg_stride + static_cast<size_t>(tok) * 4;
-                for (int c0 = 0; c0 < kWideN; c0 += 16) {
-                    float v[16];
-                    tmem_ld16(t_lane + c0, v);
+                if (seg != 0) {
+                    // not the designated reducer: store this segment's partial
+                    // ([segment][col / 4][token][4], coalesced) and release-add the counter
+                    float* mine = tile_part + seg * seg_stride + static_cast<size_t>(tok) * 4;
+                    for (int c0 = 0; c0 < kWideN; c0 += 64) {  // 4 TMEM loads in flight
+                        uint32_t r[4][16];
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4)
-                        *reinterpret_cast<float4*>(mine + static_cast<size_t>((c0 >> 2) + q4) * kWideM * 4) =
-                            make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+                        for (int k = 0; k < 4; ++k) tmem_ld16_async(t_lane + c0 + 16 * k, r[k]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4)
+                                *reinterpret_cast<float4*>(mine + static_cast<size_t>(((c0 + 16 * k) >> 2) + q4) * kWideM * 4) =
+                                    make_float4(__uint_as_float(r[k][4 * q4]), __uint_as_float(r[k][4 * q4 + 1]),
+                                                __uint_as_float(r[k][4 * q4 + 2]), __uint_as_float(r[k][4 * q4 + 3]));
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&tempty[b]);
+                    wide_bar();  // every partial store happens-before the release
+                    if (tid == 0)
+                        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(&e.counters[tile]) : "memory");
+                    continue;
                 }
-                tc_fence_before();
-                mbar_arrive(&tempty[b]);
-                __threadfence();
+                // segment 0 finishes last (end of its CTA's range): wait for the others
+                if (tid == 0) {
+                    int v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(&e.counters[tile]) : "memory");
+                    } while (v < nseg - 1);
+                    e.counters[tile] = 0;
+                }
                 wide_bar();
-                if (tid == 0) s_last = atomicAdd(&e.counters[tile], 1) == nseg - 1;
-                wide_bar();
-                if (!s_last) continue;
-                __threadfence();
-                from_tmem = false;
+                nsum = nseg;
             }
             const float* pbase = tile_part + static_cast<size_t>(tok) * 4;
             const int m0 = tile * kWideN;
             if (e.kind == kEpiStore || e.kind == kEpiResidual) {
                 for (int h = 0; h < kHalves; ++h) {  // 128-row halves (ss tiles)
                     float ss = 0.0f;
-                    for (int c0 = h * 128; c0 < h * 128 + 128; c0 += 16) {
-                        float v[16];
-                        load_cols(t_lane, c0, pbase, nseg, seg_stride, from_tmem, v);
-                        if (e.ss_in != nullptr)
+                    for (int c1 = h * 128; c1 < h * 128 + 128; c1 += 32) {
+                        // residual rows requested first, then 2 chunks of partial sums
+                        // and accumulators in one round trip
+                        float4 xr[2][4];
+                        if (e.kind == kEpiResidual && valid)
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rn);
+                            for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4)
+                                    xr[ch][q4] = __ldcg(reinterpret_cast<const float4*>(
+                                                            e.out + static_cast<size_t>(tok) * a.n_out + m0 + c1 + 16 * ch) + q4);
+                        float v2[2][16];
+                        load_cols_n<2, 2>(t_lane, c1, pbase, nsum, seg_stride, v2);
                         if (!valid) continue;
-                        float* dst = e.out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
-                        if (e.kind == kEpiResidual) {
 #pragma unroll
-                            for (int j = 0; j < 16; j += 4) {
-                                const float4 x = __ldcg(reinterpret_cast<const float4*>(dst + j));
-                                v[j] = __fadd_rn(x.x, v[j]);
-                                v[j + 1] = __fadd_rn(x.y, v[j + 1]);
-                                v[j + 2] = __fadd_rn(x.z, v[j + 2]);
-                                v[j + 3] = __fadd_rn(x.w, v[j + 3]);
+                        for (int ch = 0; ch < 2; ++ch) {
+                            const int c0 = c1 + 16 * ch;
+                            float* v = v2[ch];
+                            if (e.ss_in != nullptr)
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rn);
+                            float* dst = e.out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
+                            if (e.kind == kEpiResidual) {
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4) {
+                                    v[4 * q4] = __fadd_rn(xr[ch][q4].x, v[4 * q4]);
+                                    v[4 * q4 + 1] = __fadd_rn(xr[ch][q4].y, v[4 * q4 + 1]);
+                                    v[4 * q4 + 2] = __fadd_rn(xr[ch][q4].z, v[4 * q4 + 2]);
+                                    v[4 * q4 + 3] = __fadd_rn(xr[ch][q4].w, v[4 * q4 + 3]);
+                                }
                             }
-                        }
 #pragma unroll
-                        for (int j = 0; j < 16; j += 4)
-                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                        if (e.kind == kEpiResidual && e.u_out != nullptr) {
-                            float uv[16];
+                            for (int j = 0; j < 16; j += 4)
+                                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            if (e.kind == kEpiResidual && e.u_out != nullptr) {
+                                float uv[16];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                uv[j] = __fmul_rn(v[j], e.gain[m0 + c0 + j]);
-                                ss = __fmaf_rn(v[j], v[j], ss);
+                                for (int j = 0; j < 16; ++j) {
+                                    uv[j] = __fmul_rn(v[j], e.gain[m0 + c0 + j]);
+                                    ss = __fmaf_rn(v[j], v[j], ss);
+                                }
+                                store_bf16x16(e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0, uv);
                             }
-                            store_bf16x16(e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0, uv);
                         }
                     }
                     if (e.kind == kEpiResidual && e.u_out != nullptr && valid)
@@ -342,8 +389,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                 for (int h = 0; h < kHalves; ++h)
                     for (int k = 0; k < 4; ++k) {
                         float g[16], up[16];
-                        load_cols(t_lane, h * 128 + 16 * k, pbase, nseg, seg_stride, from_tmem, g);
-                        load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nseg, seg_stride, from_tmem, up);
+                        load_cols(t_lane, h * 128 + 16 * k, pbase, nsum, seg_stride, g);
+                        load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nsum, seg_stride, up);
                         if (!valid) continue;
                         float av[16];
 #pragma unroll
@@ -367,8 +414,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                         for (int hb = 0; hb < 128; hb += hd)
                             for (int i0 = 0; i0 < half; i0 += 16) {
                                 float lo_v[16], hi_v[16];
-                                load_cols(t_lane, h * 128 + hb + i0, pbase, nseg, seg_stride, from_tmem, lo_v);
-                                load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nseg, seg_stride, from_tmem, hi_v);
+                                load_cols(t_lane, h * 128 + hb + i0, pbase, nsum, seg_stride, lo_v);
+                                load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nsum, seg_stride, hi_v);
                                 if (!valid) continue;
                                 const int grow = r0 + hb;  // first row of the head
                                 float lo16[16], hi16[16];
@@ -400,7 +447,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                     } else {
                         for (int c0 = 0; c0 < 128; c0 += 16) {
                             float v[16];
-                            load_cols(t_lane, h * 128 + c0, pbase, nseg, seg_stride, from_tmem, v);
+                            load_cols(t_lane, h * 128 + c0, pbase, nsum, seg_stride, v);
                             if (!valid) continue;
                             float vv[16];
 #pragma unroll
@@ -411,13 +458,8 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                     }
                 }
             }
-            if (from_tmem) {
-                tc_fence_before();
-                mbar_arrive(&tempty[b]);
-            } else {
-                wide_bar();
-                if (tid == 0) e.counters[tile] = 0;
-            }
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);
         }
     }
     if (threadIdx.x == 64) stamp(4);
