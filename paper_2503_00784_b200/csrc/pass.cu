@@ -438,11 +438,6 @@ __device__ void embed_tile(const PassParams& P, int tile, int W, float* part /* 
     }
 }
 
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Wait until every producer flag feeding this CTA's k-blocks of a GEMM phase
 // is published.  Run by the whole activation-producer warp: the distinct
@@ -675,10 +670,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     __shared__ GemmArgs s_args;
     __shared__ FastEpi s_fe;
     __shared__ unsigned long long s_issue[16];  // debug: weight-load issue time per stage
-    __shared__ volatile int s_xready;           // last phase whose activations are ready
 
     if (threadIdx.x == 0) {
-        s_xready = -1;
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);  // weight producer + activation producer
             mbar_init(&empty[s], 1);
@@ -755,10 +748,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 const __nv_bfloat16* src = ph.w + static_cast<size_t>(g0) * 8192;
                 pass_stamp(P, p, 0);
                 for (int g = g0; g < g1; ++g, src += 8192) {
-                    // boundary throttle (experiment): only P.early stages of a phase
-                    // are fetched before its activations are ready
-                    if (P.early >= 0 && g - g0 >= P.early)
-                        while (s_xready < p) __nanosleep(64);
                     if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
                     if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
                     mbar_arrive_expect_tx(&full[rp.s], kABytes);
@@ -786,7 +775,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             if (lane == 0) pass_stamp(P, p, 7);
             wait_phase_inputs(P, ph.x_src, ph.x_flag, nkb, g0, g1, epoch, qtiles, lane);
             if (lane == 0) {
-                s_xready = p;
                 pass_stamp(P, p, 1);
                 const CUtensorMap* mx = ph.x_map == 0 ? &map_h : ph.x_map == 1 ? &map_o : &map_a;
                 int kb = g0 % nkb;
@@ -1079,11 +1067,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     if (tid == 0) {
                         st_release_flag(P.flags, ph.out_flag, tile, epoch);
                         pass_stamp(P, p, 6);
-                        if (P.trace2) P.trace2[p * 512 + tile] = gtimer();
-                        if (P.poll_mode == 6) {  // debug: when does the store reach L2?
-                            while (ld_relaxed(flag_at(P.flags, ph.out_flag, tile, 0)) != epoch) {}
-                            pass_stamp(P, p, 8);
-                        }
                     }
                 }
             }

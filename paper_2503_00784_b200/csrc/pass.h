@@ -40,11 +40,9 @@ struct PassParams {
     int nt;
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
-    int poll_mode;  // debug: flag polling variant
-    int early;      // stages a phase may fetch before its activations are ready (-1: no limit)
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
-    unsigned long long* trace;
-    unsigned long long* trace2;  // debug: per-tile publish times / poll batch times  // debug: [CTA][phase][4] globaltimer stamps, or nullptr
+    unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
+
     const PassState* ps;
     int* flags;
     // embedding

@@ -327,8 +327,7 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
     return DD_OK;
 }
 
-int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long* trace = nullptr,
-                        unsigned long long* trace2 = nullptr) {
+int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long* trace = nullptr) {
     const PassPhase* phases = nullptr;
     int n = 0;
     int rc = build_pass_phases(ctx, w, want_logits, &phases, &n);
@@ -341,10 +340,6 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.tmem_buf = tmem_buf_for(p.nt);
     static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 16;
     p.prefetch = env_pf;
-    static const int env_pm = getenv("DD_PASS_POLL") ? atoi(getenv("DD_PASS_POLL")) : 0;
-    p.poll_mode = env_pm;
-    static const int env_early = getenv("DD_PASS_EARLY") ? atoi(getenv("DD_PASS_EARLY")) : -1;
-    p.early = env_early;
     const int smem = pass_smem_bytes(m, p.nt, &p.stages);
     if (smem < 0) return ctx_fail(ctx, DD_E_ARG, "pass kernel shared memory plan failed");
     p.ps = ctx->d_ps;
@@ -364,7 +359,6 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.attn_part = ctx->attn_part;
     p.attn_cnt = ctx->attn_cnt;
     p.trace = trace;
-    p.trace2 = trace2;
     p.rank_of_smid = ctx->rank_of_smid_d;
     CK(launch_pass_kernel(ctx->map_h, ctx->map_o, ctx->map_a, p, smem, ctx->stream));
     return DD_OK;
@@ -1221,22 +1215,15 @@ int dd_debug_pass_timeline(dd_ctx* ctx, int w, uint64_t* trace, size_t max_entri
     unsigned long long* d = nullptr;
     CK(cudaMalloc(&d, sizeof(unsigned long long) * need));
     CK(cudaMemset(d, 0, sizeof(unsigned long long) * need));
-    const size_t need2 = 200 * 512 + static_cast<size_t>(kNumSMs) * 200 * 4;
-    unsigned long long* d2 = nullptr;
-    CK(cudaMalloc(&d2, sizeof(unsigned long long) * need2));
-    CK(cudaMemset(d2, 0, sizeof(unsigned long long) * need2));
     for (int rep = 0; rep < 2; ++rep) {
         rc = upload_dummy_pass(ctx, w);
         if (rc) return rc;
-        rc = enqueue_pass_kernel(ctx, w, true, rep ? d : nullptr, rep ? d2 : nullptr);
+        rc = enqueue_pass_kernel(ctx, w, true, rep ? d : nullptr);
         if (rc) return rc;
     }
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaMemcpy(trace, d, sizeof(unsigned long long) * need, cudaMemcpyDeviceToHost));
-    if (need + need2 <= max_entries)
-        CK(cudaMemcpy(trace + need, d2, sizeof(unsigned long long) * need2, cudaMemcpyDeviceToHost));
     cudaFree(d);
-    cudaFree(d2);
     *n_phases = n;
     ctx->last_w = 0;
     return DD_OK;

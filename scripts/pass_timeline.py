@@ -13,7 +13,7 @@ n_ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 t = Target(SHAPES["llama2_7b"], weight_seed=1234, plant=DEFAULT_PLANT, max_seq=4096)
 t.prefill([(7 * i) % 32000 for i in range(n_ctx)])
 lib = _lib.lib()
-cap = 148 * 200 * 12 + 200 * 512 + 148 * 200 * 4
+cap = 148 * 200 * 12
 buf = (C.c_uint64 * cap)()
 n = C.c_int()
 rc = lib.dd_debug_pass_timeline(t.h, w, buf, C.c_size_t(cap), C.byref(n))
@@ -49,16 +49,6 @@ for cta in range(0, 148, 21):
     r = a[cta, 9]
     print(f"cta {cta}: gu1 enter-poll {r[7]:.1f} polled {r[4]:.1f} fenced {r[5]:.1f} wstart {r[0]:.1f} | o1 mma_done {a[cta, 8, 2]:.1f} epi_done {a[cta, 8, 3]:.1f}")
 
-full = np.frombuffer(buf, dtype=np.uint64).astype(np.float64)
-base = 148 * n.value * 12
-tp = full[base: base + 200 * 512].reshape(200, 512)
-pb = full[base + 200 * 512: base + 200 * 512 + 148 * 200 * 4].reshape(148, 200, 4)
-T0 = np.frombuffer(buf, dtype=np.uint64)[: 148 * n.value * 12].reshape(148, n.value, 12)[:, 1:, 0]
-T0 = T0[T0 > 0].min()
-o = tp[8][:32]
-print("o1 per-tile publish (us, rel):", np.round(np.sort((o[o > 0] - T0) / 1e3), 1))
-b = pb[:, 9, :]
-print("gu1 poll batch done (us):", [np.round(np.sort((b[:, k][b[:, k] > 0] - T0) / 1e3)[[0, -1]], 1) if np.any(b[:, k] > 0) else None for k in range(2)])
 # per-CTA streaming speed consistency across layers (GU phases)
 d = np.array([a[:, 1 + 5 * l + 3, 2] - a[:, 1 + 5 * l + 3, 1] for l in range(1, 31)])  # [layer, cta]
 m = d.mean(0)
