@@ -219,8 +219,23 @@ struct Runner {
     std::vector<dd_iteration_record> recs;
     Clock::time_point t_start;
     double ttft = 0.0;
+    // Prompt suffix not yet in the cache (ends with c): the first scored pass of
+    // vanilla / duo covers it, so the target's forward over the prompt yields
+    // iteration 1's distribution directly instead of a prefill plus a
+    // one-token pass (the reference's iteration 1 scores the whole prefix).
+    std::vector<int32_t> pending;
 
     int c_token() const { return verified.back(); }
+
+    std::vector<int32_t> first_pass() {
+        std::vector<int32_t> p;
+        if (pending.empty()) {
+            p.push_back(c_token());
+        } else {
+            p.swap(pending);
+        }
+        return p;
+    }
 
     void truncate_cache() { ck(dd_kv_truncate(ctx, static_cast<int>(verified.size()) - 1), ctx); }
 
@@ -260,8 +275,8 @@ struct Runner {
     void run_vanilla() {  // engine.cpp:273-312
         while (verified.size() - prompt_len < static_cast<size_t>(cfg.max_new_tokens)) {
             const auto t0 = Clock::now();
-            int32_t c = c_token();
-            ck(dd_score(ctx, &c, 1), ctx);
+            const std::vector<int32_t> pass = first_pass();
+            ck(dd_score(ctx, pass.data(), static_cast<int>(pass.size())), ctx);
             const dd_verify_out o = verify(DD_MODE_VANILLA, 0, {}, true);
             verified.push_back(o.next_token);
             truncate_cache();
@@ -351,7 +366,7 @@ struct Runner {
                 std::vector<int32_t> z = verified;
                 const int L = tail ? static_cast<int>(tail->tokens.size()) : 0;
                 if (tail) z.insert(z.end(), tail->tokens.begin(), tail->tokens.end());
-                std::vector<int32_t> pass{c_token()};
+                std::vector<int32_t> pass = first_pass();
                 if (tail) pass.insert(pass.end(), tail->tokens.begin(), tail->tokens.end());
                 Bundle bundle;
                 const auto tt = Clock::now();
@@ -499,7 +514,12 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
         ck(ctx_mark(ctx, 0), ctx);
         r.t_start = Clock::now();
         ck(dd_kv_truncate(ctx, 0), ctx);
-        if (n_prompt > 1) ck(dd_prefill(ctx, prompt, n_prompt - 1), ctx);
+        // SpS drafts before its first pass, so its prefill (overlapping that
+        // drafting) stops before c; vanilla and duo score the last prefill chunk.
+        int keep = 1;
+        if (c.mode != DD_MODE_SPS) keep = (n_prompt - 1) % dd::kPrefillChunk + 1;
+        if (n_prompt > keep) ck(dd_prefill(ctx, prompt, n_prompt - keep), ctx);
+        if (keep > 1) r.pending.assign(prompt + n_prompt - keep, prompt + n_prompt);
         out->prefill_ms = 0.0;
         if (c.mode == DD_MODE_VANILLA) {
             r.run_vanilla();

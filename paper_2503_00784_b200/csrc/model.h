@@ -30,6 +30,7 @@ struct ModelDims {
 // Per-pass state shared by every kernel of a pass (device memory, updated by a
 // single small H2D copy before each pass so captured graphs stay valid).
 constexpr int kMaxPassTokens = 256;
+constexpr int kPrefillChunk = 128;  // dd_prefill's pass width: the tokens-on-M GEMM's tile height
 struct PassState {
     int n_cached;  // tokens already in the KV cache (absolute position of row 0)
     int w;         // tokens in this pass

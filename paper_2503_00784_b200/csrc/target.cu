@@ -718,7 +718,6 @@ int dd_prefill(dd_ctx* ctx, const int32_t* tokens, int n) {
     if (!ctx || (!tokens && n > 0) || n < 0) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
     if (!ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
     CK(cudaSetDevice(ctx->device));
-    constexpr int kPrefillChunk = 128;  // the tokens-on-M GEMM's tile height
     for (int i = 0; i < n; i += kPrefillChunk) {
         const int w = std::min(kPrefillChunk, n - i);
         int rc = run_pass(ctx, tokens + i, w, false);
