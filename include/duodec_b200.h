@@ -77,6 +77,29 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out);
 void dd_ctx_destroy(dd_ctx* ctx);
 const char* dd_last_error(const dd_ctx* ctx); /* ctx may be NULL: global error */
 
+/* Tensor parallelism (BASELINE config 5: 70B-shape TP=8; the
+ * reference has no multi-GPU target, this replaces its single ModelSpec
+ * forward with a Megatron-split one).  Rank tp_rank of tp_size holds
+ * n_heads/tp_size q heads, n_kv_heads/tp_size kv heads, ffn_dim/tp_size FFN
+ * features and a 128-row-aligned slice of the LM head; the embedding and the
+ * residual stream are replicated.  dd_weights_init generates the rank's
+ * slice of the same full model for any tp_size.  Before the first pass the
+ * ranks connect their exchange buffers: one process per GPU exports a CUDA
+ * IPC handle (dd_tp_export), gathers all tp_size handles in rank order over
+ * the host (e.g. torch.distributed all_gather_object) and calls
+ * dd_tp_connect; a single process driving every rank calls
+ * dd_tp_connect_local.  Every rank must then issue the same sequence of
+ * passes (dd_prefill / dd_score with the same widths): each pass ends with
+ * the full logits on every rank and dd_verify runs redundantly with the same
+ * seed and counter.  The CUDA-event timing helpers (dd_time_pass, ...) are
+ * single-rank only. */
+#define DD_TP_HANDLE_BYTES 64
+int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, int tp_size,
+                     dd_ctx** out);
+int dd_tp_export(dd_ctx* ctx, void* ipc_handle /* DD_TP_HANDLE_BYTES */);
+int dd_tp_connect(dd_ctx* ctx, const void* ipc_handles /* tp_size x DD_TP_HANDLE_BYTES */);
+int dd_tp_connect_local(dd_ctx* const* ctxs, int n);
+
 /* Generate all weights on the device from (weight_seed, plant); bit-identical
  * to the CPU oracle's generator (oracle/llama_ref.c). plant may be NULL. */
 int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plant);

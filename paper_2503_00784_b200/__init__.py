@@ -97,15 +97,37 @@ class Target:
     role (proj/include/duodec/model.hpp:57-65)."""
 
     def __init__(self, shape: dict, weight_seed: int = 1234, plant: Optional[dict] = None,
-                 max_seq: int = 4096, device: int = 0, page_size: int = 16):
+                 max_seq: int = 4096, device: int = 0, page_size: int = 16, tp_rank: int = 0,
+                 tp_size: int = 1):
         self.shape = dict(shape)
         self.vocab = shape["vocab"]
+        self.tp_rank, self.tp_size = tp_rank, tp_size
         h = C.c_void_p()
-        _check(_L.lib().dd_ctx_create(C.byref(_desc(shape, max_seq, page_size)), device,
-                                      C.byref(h)))
+        _check(_L.lib().dd_ctx_create_tp(C.byref(_desc(shape, max_seq, page_size)), device,
+                                         tp_rank, tp_size, C.byref(h)))
         self.h = h
         pl = _plant(plant)
         _check(_L.lib().dd_weights_init(self.h, weight_seed, C.byref(pl) if pl else None), self.h)
+
+    # ---- tensor parallelism (include/duodec_b200.h, dd_ctx_create_tp)
+    def tp_handle(self) -> bytes:
+        """This rank's CUDA IPC handle, to all-gather across the rank processes."""
+        buf = C.create_string_buffer(_L.DD_TP_HANDLE_BYTES)
+        _check(_L.lib().dd_tp_export(self.h, buf), self.h)
+        return buf.raw
+
+    def tp_connect(self, handles: Sequence[bytes]) -> None:
+        """Open every rank's exchange buffer (handles in rank order)."""
+        blob = b"".join(handles)
+        if len(handles) != self.tp_size or len(blob) != self.tp_size * _L.DD_TP_HANDLE_BYTES:
+            raise ConfigError("need one IPC handle per rank")
+        _check(_L.lib().dd_tp_connect(self.h, blob), self.h)
+
+    @staticmethod
+    def tp_connect_local(ranks: Sequence["Target"]) -> None:
+        """Connect the ranks of one process (ranks[r] is rank r)."""
+        arr = (C.c_void_p * len(ranks))(*[t.h.value for t in ranks])
+        _check(_L.lib().dd_tp_connect_local(arr, len(ranks)), ranks[0].h)
 
     # ---- forward contract
     def prefill(self, tokens: Sequence[int]) -> None:

@@ -13,6 +13,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libduodec_b200.so"
 DD_OK, DD_E_ARG, DD_E_CUDA, DD_E_STATE, DD_E_CAPACITY = 0, -1, -2, -3, -4
 DD_MODE_DUO, DD_MODE_SPS, DD_MODE_VANILLA = 0, 1, 2
 DD_BUDGET_FIXED, DD_BUDGET_CALIBRATED = 0, 1
+DD_TP_HANDLE_BYTES = 64
 
 
 class ModelDesc(C.Structure):
@@ -73,6 +74,10 @@ _f64p = C.POINTER(C.c_double)
 SIGNATURES = {
     "dd_ctx_create": (C.c_int, [C.POINTER(ModelDesc), C.c_int, C.POINTER(_vp)]),
     "dd_ctx_destroy": (None, [_vp]),
+    "dd_ctx_create_tp": (C.c_int, [C.POINTER(ModelDesc), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "dd_tp_export": (C.c_int, [_vp, C.c_char_p]),
+    "dd_tp_connect": (C.c_int, [_vp, C.c_char_p]),
+    "dd_tp_connect_local": (C.c_int, [C.POINTER(_vp), C.c_int]),
     "dd_last_error": (C.c_char_p, [_vp]),
     "dd_weights_init": (C.c_int, [_vp, C.c_uint64, C.POINTER(PlantDesc)]),
     "dd_prefill": (C.c_int, [_vp, _i32p, C.c_int]),

@@ -17,7 +17,8 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libduodec_b200.so"
 
-CU_SOURCES = ["gemm.cu", "gemm_wide.cu", "model.cu", "attention.cu", "pass.cu", "accept.cu", "target.cu"]
+CU_SOURCES = ["gemm.cu", "gemm_wide.cu", "model.cu", "attention.cu", "pass.cu", "accept.cu", "tp.cu",
+              "target.cu"]
 CPP_SOURCES = ["plant.cpp", "draft.cpp", "engine.cpp"]
 
 NVCC_FLAGS = [

@@ -14,6 +14,7 @@
 #include "model.h"
 #include "pass.h"
 #include "plant.h"
+#include "tp.h"
 
 namespace dd {
 
@@ -34,7 +35,16 @@ struct dd_ctx {
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     cudaEvent_t q_ready = nullptr;
     cudaEvent_t ps_done[dd::kPsRing] = {};
-    dd::ModelDims m{};
+    dd::ModelDims m{};  // this rank's shard: local heads, FFN features, head (vocabulary) rows
+    int vocab = 0;      // full vocabulary (tokens, logits, acceptance)
+    // tensor parallelism (tp.h); tp_size 1 = unsharded
+    int tp_rank = 0, tp_size = 1;
+    std::vector<int> tp_v0;        // vocabulary split, [tp_size + 1]
+    void* tp_xbuf = nullptr;       // symmetric exchange buffer (flags | partials | local logits)
+    dd::TpLayout tp_lay{};
+    dd::TpPeers tp_peers{};        // every rank's exchange buffer (device pointers)
+    bool tp_connected = false;
+    std::vector<void*> tp_opened;  // IPC-opened peer buffers
     int max_seq = 0, page_size = 16, n_pages = 0;
     bool weights_ready = false, use_graphs = true;
 

@@ -28,64 +28,71 @@ static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // ------------------------------------------------------------ weights
-// Logical element e = r * cols + c of a generated tensor goes to physical row
-// row0 + r (plain) of a pre-tiled matrix with `tcols` columns.
+// Element (r, c) of a rows x cols block is logical element
+// (src.row0 + r) * src.cols + src.col0 + c of the full generated tensor (the
+// whole tensor when unsharded, one rank's rows or columns under tensor
+// parallelism), written to physical row row0 + r of a pre-tiled matrix with
+// `cols` columns.
 __global__ void init_matrix_kernel(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
-                                   uint64_t seed, float amp, uint64_t row0, int tiled) {
+                                   uint64_t seed, float amp, uint64_t row0, int tiled,
+                                   SrcWindow src) {
     const uint64_t n = rows * cols;
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
-        const uint64_t r = row0 + e / cols, c = e % cols;
-        dst[tiled ? tiled_offset(r, c, cols) : r * cols + c] = v;
+        const uint64_t r = e / cols, c = e % cols;
+        const uint64_t le = (src.row0 + r) * (src.cols ? src.cols : cols) + src.col0 + c;
+        const __nv_bfloat16 v = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, le), amp));
+        dst[tiled ? tiled_offset(row0 + r, c, cols) : (row0 + r) * cols + c] = v;
     }
 }
 
 void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64_t seed,
-                        float amp, cudaStream_t s, uint64_t row0, int tiled) {
-    init_matrix_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, row0, tiled);
+                        float amp, cudaStream_t s, uint64_t row0, int tiled, SrcWindow src) {
+    init_matrix_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, row0, tiled, src);
 }
 
 // Logical row r of a [rows, cols] tensor stored at physical row
 // (r / 64) * 128 + offset + r % 64: the gate/up interleave that lets one
 // 128-row GEMM tile hold matching gate and up features (SwiGLU epilogue).
 __global__ void init_matrix_il_kernel(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
-                                      uint64_t seed, float amp, int offset) {
+                                      uint64_t seed, float amp, int offset, uint64_t src_row0) {
     const uint64_t n = rows * cols;
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t r = e / cols, c = e % cols;
         const uint64_t pr = (r / 64) * 128 + offset + r % 64;
-        dst[tiled_offset(pr, c, cols)] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, e), amp));
+        const uint64_t le = (src_row0 + r) * cols + c;
+        dst[tiled_offset(pr, c, cols)] = __float2bfloat16_rn(__fmul_rn(weight_unit(seed, le), amp));
     }
 }
 
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
-                                    uint64_t seed, float amp, int offset, cudaStream_t s) {
-    init_matrix_il_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, offset);
+                                    uint64_t seed, float amp, int offset, cudaStream_t s,
+                                    uint64_t src_row0) {
+    init_matrix_il_kernel<<<kNumSMs * 8, 256, 0, s>>>(dst, rows, cols, seed, amp, offset, src_row0);
 }
 
 // LM head: random rows plus, for planted tokens t, row pi(t) += coef * E[t].
-// plant_src[v] = t (or -1) with pi(t) = v.
+// plant_src[v] = t (or -1) with pi(t) = v.  Local row r is vocabulary row v0 + r.
 __global__ void init_head_kernel(__nv_bfloat16* head, const __nv_bfloat16* emb,
-                                 const int32_t* plant_src, uint64_t vocab, uint64_t d,
-                                 uint64_t seed, float amp, float coef) {
-    const uint64_t n = vocab * d;
+                                 const int32_t* plant_src, uint64_t rows, uint64_t d,
+                                 uint64_t seed, float amp, float coef, uint64_t v0) {
+    const uint64_t n = rows * d;
     for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        float w = __fmul_rn(weight_unit(seed, e), amp);
-        const uint64_t v = e / d, i = e % d;
+        const uint64_t r = e / d, i = e % d, v = v0 + r;
+        float w = __fmul_rn(weight_unit(seed, v * d + i), amp);
         const int32_t t = plant_src ? plant_src[v] : -1;
         if (t >= 0) w = __fmaf_rn(coef, __bfloat162float(emb[static_cast<uint64_t>(t) * d + i]), w);
-        head[tiled_offset(v, i, d)] = __float2bfloat16_rn(w);
+        head[tiled_offset(r, i, d)] = __float2bfloat16_rn(w);
     }
 }
 
 void launch_init_head(__nv_bfloat16* head, const __nv_bfloat16* emb, const int32_t* plant_src,
-                      uint64_t vocab, uint64_t d, uint64_t seed, float amp, float plant_coef,
-                      cudaStream_t s) {
-    init_head_kernel<<<kNumSMs * 8, 256, 0, s>>>(head, emb, plant_src, vocab, d, seed, amp,
-                                                 plant_coef);
+                      uint64_t rows, uint64_t d, uint64_t seed, float amp, float plant_coef,
+                      cudaStream_t s, uint64_t v0) {
+    init_head_kernel<<<kNumSMs * 8, 256, 0, s>>>(head, emb, plant_src, rows, d, seed, amp,
+                                                 plant_coef, v0);
 }
 
 __global__ void fill_f32_kernel(float* dst, size_t n, float v) {

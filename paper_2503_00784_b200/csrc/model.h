@@ -40,12 +40,19 @@ struct PassState {
 };
 
 // ---------------------------------------------------------------- kernels
+// Which block of the full generated tensor a (sharded) matrix holds: logical
+// element (row0 + r) * cols + col0 + c (cols == 0: the block's own width).
+struct SrcWindow {
+    uint64_t row0 = 0, col0 = 0, cols = 0;
+};
 // row0: first physical row; tiled: write the pre-tiled GEMM layout (common.cuh)
 void launch_init_matrix(__nv_bfloat16* dst, uint64_t rows, uint64_t cols, uint64_t seed,
-                        float amp, cudaStream_t s, uint64_t row0 = 0, int tiled = 1);
+                        float amp, cudaStream_t s, uint64_t row0 = 0, int tiled = 1,
+                        SrcWindow src = {});
+// rows: head rows held (vocabulary rows v0 .. v0 + rows - 1)
 void launch_init_head(__nv_bfloat16* head, const __nv_bfloat16* emb, const int32_t* plant_src,
-                      uint64_t vocab, uint64_t d, uint64_t seed, float amp, float plant_coef,
-                      cudaStream_t s);
+                      uint64_t rows, uint64_t d, uint64_t seed, float amp, float plant_coef,
+                      cudaStream_t s, uint64_t v0 = 0);
 void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
@@ -58,7 +65,8 @@ int launch_attention(const PassState* ps, int w, const ModelDims& m, const float
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s);
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
-                                    uint64_t seed, float amp, int offset, cudaStream_t s);
+                                    uint64_t seed, float amp, int offset, cudaStream_t s,
+                                    uint64_t src_row0 = 0);
 void launch_kv_compact(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                        const ModelDims& m, const int32_t* src_pos, const int32_t* dst_pos, int n,
                        cudaStream_t s);

@@ -109,6 +109,27 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         mark(0);
         return r;
     };
+    // Row-parallel GEMM (O, down): unsharded, the residual epilogue is fused;
+    // under tensor parallelism the GEMM stores its fp32 partial and
+    // tp_reduce_residual sums the ranks' partials and applies the same epilogue.
+    const bool tp = ctx->tp_size > 1;
+    const int tp_ops = 2 * m.n_layers + 1;
+    int tp_op = 0;
+    auto row_parallel = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
+                            const GemmEpiParams& er) -> cudaError_t {
+        if (!tp) return gemm(id, mw, mx, er);
+        GemmEpiParams ep = er;
+        ep.kind = kEpiStore;
+        ep.out = ctx->tp_peers.part[ctx->tp_rank] + static_cast<size_t>(tp_op & 1) * ctx->tp_lay.part_stride;
+        ep.u_out = nullptr;
+        cudaError_t r = gemm(id, mw, mx, ep);
+        if (r != cudaSuccess) return r;
+        launch_tp_reduce_residual(ctx->tp_peers, ctx->d_ps, tp_op, tp_ops, m.d, er.out, er.u_out,
+                                  er.gain, er.ss_out, s);
+        mark(2);
+        ++tp_op;
+        return cudaGetLastError();
+    };
     const int d_tiles = m.d / 128;
     // deferred RMSNorm: consumers of h scale by r computed from ss partials
     e.ss_in = ctx->ss;
@@ -135,18 +156,22 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         er.u_out = ctx->h;
         er.gain = ctx->gain_ones;
         er.ss_out = ctx->ss;
-        CK(gemm(kGO, L.o, &ctx->map_o, er));
+        CK(row_parallel(kGO, L.o, &ctx->map_o, er));
         GemmEpiParams eg = e;
         eg.kind = kEpiSwiGLU;
         eg.out_bf = ctx->a;
         CK(gemm(kGGu, L.gu, &ctx->map_h, eg));
-        CK(gemm(kGDown, L.dn, &ctx->map_a, er));
+        CK(row_parallel(kGDown, L.dn, &ctx->map_a, er));
     }
     if (want_logits) {
         GemmEpiParams el = e;
         el.kind = kEpiStore;
-        el.out = ctx->logits;
+        el.out = tp ? ctx->tp_peers.lg[ctx->tp_rank] : ctx->logits;
         CK(gemm(kGHead, ctx->head, &ctx->map_h, el));
+        if (tp) {
+            launch_tp_gather_logits(ctx->tp_peers, ctx->d_ps, tp_op, tp_ops, ctx->vocab, ctx->logits, s);
+            mark(2);
+        }
     }
     CK(cudaGetLastError());
     return DD_OK;
@@ -404,8 +429,10 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
     if (ctx->n_cached + w > ctx->max_seq)
         return ctx_fail(ctx, DD_E_CAPACITY, "KV cache capacity exceeded");
     for (int i = 0; i < w; ++i)
-        if (tokens[i] < 0 || tokens[i] >= ctx->m.vocab)
+        if (tokens[i] < 0 || tokens[i] >= ctx->vocab)
             return ctx_fail(ctx, DD_E_ARG, "token outside vocabulary");
+    if (ctx->tp_size > 1 && !ctx->tp_connected)
+        return ctx_fail(ctx, DD_E_STATE, "tensor-parallel ranks not connected (dd_tp_connect)");
     const int slot = ctx->ps_slot;
     ctx->ps_slot = (slot + 1) % kPsRing;
     CK(cudaEventSynchronize(ctx->ps_done[slot]));
@@ -462,17 +489,30 @@ const char* dd_last_error(const dd_ctx* ctx) {
 }
 
 int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
+    return dd_ctx_create_tp(desc, cuda_device, 0, 1, out);
+}
+
+int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, int tp_size,
+                     dd_ctx** out) {
     dd_ctx* ctx = nullptr;
     if (!desc || !out) return ctx_fail(nullptr, DD_E_ARG, "null argument");
     *out = nullptr;
     const dd_model_desc& d = *desc;
+    const int n_kv = d.n_kv_heads > 0 ? d.n_kv_heads : d.n_heads;
+    if (tp_size < 1 || tp_size > kMaxTp || tp_rank < 0 || tp_rank >= tp_size)
+        return ctx_fail(nullptr, DD_E_ARG, "bad tensor-parallel rank / size");
+    // Megatron split: whole heads (q and kv) and 64-feature FFN blocks per rank
+    if (d.n_heads % tp_size || n_kv % tp_size || d.ffn_dim % (64 * tp_size) ||
+        d.vocab / 128 < tp_size)
+        return ctx_fail(nullptr, DD_E_ARG, "shape does not split over the tensor-parallel ranks");
+    const int h_l = d.n_heads / tp_size, kv_l = n_kv / tp_size, ffn_l = d.ffn_dim / tp_size;
     if (d.n_layers < 1 || d.d_model % 128 || d.head_dim % 32 || d.head_dim > 256 ||
-        d.n_heads % std::max(1, d.n_kv_heads) || d.ffn_dim % 128 || d.vocab % 128 ||
-        (d.n_heads * d.head_dim) % 128 || (std::max(1, d.n_kv_heads) * d.head_dim) % 128 ||
+        d.n_heads % std::max(1, n_kv) || (tp_size == 1 && d.ffn_dim % 128) || d.vocab % 128 ||
+        (h_l * d.head_dim) % 128 || (kv_l * d.head_dim) % 128 ||
         (d.head_dim != 64 && d.head_dim != 128) || d.max_seq < 1)
         return ctx_fail(nullptr, DD_E_ARG,
                         "unsupported shape (d_model, ffn_dim, vocab must be multiples of 128; "
-                        "head_dim 64/128; q and kv widths multiples of 128)");
+                        "head_dim 64/128; per-rank q and kv widths multiples of 128)");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cuda_device)
         return ctx_fail(nullptr, DD_E_CUDA, "no CUDA device available (no CPU fallback exists)");
@@ -482,14 +522,20 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     ctx = new dd_ctx();
     ctx->device = cuda_device;
     CK(cudaSetDevice(cuda_device));
+    ctx->tp_rank = tp_rank;
+    ctx->tp_size = tp_size;
+    ctx->vocab = d.vocab;
+    ctx->tp_v0.resize(tp_size + 1);
+    for (int r = 0; r <= tp_size; ++r)  // whole 128-row head tiles per rank
+        ctx->tp_v0[r] = 128 * static_cast<int>(static_cast<int64_t>(d.vocab / 128) * r / tp_size);
     ModelDims& m = ctx->m;
     m.n_layers = d.n_layers;
     m.d = d.d_model;
-    m.n_heads = d.n_heads;
-    m.n_kv_heads = d.n_kv_heads > 0 ? d.n_kv_heads : d.n_heads;
+    m.n_heads = h_l;
+    m.n_kv_heads = kv_l;
     m.head_dim = d.head_dim;
-    m.ffn = d.ffn_dim;
-    m.vocab = d.vocab;
+    m.ffn = ffn_l;
+    m.vocab = ctx->tp_v0[tp_rank + 1] - ctx->tp_v0[tp_rank];
     m.eps = d.rms_eps;
     m.rope_theta = d.rope_theta;
     ctx->page_size = d.page_size > 0 ? d.page_size : 16;
@@ -502,7 +548,7 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
 
     // weights
     const size_t d_ = m.d;
-    CK(cudaMalloc(&ctx->emb, sizeof(__nv_bfloat16) * m.vocab * d_));
+    CK(cudaMalloc(&ctx->emb, sizeof(__nv_bfloat16) * ctx->vocab * d_));  // replicated
     CK(cudaMalloc(&ctx->head, sizeof(__nv_bfloat16) * m.vocab * d_));
     ctx->layers.resize(m.n_layers);
     for (auto& L : ctx->layers) {
@@ -559,7 +605,18 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
     CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
     CK(cudaMalloc(&ctx->ss, sizeof(float) * R * (m.d / 128)));
-    CK(cudaMalloc(&ctx->logits, sizeof(float) * R * m.vocab));
+    CK(cudaMalloc(&ctx->logits, sizeof(float) * R * ctx->vocab));
+    if (tp_size > 1) {
+        int max_lv = 0;
+        for (int r = 0; r < tp_size; ++r) max_lv = std::max(max_lv, ctx->tp_v0[r + 1] - ctx->tp_v0[r]);
+        ctx->tp_lay = tp_layout(m.d, max_lv);
+        CK(cudaMalloc(&ctx->tp_xbuf, ctx->tp_lay.bytes));
+        CK(cudaMemset(ctx->tp_xbuf, 0, ctx->tp_lay.bytes));
+        TpPeers& P = ctx->tp_peers;
+        P.rank = tp_rank;
+        P.size = tp_size;
+        for (int r = 0; r <= tp_size; ++r) P.v0[r] = ctx->tp_v0[r];
+    }
 
     // paged KV cache (all pages reserved up front; page table maps logical->physical)
     const size_t kv_elems = static_cast<size_t>(ctx->n_pages) * m.n_layers * 2 * m.n_kv_heads *
@@ -574,7 +631,9 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     // persistent pass kernel scratch
     {
         const char* env = getenv("DD_PASS_KERNEL");
-        ctx->use_pass_kernel = !(env && env[0] == '0');
+        // the persistent pass kernel has no cross-rank reduction (tp.h): sharded
+        // contexts run one launch per GEMM / attention / reduction
+        ctx->use_pass_kernel = !(env && env[0] == '0') && tp_size == 1;
         // embed + per layer (qkv, attention, o, gate/up, down) + head
         const size_t per_layer = m.qkv_rows() / 128 + m.n_heads * 16 + m.d / 128 + 2 * m.ffn / 128 + m.d / 128;
         const size_t n_flags = m.d / 128 + per_layer * m.n_layers + m.vocab / 128;
@@ -624,9 +683,9 @@ int dd_ctx_create(const dd_model_desc* desc, int cuda_device, dd_ctx** out) {
     CK(cudaMemset(ctx->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&ctx->d_out, sizeof(dd_verify_out)));
     CK(cudaHostAlloc(&ctx->h_out, sizeof(dd_verify_out), cudaHostAllocDefault));
-    CK(cudaMalloc(&ctx->q_rows, sizeof(float) * kMaxPassTokens * m.vocab));
+    CK(cudaMalloc(&ctx->q_rows, sizeof(float) * kMaxPassTokens * ctx->vocab));
     CK(cudaMalloc(&ctx->d_tail, sizeof(int32_t) * kMaxPassTokens));
-    CK(cudaHostAlloc(&ctx->h_q_stage, sizeof(float) * kMaxPassTokens * m.vocab,
+    CK(cudaHostAlloc(&ctx->h_q_stage, sizeof(float) * kMaxPassTokens * ctx->vocab,
                      cudaHostAllocDefault));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->use_graphs = true;
@@ -657,6 +716,8 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->attn_part, ctx->attn_cnt, ctx->sk_prefix_d, ctx->rank_of_smid_d};
     for (void* p : dev)
         if (p) cudaFree(p);
+    for (void* p : ctx->tp_opened) cudaIpcCloseMemHandle(p);
+    if (ctx->tp_xbuf) cudaFree(ctx->tp_xbuf);
     if (ctx->h_ps) cudaFreeHost(ctx->h_ps);
     if (ctx->h_out) cudaFreeHost(ctx->h_out);
     if (ctx->h_q_stage) cudaFreeHost(ctx->h_q_stage);
@@ -674,34 +735,40 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
     const ModelDims& m = ctx->m;
     const float amp_proj = static_cast<float>(0.02 * std::sqrt(3.0));
     const float amp_out = static_cast<float>(0.02 / std::sqrt(2.0 * m.n_layers) * std::sqrt(3.0));
-    PlantTable pt = make_plant_table(m.vocab, m.d, plant);
+    PlantTable pt = make_plant_table(ctx->vocab, m.d, plant);
     const float amp_emb = static_cast<float>(pt.emb_std * std::sqrt(3.0));
     cudaStream_t s = ctx->stream;
     const uint64_t d_ = m.d;
-    launch_init_matrix(ctx->emb, m.vocab, d_, derive_seed(weight_seed, kTensorEmb), amp_emb, s, 0,
+    launch_init_matrix(ctx->emb, ctx->vocab, d_, derive_seed(weight_seed, kTensorEmb), amp_emb, s, 0,
                        0);  // gathered, row-major
     int32_t* d_src = nullptr;
     if (pt.any) {
-        CK(cudaMalloc(&d_src, sizeof(int32_t) * m.vocab));
-        CK(cudaMemcpyAsync(d_src, pt.src.data(), sizeof(int32_t) * m.vocab, cudaMemcpyHostToDevice,
+        CK(cudaMalloc(&d_src, sizeof(int32_t) * ctx->vocab));
+        CK(cudaMemcpyAsync(d_src, pt.src.data(), sizeof(int32_t) * ctx->vocab, cudaMemcpyHostToDevice,
                            s));
     }
     launch_init_head(ctx->head, ctx->emb, d_src, m.vocab, d_, derive_seed(weight_seed, kTensorHead),
-                     amp_proj, pt.coef, s);
+                     amp_proj, pt.coef, s, ctx->tp_v0[ctx->tp_rank]);
+    // this rank's rows (column-parallel) or columns (row-parallel) of every
+    // full generated tensor, so any tp_size reproduces the same model
+    const uint64_t r = ctx->tp_rank, tp = ctx->tp_size;
     for (int l = 0; l < m.n_layers; ++l) {
         LayerW& L = ctx->layers[l];
-        const uint64_t qd = m.q_dim(), kvd = m.kv_dim();
-        launch_init_matrix(L.qkv, qd, d_, derive_seed(weight_seed, tensor_id(l, kWq)), amp_proj, s, 0);
+        const uint64_t qd = m.q_dim(), kvd = m.kv_dim(), f = m.ffn;
+        launch_init_matrix(L.qkv, qd, d_, derive_seed(weight_seed, tensor_id(l, kWq)), amp_proj, s, 0,
+                           1, SrcWindow{r * qd, 0, 0});
         launch_init_matrix(L.qkv, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWk)), amp_proj, s,
-                           qd);
+                           qd, 1, SrcWindow{r * kvd, 0, 0});
         launch_init_matrix(L.qkv, kvd, d_, derive_seed(weight_seed, tensor_id(l, kWv)), amp_proj, s,
-                           qd + kvd);
-        launch_init_matrix(L.o, d_, qd, derive_seed(weight_seed, tensor_id(l, kWo)), amp_out, s);
-        launch_init_matrix_interleaved(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWg)),
-                                       amp_proj, 0, s);
-        launch_init_matrix_interleaved(L.gu, m.ffn, d_, derive_seed(weight_seed, tensor_id(l, kWu)),
-                                       amp_proj, 64, s);
-        launch_init_matrix(L.dn, d_, m.ffn, derive_seed(weight_seed, tensor_id(l, kWd)), amp_out, s);
+                           qd + kvd, 1, SrcWindow{r * kvd, 0, 0});
+        launch_init_matrix(L.o, d_, qd, derive_seed(weight_seed, tensor_id(l, kWo)), amp_out, s, 0, 1,
+                           SrcWindow{0, r * qd, qd * tp});
+        launch_init_matrix_interleaved(L.gu, f, d_, derive_seed(weight_seed, tensor_id(l, kWg)),
+                                       amp_proj, 0, s, r * f);
+        launch_init_matrix_interleaved(L.gu, f, d_, derive_seed(weight_seed, tensor_id(l, kWu)),
+                                       amp_proj, 64, s, r * f);
+        launch_init_matrix(L.dn, d_, f, derive_seed(weight_seed, tensor_id(l, kWd)), amp_out, s, 0, 1,
+                           SrcWindow{0, r * f, f * tp});
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -711,6 +778,74 @@ int dd_weights_init(dd_ctx* ctx, uint64_t weight_seed, const dd_plant_desc* plan
     // B200s: the slow SMs share a saturated resource)
     const char* bal = getenv("DD_PASS_BALANCE");
     if (ctx->use_pass_kernel && bal && bal[0] == '1') return dd_pass_balance(ctx);
+    return DD_OK;
+}
+
+static void tp_set_peer(dd_ctx* ctx, int r, char* base) {
+    TpPeers& P = ctx->tp_peers;
+    P.flags[r] = reinterpret_cast<int*>(base + ctx->tp_lay.flags_off);
+    P.part[r] = reinterpret_cast<float*>(base + ctx->tp_lay.part_off);
+    P.lg[r] = reinterpret_cast<float*>(base + ctx->tp_lay.lg_off);
+}
+
+int dd_tp_export(dd_ctx* ctx, void* ipc_handle) {
+    if (!ctx || !ipc_handle) return ctx_fail(ctx, DD_E_ARG, "null argument");
+    if (ctx->tp_size < 2) return ctx_fail(ctx, DD_E_STATE, "context is not tensor-parallel");
+    CK(cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, ctx->tp_xbuf));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+    return DD_OK;
+}
+
+int dd_tp_connect(dd_ctx* ctx, const void* ipc_handles) {
+    if (!ctx || !ipc_handles) return ctx_fail(ctx, DD_E_ARG, "null argument");
+    if (ctx->tp_size < 2 || ctx->tp_connected)
+        return ctx_fail(ctx, DD_E_STATE, "context is not tensor-parallel or already connected");
+    static_assert(sizeof(cudaIpcMemHandle_t) == DD_TP_HANDLE_BYTES, "IPC handle size");
+    CK(cudaSetDevice(ctx->device));
+    const char* hb = static_cast<const char*>(ipc_handles);
+    for (int r = 0; r < ctx->tp_size; ++r) {
+        if (r == ctx->tp_rank) {
+            tp_set_peer(ctx, r, static_cast<char*>(ctx->tp_xbuf));
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hb + static_cast<size_t>(r) * DD_TP_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->tp_opened.push_back(p);
+        tp_set_peer(ctx, r, static_cast<char*>(p));
+    }
+    ctx->tp_connected = true;
+    return DD_OK;
+}
+
+int dd_tp_connect_local(dd_ctx* const* ctxs, int n) {
+    if (!ctxs || n < 2 || n > kMaxTp) return ctx_fail(nullptr, DD_E_ARG, "bad rank list");
+    for (int r = 0; r < n; ++r)
+        if (!ctxs[r] || ctxs[r]->tp_size != n || ctxs[r]->tp_rank != r || ctxs[r]->tp_connected)
+            return ctx_fail(ctxs[r], DD_E_ARG, "ctxs[r] must be unconnected rank r of an n-way split");
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            dd_ctx* ctx = ctxs[i];  // error target of CK
+            const int di = ctxs[i]->device, dj = ctxs[j]->device;
+            if (di == dj) continue;
+            int ok = 0;
+            CK(cudaDeviceCanAccessPeer(&ok, di, dj));
+            if (!ok) return ctx_fail(ctxs[i], DD_E_CUDA, "no peer access between the ranks' GPUs");
+            CK(cudaSetDevice(di));
+            cudaError_t e = cudaDeviceEnablePeerAccess(dj, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else if (e != cudaSuccess) {
+                return ctx_fail(ctxs[i], DD_E_CUDA, cudaGetErrorString(e));
+            }
+        }
+    for (int i = 0; i < n; ++i) {
+        for (int r = 0; r < n; ++r) tp_set_peer(ctxs[i], r, static_cast<char*>(ctxs[r]->tp_xbuf));
+        ctxs[i]->tp_connected = true;
+    }
     return DD_OK;
 }
 
@@ -768,8 +903,8 @@ int dd_read_logits(dd_ctx* ctx, float* host, int row0, int rows) {
     if (row0 < 0 || rows < 0 || row0 + rows > ctx->last_w)
         return ctx_fail(ctx, DD_E_ARG, "rows outside the last pass");
     CK(cudaSetDevice(ctx->device));
-    CK(cudaMemcpyAsync(host, ctx->logits + static_cast<size_t>(row0) * ctx->m.vocab,
-                       sizeof(float) * rows * ctx->m.vocab, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(host, ctx->logits + static_cast<size_t>(row0) * ctx->vocab,
+                       sizeof(float) * rows * ctx->vocab, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return DD_OK;
 }
@@ -777,7 +912,7 @@ int dd_read_logits(dd_ctx* ctx, float* host, int row0, int rows) {
 int dd_upload_q(dd_ctx* ctx, const float* q_rows, int rows, int vocab) {
     if (!ctx || (!q_rows && rows > 0)) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
     // vocab may be below the model's for dd_verify_probs (Markov-table rows)
-    if (vocab < 1 || vocab > ctx->m.vocab || rows < 0 || rows > kMaxPassTokens)
+    if (vocab < 1 || vocab > ctx->vocab || rows < 0 || rows > kMaxPassTokens)
         return ctx_fail(ctx, DD_E_ARG, "q rows shape mismatch");
     CK(cudaSetDevice(ctx->device));
     const size_t bytes = sizeof(float) * static_cast<size_t>(rows) * vocab;
@@ -831,7 +966,7 @@ static int check_verify_args(dd_ctx* ctx, const dd_verify_args* args) {
     if (args->tail_len < 0 || (args->mode == DD_MODE_VANILLA && args->tail_len != 0))
         return ctx_fail(ctx, DD_E_ARG, "bad tail length");
     for (int i = 0; i < args->n_firsts; ++i)
-        if (args->firsts[i] < 0 || args->firsts[i] >= ctx->m.vocab)
+        if (args->firsts[i] < 0 || args->firsts[i] >= ctx->vocab)
             return ctx_fail(ctx, DD_E_ARG, "bundle token outside vocabulary");
     return DD_OK;
 }
@@ -845,7 +980,7 @@ int dd_verify(dd_ctx* ctx, const dd_verify_args* args, dd_verify_out* out) {
     if (L + 1 > ctx->last_w) return ctx_fail(ctx, DD_E_ARG, "tail longer than the scored pass");
     CK(cudaSetDevice(ctx->device));
     AcceptParams p{};
-    p.V = ctx->m.vocab;
+    p.V = ctx->vocab;
     p.L = L;
     p.row0 = ctx->last_w - 1 - L;
     p.logits = ctx->logits;
@@ -1101,7 +1236,7 @@ int dd_read_weights(dd_ctx* ctx, int which, int layer, uint16_t* host, size_t n)
     size_t count = 0;
     const size_t d_ = m.d;
     switch (which) {
-        case 0: src = ctx->emb; count = static_cast<size_t>(m.vocab) * d_; break;
+        case 0: src = ctx->emb; count = static_cast<size_t>(ctx->vocab) * d_; break;
         case 1: src = ctx->head; count = static_cast<size_t>(m.vocab) * d_; break;
         case 2: src = ctx->layers[layer].qkv; count = static_cast<size_t>(m.qkv_rows()) * d_; break;
         case 3: src = ctx->layers[layer].o; count = d_ * m.q_dim(); break;

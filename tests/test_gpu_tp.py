@@ -1,0 +1,121 @@
+"""Tensor-parallel target on one GPU (-m gpu).
+
+The round's GPU boxes have one B200, so the Megatron split is exercised with
+both ranks of a TP=2 group on the same device, connected in-process
+(dd_tp_connect_local): the exchange kernels (csrc/tp.cu) run the same code on
+peer pointers whether the peer buffer is on this GPU or across NVLink.
+
+- each rank's weights are bit-exact slices of the unsharded model's tensors
+- the ranks' logits are bit-identical (rank-ordered reduction, redundant
+  gather), and match the CPU oracle's unsharded forward at the same bar as
+  the unsharded pass (test_gpu_kernels.py)
+- decode widths (per-launch skinny GEMM) and prefill widths (tokens-on-M GEMM)
+- KV rollback on every rank, then a greedy chain equal to the unsharded one
+"""
+import numpy as np
+import pytest
+
+from oracle.llama import OracleLlama
+from paper_2503_00784_b200 import SHAPES, Target
+
+pytestmark = pytest.mark.gpu
+
+# GQA like the 70B shape (8 q heads per kv head there, 2 here), small enough
+# for the oracle; per rank: 4 q heads, 2 kv heads, 768 FFN features
+TP_SHAPE = dict(n_layers=2, d_model=512, n_heads=8, n_kv_heads=4, head_dim=64, ffn_dim=1536,
+                vocab=32000, rms_eps=1e-5, rope_theta=1e4)
+PLANT = dict(plant_seed=7, alpha=0.5, gain=1.0, emb_std=1.0)
+SEED = 31
+
+
+@pytest.fixture(scope="module")
+def group():
+    ranks = [Target(TP_SHAPE, weight_seed=SEED, plant=PLANT, max_seq=512, tp_rank=r, tp_size=2)
+             for r in range(2)]
+    Target.tp_connect_local(ranks)
+    full = Target(TP_SHAPE, weight_seed=SEED, plant=PLANT, max_seq=512)
+    yield ranks, full
+    for t in ranks + [full]:
+        t.close()
+
+
+def each(ranks, fn):
+    for t in ranks:
+        fn(t)
+
+
+def test_rank_weights_are_slices(group):
+    ranks, full = group
+    d, hd = TP_SHAPE["d_model"], TP_SHAPE["head_dim"]
+    qd, kvd, F = TP_SHAPE["n_heads"] * hd, TP_SHAPE["n_kv_heads"] * hd, TP_SHAPE["ffn_dim"]
+    qkv = full.read_weights(2, 1, (qd + 2 * kvd) * d).reshape(qd + 2 * kvd, d)
+    o = full.read_weights(3, 1, d * qd).reshape(d, qd)
+    gu = full.read_weights(4, 1, 2 * F * d).reshape(2 * F, d)
+    dn = full.read_weights(5, 1, d * F).reshape(d, F)
+    head = full.read_weights(1, 0, TP_SHAPE["vocab"] * d).reshape(-1, d)
+    q2, k2, f2 = qd // 2, kvd // 2, F // 2
+    v0 = 0
+    for r, t in enumerate(ranks):
+        lq = t.read_weights(2, 1, (q2 + 2 * k2) * d).reshape(-1, d)
+        want = np.concatenate([qkv[r * q2:(r + 1) * q2], qkv[qd + r * k2:qd + (r + 1) * k2],
+                               qkv[qd + kvd + r * k2:qd + kvd + (r + 1) * k2]])
+        assert np.array_equal(lq, want)
+        assert np.array_equal(t.read_weights(3, 1, d * q2).reshape(d, q2), o[:, r * q2:(r + 1) * q2])
+        lg = t.read_weights(4, 1, 2 * f2 * d).reshape(2 * f2, d)
+        assert np.array_equal(lg[:f2], gu[r * f2:(r + 1) * f2])
+        assert np.array_equal(lg[f2:], gu[F + r * f2:F + (r + 1) * f2])
+        assert np.array_equal(t.read_weights(5, 1, d * f2).reshape(d, f2), dn[:, r * f2:(r + 1) * f2])
+        rows = 128 * (250 * (r + 1) // 2) - v0
+        assert np.array_equal(t.read_weights(1, 0, rows * d).reshape(rows, d), head[v0:v0 + rows])
+        v0 += rows
+    assert v0 == TP_SHAPE["vocab"]
+
+
+@pytest.mark.parametrize("w", [1, 8, 17, 64])
+def test_tp_logits_vs_oracle(group, w):
+    ranks, _ = group
+    rng = np.random.default_rng(100 + w)
+    prompt = rng.integers(0, TP_SHAPE["vocab"], 40).tolist()
+    new = rng.integers(0, TP_SHAPE["vocab"], w).tolist()
+    each(ranks, lambda t: t.truncate(0))
+    each(ranks, lambda t: t.prefill(prompt))
+    each(ranks, lambda t: t.score(new))
+    g0, g1 = ranks[0].logits(0, w), ranks[1].logits(0, w)
+    assert np.array_equal(g0, g1), "ranks disagree"
+    orc = OracleLlama(TP_SHAPE, weight_seed=SEED, plant=PLANT, max_seq=512, threads=8)
+    orc.forward(prompt)
+    o = orc.forward(new)
+    orc.close()
+    rel = np.abs(g0 - o).max() / np.abs(o).max()
+    assert rel < 2e-3, f"relative logit error {rel}"
+    assert (g0.argmax(-1) == o.argmax(-1)).mean() >= 0.85
+
+
+def test_tp_rollback_and_greedy_chain(group):
+    ranks, full = group
+    rng = np.random.default_rng(7)
+    prompt = rng.integers(0, TP_SHAPE["vocab"], 24).tolist()
+    junk = rng.integers(0, TP_SHAPE["vocab"], 5).tolist()
+    chains = []
+    for grp in (ranks, [full]):
+        each(grp, lambda t: t.truncate(0))
+        each(grp, lambda t: t.prefill(prompt[:-1]))
+        each(grp, lambda t: t.score(junk))  # rejected tail: rolled back below
+        each(grp, lambda t: t.truncate(len(prompt) - 1))
+        tok, chain, margins = prompt[-1], [], []
+        for _ in range(12):
+            each(grp, lambda t: t.score([tok]))
+            lg = grp[0].logits(0, 1)[0]
+            if len(grp) > 1:
+                assert np.array_equal(lg, grp[1].logits(0, 1)[0])
+            s = np.sort(lg)
+            margins.append(s[-1] - s[-2])
+            tok = int(lg.argmax())
+            chain.append(tok)
+        chains.append((chain, margins))
+        assert all(t.kv_len() == len(prompt) - 1 + 12 for t in grp)
+    (a, ma), (b, _) = chains
+    for i in range(len(a)):
+        if ma[i] < 2e-3:
+            break
+        assert a[i] == b[i], f"position {i}"
