@@ -287,6 +287,11 @@ typedef struct dd_generation_result { /* GenerationResult (engine.hpp:72-78) */
  * may be NULL for vanilla).  prompt is a host buffer. */
 int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
                   const int32_t* prompt, int n_prompt, dd_generation_result* out);
+/* The same generation on a connected tensor-parallel group driven by one
+ * process (ctxs[r] is rank r): every pass is issued to all ranks, acceptance
+ * runs on rank 0, rollback on all.  Needs a fixed budget policy. */
+int dd_engine_run_tp(dd_ctx* const* ctxs, int n, dd_draft* draft, const dd_engine_config* cfg,
+                     const int32_t* prompt, int n_prompt, dd_generation_result* out);
 
 /* calibrate(): median GPU scored pass at probe_len over median CPU draft
  * token; *budget = choose_budget(c) capped at hard_cap. */

@@ -352,9 +352,12 @@ class GenerationResult:
     device_ttft_ms: float = 0.0
 
 
-def run_generation(target: Target, draft: Optional[Draft], prompt: Sequence[int],
+def run_generation(target, draft: Optional[Draft], prompt: Sequence[int],
                    config: EngineConfig) -> GenerationResult:
-    """run_generation (proj/src/engine.cpp:514-532) through dd_engine_run."""
+    """run_generation (proj/src/engine.cpp:514-532) through dd_engine_run.
+
+    `target` is a Target, or the rank-ordered list of a connected
+    tensor-parallel group driven by this process (dd_engine_run_tp)."""
     p = _i32(prompt)
     cap = config.max_new_tokens + config.budget_hard_cap + 8
     toks = np.zeros(cap, dtype=np.int32)
@@ -365,8 +368,13 @@ def run_generation(target: Target, draft: Optional[Draft], prompt: Sequence[int]
     r.iterations = iters
     r.max_iterations = cap
     cfg = config.to_c()
-    _check(_L.lib().dd_engine_run(target.h, draft.h if draft else None, C.byref(cfg), _i32p(p),
-                                  len(p), C.byref(r)), target.h)
+    if isinstance(target, (list, tuple)):
+        arr = (C.c_void_p * len(target))(*[t.h.value for t in target])
+        _check(_L.lib().dd_engine_run_tp(arr, len(target), draft.h if draft else None,
+                                         C.byref(cfg), _i32p(p), len(p), C.byref(r)), target[0].h)
+    else:
+        _check(_L.lib().dd_engine_run(target.h, draft.h if draft else None, C.byref(cfg),
+                                      _i32p(p), len(p), C.byref(r)), target.h)
     out = GenerationResult(tokens=[int(x) for x in toks[:r.n_tokens]], ttft_ms=r.ttft_ms,
                            total_ms=r.total_ms, tps=r.tps, prefill_ms=r.prefill_ms,
                            budget=r.budget_used, device_ms=r.device_ms, h2d_bytes=r.h2d_bytes,

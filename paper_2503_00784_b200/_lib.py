@@ -113,6 +113,8 @@ SIGNATURES = {
     "dd_draft_time_token": (C.c_int, [_vp, C.c_int, _f32p]),
     "dd_engine_run": (C.c_int, [_vp, _vp, C.POINTER(EngineConfigC), _i32p, C.c_int,
                                 C.POINTER(GenerationResultC)]),
+    "dd_engine_run_tp": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.POINTER(EngineConfigC), _i32p,
+                                   C.c_int, C.POINTER(GenerationResultC)]),
     "dd_calibrate": (C.c_int, [_vp, _vp, C.c_int, C.c_int, C.c_int, _f64p,
                                C.POINTER(C.c_int)]),
 }

@@ -207,7 +207,8 @@ struct Channel {
 };
 
 struct Runner {
-    dd_ctx* ctx;
+    dd_ctx* ctx;                // rank 0: acceptance, timing
+    std::vector<dd_ctx*> ranks;  // every tensor-parallel rank (ranks[0] == ctx)
     dd_draft* draft;
     dd_engine_config cfg;
     int V = 0;
@@ -237,7 +238,21 @@ struct Runner {
         return p;
     }
 
-    void truncate_cache() { ck(dd_kv_truncate(ctx, static_cast<int>(verified.size()) - 1), ctx); }
+    // Every rank runs the same passes; each call only enqueues (the ranks'
+    // reductions meet on the devices), so issuing them in rank order is safe.
+    void score(const std::vector<int32_t>& pass) {
+        for (dd_ctx* r : ranks) ck(dd_score(r, pass.data(), static_cast<int>(pass.size())), r);
+    }
+    void truncate_all(int n) {
+        for (dd_ctx* r : ranks) ck(dd_kv_truncate(r, n), r);
+    }
+    void prefill(const int32_t* tokens, int n) {  // chunk-major: no rank runs ahead
+        for (int i = 0; i < n; i += dd::kPrefillChunk) {
+            const int w = std::min(dd::kPrefillChunk, n - i);
+            for (dd_ctx* r : ranks) ck(dd_prefill(r, tokens + i, w), r);
+        }
+    }
+    void truncate_cache() { truncate_all(static_cast<int>(verified.size()) - 1); }
 
     void record(dd_iteration_record r) {
         recs.push_back(r);
@@ -275,8 +290,7 @@ struct Runner {
     void run_vanilla() {  // engine.cpp:273-312
         while (verified.size() - prompt_len < static_cast<size_t>(cfg.max_new_tokens)) {
             const auto t0 = Clock::now();
-            const std::vector<int32_t> pass = first_pass();
-            ck(dd_score(ctx, pass.data(), static_cast<int>(pass.size())), ctx);
+            score(first_pass());
             const dd_verify_out o = verify(DD_MODE_VANILLA, 0, {}, true);
             verified.push_back(o.next_token);
             truncate_cache();
@@ -308,7 +322,7 @@ struct Runner {
             upload_rows(dists, 0);
             std::vector<int32_t> pass{c_token()};
             pass.insert(pass.end(), toks.begin(), toks.end());
-            ck(dd_score(ctx, pass.data(), static_cast<int>(pass.size())), ctx);
+            score(pass);
             const dd_verify_out o = verify(DD_MODE_SPS, budget, {}, cfg.greedy);
             verified.insert(verified.end(), toks.begin(), toks.begin() + o.sps_accepted);
             verified.push_back(o.next_token);
@@ -373,13 +387,13 @@ struct Runner {
                 double comm = 0.0;
                 if (threaded) {
                     ch.post_request(std::move(z));
-                    ck(dd_score(ctx, pass.data(), static_cast<int>(pass.size())), ctx);
+                    score(pass);
                     const auto tw = Clock::now();
                     bundle = ch.wait_reply();  // rendezvous
                     comm = ms_since(tw);
                 } else {
                     bundle = draft_dynamic(dm, z, budget, cfg.max_sequences, rng_draft);
-                    ck(dd_score(ctx, pass.data(), static_cast<int>(pass.size())), ctx);
+                    score(pass);
                 }
                 const auto tv = Clock::now();
                 std::vector<int32_t> firsts;
@@ -479,8 +493,10 @@ int dd_calibrate(dd_ctx* ctx, dd_draft* draft, int probe_len, int trials, int ha
     return DD_OK;
 }
 
-int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
-                  const int32_t* prompt, int n_prompt, dd_generation_result* out) {
+static int engine_run(const std::vector<dd_ctx*>& ranks, dd_draft* draft,
+                      const dd_engine_config* cfg, const int32_t* prompt, int n_prompt,
+                      dd_generation_result* out) {
+    dd_ctx* ctx = ranks[0];
     if (!ctx || !cfg || !prompt || !out || n_prompt < 1) return DD_E_ARG;
     const dd_engine_config& c = *cfg;
     // EngineConfig::validate (engine.cpp:230-249); greedy replaces T > 0
@@ -491,8 +507,11 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
         return ctx_fail(ctx, DD_E_ARG, "invalid engine configuration");
     if (c.mode != DD_MODE_VANILLA && !draft)
         return ctx_fail(ctx, DD_E_ARG, "sps/duo mode requires a draft model");
+    if (ranks.size() > 1 && c.mode != DD_MODE_VANILLA && c.budget_policy == DD_BUDGET_CALIBRATED)
+        return ctx_fail(ctx, DD_E_ARG, "a tensor-parallel group needs a fixed budget");
     Runner r;
     r.ctx = ctx;
+    r.ranks = ranks;
     r.draft = draft;
     r.cfg = c;
     try {
@@ -510,15 +529,15 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
         r.prompt_len = static_cast<size_t>(n_prompt);
         r.rng_draft.seed = c.draft_seed;
         r.rng_verify.seed = c.verify_seed;
-        ctx->h2d_bytes = ctx->d2h_bytes = ctx->launches = 0;
+        for (dd_ctx* k : ranks) k->h2d_bytes = k->d2h_bytes = k->launches = 0;
         ck(ctx_mark(ctx, 0), ctx);
         r.t_start = Clock::now();
-        ck(dd_kv_truncate(ctx, 0), ctx);
+        r.truncate_all(0);
         // SpS drafts before its first pass, so its prefill (overlapping that
         // drafting) stops before c; vanilla and duo score the last prefill chunk.
         int keep = 1;
         if (c.mode != DD_MODE_SPS) keep = (n_prompt - 1) % dd::kPrefillChunk + 1;
-        if (n_prompt > keep) ck(dd_prefill(ctx, prompt, n_prompt - keep), ctx);
+        if (n_prompt > keep) r.prefill(prompt, n_prompt - keep);
         if (keep > 1) r.pending.assign(prompt + n_prompt - keep, prompt + n_prompt);
         out->prefill_ms = 0.0;
         if (c.mode == DD_MODE_VANILLA) {
@@ -535,9 +554,14 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
         ck(ctx_mark(ctx, 1), ctx);
         out->device_ms = ctx_elapsed_ms(ctx, 1);
         out->device_ttft_ms = ctx_elapsed_ms(ctx, 2);
-        out->h2d_bytes = ctx->h2d_bytes + sizeof(int32_t) * static_cast<uint64_t>(n_prompt);
-        out->d2h_bytes = ctx->d2h_bytes;
-        out->gpu_launches = ctx->launches;
+        out->h2d_bytes = sizeof(int32_t) * static_cast<uint64_t>(n_prompt);
+        out->d2h_bytes = 0;
+        out->gpu_launches = 0;
+        for (dd_ctx* k : ranks) {
+            out->h2d_bytes += k->h2d_bytes;
+            out->d2h_bytes += k->d2h_bytes;
+            out->gpu_launches += k->launches;
+        }
         const size_t gen = r.verified.size() - r.prompt_len;
         out->n_tokens = static_cast<int>(gen);
         for (size_t i = 0; i < gen && static_cast<int>(i) < out->max_tokens; ++i)
@@ -555,6 +579,22 @@ int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
     } catch (const std::exception& e) {
         return ctx_fail(ctx, DD_E_STATE, e.what());
     }
+}
+
+int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
+                  const int32_t* prompt, int n_prompt, dd_generation_result* out) {
+    return engine_run({ctx}, draft, cfg, prompt, n_prompt, out);
+}
+
+int dd_engine_run_tp(dd_ctx* const* ctxs, int n, dd_draft* draft, const dd_engine_config* cfg,
+                     const int32_t* prompt, int n_prompt, dd_generation_result* out) {
+    if (!ctxs || n < 1) return DD_E_ARG;
+    std::vector<dd_ctx*> ranks(ctxs, ctxs + n);
+    for (int i = 0; i < n; ++i)
+        if (!ranks[i] || (n > 1 && (ranks[i]->tp_size != n || ranks[i]->tp_rank != i ||
+                                    !ranks[i]->tp_connected)))
+            return ctx_fail(ranks[i], DD_E_ARG, "ctxs[i] must be connected rank i of the group");
+    return engine_run(ranks, draft, cfg, prompt, n_prompt, out);
 }
 
 }  // extern "C"

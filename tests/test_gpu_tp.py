@@ -119,3 +119,53 @@ def test_tp_rollback_and_greedy_chain(group):
         if ma[i] < 2e-3:
             break
         assert a[i] == b[i], f"position {i}"
+
+
+def test_tp_engine_duo_equals_vanilla(group):
+    """Greedy DuoDecoding on the TP group emits exactly the group's own argmax
+    chain (vanilla), token for token: widths do not change the logits."""
+    from paper_2503_00784_b200 import Draft, EngineConfig, run_generation
+    ranks, _ = group
+    drf = Draft(SHAPES["llama_68m"], weight_seed=22, plant=PLANT, threads=4)
+    prompt = np.random.default_rng(4).integers(0, TP_SHAPE["vocab"], 32).tolist()
+    out = {}
+    for mode in ("vanilla", "duo", "sps"):
+        cfg = EngineConfig(mode=mode, budget=5, max_sequences=4, max_new_tokens=32, greedy=True)
+        res = run_generation(ranks, drf if mode != "vanilla" else None, prompt, cfg)
+        out[mode] = res.tokens[:32]
+        assert all(t.kv_len() == ranks[0].kv_len() for t in ranks)
+    drf.close()
+    assert out["duo"] == out["vanilla"]
+    assert out["sps"] == out["vanilla"]
+
+
+def test_tp_two_processes_ipc(tmp_path):
+    """Two rank processes connected through CUDA IPC handles exchanged over
+    gloo (the one-process-per-GPU deployment), here sharing one GPU."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    rng = np.random.default_rng(77)
+    spec = dict(shape=TP_SHAPE, seed=SEED, plant=PLANT,
+                prompt=rng.integers(0, TP_SHAPE["vocab"], 30).tolist(),
+                new=rng.integers(0, TP_SHAPE["vocab"], 6).tolist())
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    worker = Path(__file__).resolve().parent / "tp_ipc_worker.py"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(worker), str(tmp_path),
+           json.dumps(spec)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240,
+                       env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    g0, g1 = (np.load(tmp_path / f"logits_r{i}.npy") for i in range(2))
+    assert np.array_equal(g0, g1)
+    orc = OracleLlama(TP_SHAPE, weight_seed=SEED, plant=PLANT, max_seq=512, threads=8)
+    orc.forward(spec["prompt"])
+    o = orc.forward(spec["new"])
+    orc.close()
+    assert np.abs(g0 - o).max() / np.abs(o).max() < 2e-3
