@@ -935,6 +935,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     if (a.epi.u_out != nullptr) gcol = a.epi.gain[tile * kBlockM + tid];
                 }
                 mbar_wait(&tfull[b], (u >> 1) & 1u);
+                if (tid == 0) pass_stamp(P, p, 4);  // debug: accumulator of the CTA's latest tile ready
                 __syncwarp();
                 tc_fence_after();
                 const uint32_t t_lane =
@@ -967,6 +968,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                             if (tid == 0) {
                                 while (ld_acquire(&a.epi.counters[tile]) < nseg - 1) __nanosleep(32);
                                 a.epi.counters[tile] = 0;
+                                pass_stamp(P, p, 5);  // debug: reducer saw every partial
                             }
                             epi_bar();
                             const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * W * 128 + row;
@@ -988,7 +990,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
 #pragma unroll
                                         for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], pv[k][j]);
                             }
+                            if (tid == 0) pass_stamp(P, p, 8);  // debug: partials summed
                             fast_tile_epilogue(a, s_fe, s_part, tile, acc, xv, gcol, red, tid);
+                            if (tid == 0) pass_stamp(P, p, 9);
                             publish = true;
                         }
                     }
