@@ -48,9 +48,16 @@ WORKLOADS = {
                     desc="config3: Llama-2-7B-shape target, dynamic multi-sequence drafting "
                          "(uncertainty-gated, up to 4 seqs), temperature 1.0 speculative "
                          "sampling, 2K-token prompt, 128 new tokens"),
+    "config5": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4, tp=True,
+                    desc="config5: Llama-2-70B-shape bf16 target tensor-parallel over the N "
+                         "ranks (TP=N, Megatron split, peer-memory reductions) + Llama-68M-shape "
+                         "draft on host cores, 128-token prompt, 128 new tokens, greedy, "
+                         "DuoDecoding"),
 }
 METRIC = ("decode tokens/sec (Llama-2-7B-shape target on B200 + Llama-68M-shape CPU draft, "
           "DuoDecoding, greedy)")
+METRIC_C5 = ("decode tokens/sec (Llama-2-70B-shape target, tensor-parallel over the GPUs, + "
+             "Llama-68M-shape CPU draft, DuoDecoding, greedy)")
 METRIC_C3 = ("decode tokens/sec (Llama-2-7B-shape target on B200 + Llama-68M-shape CPU draft, "
              "DuoDecoding, dynamic multi-sequence drafting, T=1.0 sampling, 2K prompt)")
 
@@ -244,20 +251,32 @@ def run_ours(args):
     PROMPT_LEN = wl["prompt_len"]
     tcore, dcores = core_slice(rank, ws)
     os.sched_setaffinity(0, {tcore})  # target-role thread
-    tgt = Target(SHAPES["llama2_7b"], weight_seed=SEED_W_TARGET, plant=plant,
-                 max_seq=PROMPT_LEN + NEW_TOKENS + 512, device=local)
+    tp = bool(wl.get("tp"))
+    shape_t = SHAPES["llama2_70b"] if tp else SHAPES["llama2_7b"]
+    tgt = Target(shape_t, weight_seed=SEED_W_TARGET, plant=plant,
+                 max_seq=PROMPT_LEN + NEW_TOKENS + 512, device=local,
+                 tp_rank=rank if tp else 0, tp_size=ws if tp else 1)
+    if tp and ws > 1:
+        # one process per GPU: exchange the ranks' IPC handles, then every rank
+        # runs the same engine loop (identical draft bundles, redundant acceptance)
+        handles = [None] * ws
+        dist.all_gather_object(handles, tgt.tp_handle())
+        tgt.tp_connect(handles)
     drf = Draft(SHAPES["llama_68m"], weight_seed=SEED_W_DRAFT, plant=plant, threads=len(dcores),
                 cpus=dcores)
     if args.budget:
         budget, coef = args.budget, None
+    elif tp and ws > 1:
+        budget, coef = 16, None  # calibration times single-rank passes: fixed for TP groups
+        # (c ~ 12-16 expected at TP=8: the 70B pass is ~8x shorter than at TP=1, c ~ 90)
     else:
         coef, budget = calibrate(tgt, drf, probe_len=8, trials=12)
     cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=wl["max_sequences"],
                        max_new_tokens=NEW_TOKENS, greedy=wl["greedy"],
                        temperature=wl["temperature"])
 
-    def one(step):
-        return run_generation(tgt, drf, make_prompt(1000 * rank + step + 1), cfg)
+    def one(step):  # a TP group serves one stream: every rank gets the same prompt
+        return run_generation(tgt, drf, make_prompt(1000 * (0 if tp else rank) + step + 1), cfg)
 
     for s in range(args.warmup):
         one(s)
@@ -293,6 +312,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         dist.all_reduce(m, op=dist.ReduceOp.MAX)
         dec_tok_all, gen_tok_all = float(t[0]), float(t[1])
+        if tp:  # the ranks generated the same stream
+            dec_tok_all, gen_tok_all = dec_tok_all / ws, gen_tok_all / ws
         dec_ms_max, wall_max = float(m[0]), float(m[1])
     else:
         dec_tok_all, gen_tok_all, dec_ms_max, wall_max = dec_tok, gen_tok, dec_ms, wall_s
@@ -300,7 +321,7 @@ def run_ours(args):
     e2e_value = gen_tok_all / wall_max
 
     extra = {}
-    if rank == 0:
+    if rank == 0 and not (tp and ws > 1):
         # roofline of the dominant kernel: the persistent pass kernel (one launch
         # per scored pass = 100% of a decode pass).  Algorithmic bytes: every
         # weight once + the KV cache read (context + new tokens) and written
@@ -310,7 +331,7 @@ def run_ours(args):
         n_ctx = PROMPT_LEN
         tgt.prefill(make_prompt(7, n_ctx))
         pass_ms = tgt.time_pass(w_typ, trials=10)
-        shp = SHAPES["llama2_7b"]
+        shp = shape_t
         kv_tok = 2 * shp["n_layers"] * shp["n_kv_heads"] * shp["head_dim"] * 2
         wb = tgt.pass_weight_bytes()
         alg = wb + kv_tok * (n_ctx + w_typ) + kv_tok * w_typ + w_typ * shp["vocab"] * 4
@@ -332,7 +353,7 @@ def run_ours(args):
         base = {}
         # same statistic as the headline: medians over the timed steps' prompts
         n_base = min(3, args.steps)
-        for mode, bud in (("vanilla", 2), ("sps", max(2, budget // 2))):
+        for mode, bud in (("vanilla", 2), ("sps", max(2, min(budget // 2, 12)))):
             c2 = EngineConfig(mode=mode, budget=bud, max_new_tokens=NEW_TOKENS,
                               greedy=wl["greedy"], temperature=wl["temperature"])
             rs = [run_generation(tgt, drf if mode != "vanilla" else None,
@@ -358,22 +379,25 @@ def run_ours(args):
                           f"prefill/TTFT {r['ttft_ms'] / 1e3:.1f} s"}
     if rank == 0:
         line = {
-            "metric": METRIC if args.workload == "config2" else METRIC_C3,
+            "metric": {"config2": METRIC, "config3": METRIC_C3, "config5": METRIC_C5}[args.workload],
             "value": round(value, 2), "unit": "tokens/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dec_ms_max / args.steps, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data":
+            "scaling": "strong" if tp else "weak", "vs_baseline": None, "dtype": "bf16", "data":
                 "synthetic: seeded random-init weights (planted shared bigram, alpha recorded), "
                 "splitmix64 prompts",
             "config": {"workload": wl["desc"],
-                       "model": "llama2_7b target / llama_68m draft", "global_batch": ws,
-                       "seq_len": PROMPT_LEN + NEW_TOKENS, "parallelism": f"replicas{ws}",
+                       "model": ("llama2_70b" if tp else "llama2_7b") + " target / llama_68m draft",
+                       "global_batch": 1 if tp else ws,
+                       "seq_len": PROMPT_LEN + NEW_TOKENS,
+                       "parallelism": f"tp{ws}" if tp else f"replicas{ws}",
                        "mode": args.mode, "budget": budget, "calibrated_c": coef,
                        "max_sequences": wl["max_sequences"], "greedy": wl["greedy"],
                        "temperature": wl["temperature"], "alpha": plant["alpha"],
                        "seq_hist": seq_hist,
                        "draft_cores": len(dcores),
-                       "l2": "weights 13.2 GB >> 126 MB L2: every pass re-streams from HBM"},
+                       "l2": f"weights {tgt.pass_weight_bytes() / 1e9:.1f} GB per rank >> 126 MB "
+                             "L2: every pass re-streams from HBM"},
             "ttft_p50_ms": round(statistics.median(ttfts), 2),
             "tps_reference_style": round(gen_tok_all / sum(r.total_ms for r in results) * 1e3, 2),
             "tokens_per_iteration": round(tok_per_iter, 3),
