@@ -485,7 +485,21 @@ int dd_calibrate(dd_ctx* ctx, dd_draft* draft, int probe_len, int trials, int ha
     int rc = dd_time_pass(ctx, probe_len, trials + 5, &t_ms);
     if (rc) return rc;
     dd_kv_truncate(ctx, n0);
-    rc = dd_draft_time_token(draft, trials, &d_ms);
+    {
+        // time the draft where run_duo runs it: pool thread 0 on the draft's
+        // first core (the caller may be pinned to the target-role core)
+        cpu_set_t saved;
+        const bool pin = !draft->cpus.empty() &&
+                         pthread_getaffinity_np(pthread_self(), sizeof(saved), &saved) == 0;
+        if (pin) {
+            cpu_set_t set;
+            CPU_ZERO(&set);
+            CPU_SET(draft->cpus[0], &set);
+            pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+        }
+        rc = dd_draft_time_token(draft, trials, &d_ms);
+        if (pin) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
+    }
     if (rc) return rc;
     if (d_ms < 1e-6f) return DD_E_STATE;  // DegenerateTiming
     *cost_coefficient = static_cast<double>(t_ms) / static_cast<double>(d_ms);

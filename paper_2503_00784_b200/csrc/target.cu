@@ -90,9 +90,11 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
-    // prefill widths (49..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu);
-    // narrower passes are faster on the skinny stream-K GEMM (measured crossover)
-    const bool wide = w > 48 && w <= 128 && ctx->ws_wide != nullptr;
+    // prefill widths (37..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu);
+    // narrower passes are faster on the skinny stream-K GEMM (measured crossover,
+    // scripts/pass_width_probe.py: equal at 17-32, wide ahead from ~40 on 7B and 70B)
+    static const int wide_min = getenv("DD_WIDE_MIN") ? atoi(getenv("DD_WIDE_MIN")) : 37;
+    const bool wide = w >= wide_min && w <= 128 && ctx->ws_wide != nullptr;
     auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
                     const GemmEpiParams& ep) -> cudaError_t {
         int n_out, k;
@@ -394,7 +396,10 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
 // The persistent pass kernel serves decode widths; wide (prefill) passes are
 // compute-heavier and run as one launch per GEMM / attention, whose
 // 2-CTA-per-SM GEMM keeps more tiles in flight for the epilogue-heavy wide case.
-bool use_pass_kernel(const dd_ctx* ctx, int w) { return ctx->use_pass_kernel && w <= gemm_dev::kChunk; }
+bool use_pass_kernel(const dd_ctx* ctx, int w) {
+    static const int max_w = getenv("DD_PASS_MAXW") ? atoi(getenv("DD_PASS_MAXW")) : gemm_dev::kChunk;
+    return ctx->use_pass_kernel && w <= max_w;
+}
 
 int enqueue_pass(dd_ctx* ctx, int w, bool want_logits, int* kernels) {
     if (use_pass_kernel(ctx, w)) {
