@@ -26,7 +26,7 @@ struct LayerW {
     // all four stored pre-tiled (common.cuh tiled_offset) for 16 KiB bulk loads
 };
 
-constexpr int kPsRing = 4;
+constexpr int kPsRing = 32;  // pinned PassState staging: a 4K-token prefill enqueues without blocking
 
 }  // namespace dd
 
