@@ -138,6 +138,13 @@ __device__ __forceinline__ int v_chunk(int key, int ch) {
 // warp w accumulates O for its quarter of the head dims (mma.sync m16n8k16).
 // Groups merge through global partials; the last-arriving group combines them
 // in group order and publishes the (head, tile) flag.
+// Chunk groups of a (head, query tile) item: up to `cpg` chunks run in one
+// group before the item is split (each extra group costs a partial round trip
+// and the last arriver's combine).
+__device__ __forceinline__ int attn_groups(int n_chunks, int cpg) {
+    return min(kAttnGroups, max(1, (n_chunks + cpg - 1) / cpg));
+}
+
 template <int HD>
 __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_smem, int* s_bcast,
                           int head, int qt, int grp, int epoch, int tid) {
@@ -151,7 +158,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     const int t_hi = min(W, (qt + 1) * 16);
     const int kmax = n0 + t_hi - 1;
     const int n_chunks = kmax / kAttnChunk + 1;
-    const int active = min(n_chunks, kAttnGroups);
+    const int active = attn_groups(n_chunks, P.attn_cpg);
     const int warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, c = lane & 3;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
@@ -223,11 +230,11 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     for (int t = 0; t < NTW; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
     float m_g = -INFINITY, m_g8 = -INFINITY, l_g = 0.f, l_g8 = 0.f;
 
-    for (int i = 0, chunk = grp; chunk < n_chunks; ++i, chunk += kAttnGroups) {
+    for (int i = 0, chunk = grp; chunk < n_chunks; ++i, chunk += active) {
         const int kb = chunk * kAttnChunk;
         const int b = i & 1;
-        if (chunk + kAttnGroups < n_chunks) {
-            stage(chunk + kAttnGroups, b ^ 1);
+        if (chunk + active < n_chunks) {
+            stage(chunk + active, b ^ 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     const int qt = (item / kAttnGroups) % qtiles;
                     const int head = item / (kAttnGroups * qtiles);
                     const int kmax = n0 + min(W, (qt + 1) * 16) - 1;
-                    if (grp > kmax / kAttnChunk) continue;  // no chunk for this group
+                    if (grp >= attn_groups(kmax / kAttnChunk + 1, P.attn_cpg)) continue;  // no chunk for this group
                     if (tid == 0) PASS_DBG(6, p * 100000 + item);
                     if (hd == 128)
                         attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);

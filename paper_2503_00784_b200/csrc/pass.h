@@ -40,6 +40,7 @@ struct PassParams {
     int nt;
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
+    int attn_cpg;  // attention: 64-key chunks per group before an item is split
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 

@@ -367,6 +367,11 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.tmem_buf = tmem_buf_for(p.nt);
     static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 16;
     p.prefetch = env_pf;
+    // up to 6 chunks (384 keys) per attention group: below that the groups'
+    // partial round trip and combine cost more than running the chunks in
+    // sequence (scripts/pass_ab.py with DD_ATTN_CPG)
+    static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 6;
+    p.attn_cpg = env_cpg;
     const int smem = pass_smem_bytes(m, p.nt, &p.stages);
     if (smem < 0) return ctx_fail(ctx, DD_E_ARG, "pass kernel shared memory plan failed");
     p.ps = ctx->d_ps;
