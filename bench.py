@@ -40,11 +40,11 @@ PROMPT_LEN, NEW_TOKENS = 128, 128
 # BASELINE.json configs: config2 (headline) = 128-token prompt, greedy;
 # config3 = 2K-token prompt, temperature 1.0 speculative sampling, up to 4 sequences
 WORKLOADS = {
-    "config2": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4,
+    "config2": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4, hard_cap=16,
                     desc="config2: Llama-2-7B-shape bf16 target on 1 B200 per rank + "
                          "Llama-68M-shape draft on pinned host cores, 128-token prompt, "
                          "128 new tokens, greedy, DuoDecoding"),
-    "config3": dict(prompt_len=2048, greedy=False, temperature=1.0, max_sequences=4,
+    "config3": dict(prompt_len=2048, greedy=False, temperature=1.0, max_sequences=4, hard_cap=16,
                     desc="config3: Llama-2-7B-shape target, dynamic multi-sequence drafting "
                          "(uncertainty-gated, up to 4 seqs), temperature 1.0 speculative "
                          "sampling, 2K-token prompt, 128 new tokens"),
@@ -270,7 +270,11 @@ def run_ours(args):
         budget, coef = 16, None  # calibration times single-rank passes: fixed for TP groups
         # (c ~ 12-16 expected at TP=8: the 70B pass is ~8x shorter than at TP=1, c ~ 90)
     else:
-        coef, budget = calibrate(tgt, drf, probe_len=8, trials=12)
+        # budget_hard_cap (the reference's EngineConfig knob): 16 on the 7B
+        # workloads = the widest pass the persistent pass kernel runs (wider
+        # passes take the per-launch path, +30% per pass); none on the 70B shape,
+        # whose long passes favour long drafts
+        coef, budget = calibrate(tgt, drf, probe_len=8, trials=12, hard_cap=wl.get("hard_cap", 256))
     cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=wl["max_sequences"],
                        max_new_tokens=NEW_TOKENS, greedy=wl["greedy"],
                        temperature=wl["temperature"])
@@ -392,6 +396,7 @@ def run_ours(args):
                        "seq_len": PROMPT_LEN + NEW_TOKENS,
                        "parallelism": f"tp{ws}" if tp else f"replicas{ws}",
                        "mode": args.mode, "budget": budget, "calibrated_c": coef,
+                       "budget_hard_cap": wl.get("hard_cap", 256),
                        "max_sequences": wl["max_sequences"], "greedy": wl["greedy"],
                        "temperature": wl["temperature"], "alpha": plant["alpha"],
                        "seq_hist": seq_hist,

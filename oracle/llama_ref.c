@@ -271,7 +271,7 @@ void orc_llama_free(orc_llama* m) {
  * (paper_2503_00784_b200/csrc/draft.cpp quantize / quantize_acts / qdot_rows);
  * the integer dot products are exact, so logits match bit-for-bit up to the
  * float epilogue order. */
-static orc_qmat quantize_rows(const uint16_t* w, int rows, int cols) {
+static orc_qmat quantize_rows_levels(const uint16_t* w, int rows, int cols, int levels) {
     orc_qmat m;
     m.rows = rows;
     m.cols = cols;
@@ -284,15 +284,18 @@ static orc_qmat quantize_rows(const uint16_t* w, int rows, int cols) {
             const float a = fabsf(bf2f(src[c]));
             if (a > mx) mx = a;
         }
-        const float sc = mx > 0.0f ? mx / 127.0f : 1.0f;
+        const float sc = mx > 0.0f ? mx / (float)levels : 1.0f;
         for (int c = 0; c < cols; ++c) {
             int v = (int)nearbyintf(bf2f(src[c]) / sc);
-            v = v < -127 ? -127 : (v > 127 ? 127 : v);
+            v = v < -levels ? -levels : (v > levels ? levels : v);
             m.q[(size_t)r * cols + c] = (int8_t)v;
         }
         m.scale[r] = sc;
     }
     return m;
+}
+static orc_qmat quantize_rows(const uint16_t* w, int rows, int cols) {
+    return quantize_rows_levels(w, rows, cols, 127);
 }
 
 void orc_llama_set_quant(orc_llama* m, int on) {
@@ -305,7 +308,8 @@ void orc_llama_set_quant(orc_llama* m, int on) {
         Ly->qgu = quantize_rows(Ly->gu, 2 * m->F, m->d);
         Ly->qdn = quantize_rows(Ly->dn, m->d, m->F);
     }
-    m->qhead = quantize_rows(m->head, m->V, m->d);
+    /* the draft's LM head is 4-bit (draft.cpp quantize4) when d is a multiple of 128 */
+    m->qhead = quantize_rows_levels(m->head, m->V, m->d, m->d % 128 == 0 ? 7 : 127);
     m->quant = 1;
 }
 

@@ -98,6 +98,40 @@ QMat quantize(const std::vector<uint16_t>& w, int rows, int cols, SpinPool& pool
     return m;
 }
 
+// W4 head quantisation (Q4Mat): scale = max|w| / 7, values in [-7, 7]
+// (mirrored bit-for-bit by oracle/llama_ref.c quantize_rows with 7 levels).
+Q4Mat quantize4(const std::vector<uint16_t>& w, int rows, int cols, SpinPool& pool) {
+    Q4Mat m;
+    m.rows = rows;
+    m.cols = cols;
+    m.q.resize(static_cast<size_t>(rows) * cols / 2);
+    m.scale.resize(rows);
+    m.rowsum.resize(rows);
+    pool.run([&](int tid, int nt) {
+        const int lo = static_cast<int>(static_cast<int64_t>(rows) * tid / nt);
+        const int hi = static_cast<int>(static_cast<int64_t>(rows) * (tid + 1) / nt);
+        std::vector<int> v(cols);
+        for (int r = lo; r < hi; ++r) {
+            const uint16_t* src = &w[static_cast<size_t>(r) * cols];
+            float mx = 0.0f;
+            for (int c = 0; c < cols; ++c) mx = std::max(mx, std::fabs(bf2f(src[c])));
+            const float sc = mx > 0.0f ? mx / 7.0f : 1.0f;
+            int32_t sum = 0;
+            for (int c = 0; c < cols; ++c) {
+                v[c] = std::max(-7, std::min(7, static_cast<int>(std::nearbyint(bf2f(src[c]) / sc))));
+                sum += v[c];
+            }
+            uint8_t* dst = &m.q[static_cast<size_t>(r) * cols / 2];
+            for (int b = 0; b < cols / 128; ++b)
+                for (int j = 0; j < 64; ++j)
+                    dst[b * 64 + j] = static_cast<uint8_t>((v[b * 128 + j] + 8) | ((v[b * 128 + 64 + j] + 8) << 4));
+            m.scale[r] = sc;
+            m.rowsum[r] = sum;
+        }
+    });
+    return m;
+}
+
 // Per-token symmetric int8 activation quantisation, stored as u8 = q + 128.
 void quantize_acts(SpinPool& pool, const uint16_t* X, int w, int k, std::vector<uint8_t>& xq,
                    std::vector<float>& xs) {
@@ -182,6 +216,62 @@ __attribute__((target("avx512f,avx512bw,avx512vnni"))) void qdot_rows(
         for (; n + 8 <= hi; n += 8) qdot_block<1, 8>(m, xq, xs, t, n, Y);
         for (; n < hi; ++n) qdot_block<1, 1>(m, xq, xs, t, n, Y);
     }
+}
+
+__attribute__((target("avx512f,avx512bw,avx512vnni"), always_inline)) inline void q4_finish(
+    const Q4Mat& m, int n, __m512i acc, int32_t xsum, float xs, float* Y) {
+    const int32_t dot = _mm512_reduce_add_epi32(acc) - 8 * xsum - 128 * m.rowsum[n];
+    Y[n] = static_cast<float>(dot) * (xs * m.scale[n]);
+}
+
+// One token against the W4 head.  With u8 activations a = q + 128 and
+// offset-binary weights b = w + 8, dpbusd sums a.b = q.w + 8 sum(q) + 128 sum(w)
+// + 1024 k, so q.w = a.b - 8 sum(a) - 128 sum(w): exact integers.
+__attribute__((target("avx512f,avx512bw,avx512vnni"))) void qdot4_rows(
+    const Q4Mat& m, const uint8_t* xq, float xs, int32_t xsum, int lo, int hi, float* Y) {
+    const int nb = m.cols / 128;
+    const size_t rb = static_cast<size_t>(m.cols) / 2;
+    const __m512i mask = _mm512_set1_epi8(0x0F);
+    int n = lo;
+    for (; n + 8 <= hi; n += 8) {
+        __m512i acc[8];
+#pragma GCC unroll 8
+        for (int r = 0; r < 8; ++r) acc[r] = _mm512_setzero_si512();
+        for (int b = 0; b < nb; ++b) {
+            const __m512i x0 = _mm512_loadu_si512(xq + b * 128), x1 = _mm512_loadu_si512(xq + b * 128 + 64);
+#pragma GCC unroll 8
+            for (int r = 0; r < 8; ++r) {
+                const __m512i v = _mm512_loadu_si512(&m.q[(n + r) * rb + b * 64]);
+                acc[r] = _mm512_dpbusd_epi32(acc[r], x0, _mm512_and_si512(v, mask));
+                acc[r] = _mm512_dpbusd_epi32(acc[r], x1, _mm512_and_si512(_mm512_srli_epi16(v, 4), mask));
+            }
+        }
+#pragma GCC unroll 8
+        for (int r = 0; r < 8; ++r) q4_finish(m, n + r, acc[r], xsum, xs, Y);
+    }
+    for (; n < hi; ++n) {
+        __m512i acc = _mm512_setzero_si512();
+        for (int b = 0; b < nb; ++b) {
+            const __m512i v = _mm512_loadu_si512(&m.q[n * rb + b * 64]);
+            acc = _mm512_dpbusd_epi32(acc, _mm512_loadu_si512(xq + b * 128), _mm512_and_si512(v, mask));
+            acc = _mm512_dpbusd_epi32(acc, _mm512_loadu_si512(xq + b * 128 + 64),
+                                      _mm512_and_si512(_mm512_srli_epi16(v, 4), mask));
+        }
+        q4_finish(m, n, acc, xsum, xs, Y);
+    }
+}
+
+void matmul4(SpinPool& pool, const Q4Mat& m, const uint16_t* x, float* Y, std::vector<uint8_t>& xq,
+             std::vector<float>& xs) {
+    quantize_acts(pool, x, 1, m.cols, xq, xs);
+    int32_t xsum = 0;
+    for (int i = 0; i < m.cols; ++i) xsum += xq[i];
+    const int blocks = (m.rows + 7) / 8;
+    pool.run([&](int tid, int nt) {
+        const int lo = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * tid / nt) * 8);
+        const int hi = std::min(m.rows, static_cast<int>(static_cast<int64_t>(blocks) * (tid + 1) / nt) * 8);
+        if (lo < hi) qdot4_rows(m, xq.data(), xs[0], xsum, lo, hi, Y);
+    });
 }
 
 void matmul(SpinPool& pool, const QMat& m, const uint16_t* X, int w, float* Y,
@@ -291,7 +381,12 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
                 head_bf[e] = f2bf(w);
             }
         });
-        head_ = quantize(head_bf, V_, d_, *pool_);
+        head_w4_ = d_ % 128 == 0;
+        if (head_w4_) {
+            head4_ = quantize4(head_bf, V_, d_, *pool_);
+        } else {
+            head_ = quantize(head_bf, V_, d_, *pool_);
+        }
     }
     layers_.resize(L_);
     for (int l = 0; l < L_; ++l) {
@@ -584,7 +679,11 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);
         });
     }
-    matmul(*pool_, head_, &hb_[(W - 1) * d_], 1, logits_last, xq_, xs_);
+    if (head_w4_) {
+        matmul4(*pool_, head4_, &hb_[(W - 1) * d_], logits_last, xq_, xs_);
+    } else {
+        matmul(*pool_, head_, &hb_[(W - 1) * d_], 1, logits_last, xq_, xs_);
+    }
     for (int i = 0; i < V_; ++i) logits_last[i] *= rn[W - 1];
     tokens_.insert(tokens_.end(), toks, toks + w);
 }
@@ -742,19 +841,22 @@ int dd_draft_logits(dd_draft* d, const int32_t* ctx_tokens, int n, float* logits
 
 int dd_draft_time_token(dd_draft* d, int trials, float* median_ms) {
     if (!d || !median_ms || trials < 1) return DD_E_ARG;
-    // calibrate()'s denominator: one single-token forward (engine.cpp:559-561),
-    // measured as the incremental cost of one token on a 8-token context
-    std::vector<int32_t> ctx(9, 0);
+    // calibrate()'s denominator: the cost of one single-token forward
+    // (engine.cpp:559-561), measured the way drafting runs them - a run of 8
+    // consecutive tokens after an 8-token context, per-token mean - so the pool
+    // threads are as warm as in draft_dynamic; median over the trials
+    constexpr int kRun = 8;
+    std::vector<int32_t> ctx(8 + kRun, 0);
     std::vector<float> lg(d->model->vocab());
     std::vector<double> ms;
-    for (int i = 0; i < 5 + trials; ++i) {
-        ctx.back() = i % 7 + 1;
+    for (int i = 0; i < 3 + trials; ++i) {
+        for (int j = 0; j < kRun; ++j) ctx[8 + j] = (i * kRun + j) % 7 + 1;
         d->model->logits(ctx.data(), 8, lg.data());  // cache holds 8 tokens
         const auto t0 = std::chrono::steady_clock::now();
-        d->model->logits(ctx.data(), 9, lg.data());  // exactly one new token
+        for (int j = 1; j <= kRun; ++j) d->model->logits(ctx.data(), 8 + j, lg.data());  // one new token each
         const double x =
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        if (i >= 5) ms.push_back(x);
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count() / kRun;
+        if (i >= 3) ms.push_back(x);
     }
     std::sort(ms.begin(), ms.end());
     const size_t n = ms.size();

@@ -42,6 +42,19 @@ struct QMat {
     std::vector<int32_t> rowsum;  // [rows] sum of q
 };
 
+// W4 LM head (the draft's largest matrix, streamed once per drafted token):
+// per-row symmetric 4-bit (scale = max|w| / 7), stored offset-binary (w + 8)
+// two per byte - byte j of the 64-byte block b holds k = 128 b + j in its low
+// and k = 128 b + 64 + j in its high nibble, so one load and two masks give
+// the VNNI operands of two 64-wide activation slices.  Used when cols is a
+// multiple of 128 (else the head stays W8).
+struct Q4Mat {
+    int rows = 0, cols = 0;
+    std::vector<uint8_t> q;       // [rows][cols / 2]
+    std::vector<float> scale;     // [rows]
+    std::vector<int32_t> rowsum;  // [rows] sum of the signed 4-bit values
+};
+
 struct DraftLayer {
     QMat qkv, o, gu, dn;  // row-major [out][in]
 };
@@ -73,6 +86,8 @@ class CpuLlama {
     float eps_;
     std::vector<uint16_t> emb_;
     QMat head_;
+    Q4Mat head4_;
+    bool head_w4_ = false;
     std::vector<DraftLayer> layers_;
     std::vector<uint16_t> kv_;  // K: [L][Hkv][max_seq/16][hd][16] (16-key blocks, dim-major inside), V: [L][Hkv][max_seq][hd]; bf16
     std::vector<float> rope_cos_, rope_sin_;
