@@ -365,7 +365,7 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.n_phases = n;
     p.nt = round_nt(w);
     p.tmem_buf = tmem_buf_for(p.nt);
-    static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 16;
+    static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 4;
     p.prefetch = env_pf;
     // up to 6 chunks (384 keys) per attention group: below that the groups'
     // partial round trip and combine cost more than running the chunks in
