@@ -309,7 +309,9 @@ void orc_llama_set_quant(orc_llama* m, int on) {
         Ly->qdn = quantize_rows(Ly->dn, m->d, m->F);
     }
     /* the draft's LM head is 4-bit (draft.cpp quantize4) when d is a multiple of 128 */
-    m->qhead = quantize_rows_levels(m->head, m->V, m->d, m->d % 128 == 0 ? 7 : 127);
+    const char* hb = getenv("DD_DRAFT_HEAD_BITS");
+    const int w4 = m->d % 128 == 0 && !(hb && atoi(hb) == 8);
+    m->qhead = quantize_rows_levels(m->head, m->V, m->d, w4 ? 7 : 127);
     m->quant = 1;
 }
 

@@ -381,7 +381,8 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
                 head_bf[e] = f2bf(w);
             }
         });
-        head_w4_ = d_ % 128 == 0;
+        const char* hb = getenv("DD_DRAFT_HEAD_BITS");
+        head_w4_ = d_ % 128 == 0 && !(hb && atoi(hb) == 8);
         if (head_w4_) {
             head4_ = quantize4(head_bf, V_, d_, *pool_);
         } else {

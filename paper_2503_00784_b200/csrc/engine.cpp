@@ -497,9 +497,13 @@ int dd_calibrate(dd_ctx* ctx, dd_draft* draft, int probe_len, int trials, int ha
             CPU_SET(draft->cpus[0], &set);
             pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
         }
-        // the first run after the draft's creation measures cold caches and
-        // clocks (+40% on the pool's hosts): time twice, keep the second
-        rc = dd_draft_time_token(draft, trials, &d_ms);
+        // measure the draft in steady state, as run_duo runs it: the first
+        // ~second of drafting after the draft's creation runs up to 40% slower
+        // on the pool's hosts (clocks, caches), so keep drafting for 1 s first
+        const auto t_warm = std::chrono::steady_clock::now();
+        do {
+            rc = dd_draft_time_token(draft, trials, &d_ms);
+        } while (rc == DD_OK && std::chrono::steady_clock::now() - t_warm < std::chrono::seconds(1));
         if (rc == DD_OK) rc = dd_draft_time_token(draft, trials, &d_ms);
         if (pin) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
     }
