@@ -402,7 +402,10 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
 // compute-heavier and run as one launch per GEMM / attention, whose
 // 2-CTA-per-SM GEMM keeps more tiles in flight for the epilogue-heavy wide case.
 bool use_pass_kernel(const dd_ctx* ctx, int w) {
-    static const int max_w = getenv("DD_PASS_MAXW") ? atoi(getenv("DD_PASS_MAXW")) : gemm_dev::kChunk;
+    // DD_PASS_MAXW (A/B knob, <= 64): widths above 16 leave the register-resident
+    // epilogue and run slower than the per-launch path (scripts/pass_width_probe.py)
+    static const int max_w =
+        getenv("DD_PASS_MAXW") ? std::min(64, atoi(getenv("DD_PASS_MAXW"))) : gemm_dev::kChunk;
     return ctx->use_pass_kernel && w <= max_w;
 }
 
