@@ -244,7 +244,7 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", init_method="env://")
     from paper_2503_00784_b200 import (DEFAULT_PLANT, SHAPES, Draft, EngineConfig, Target,
-                                       calibrate, run_generation)
+                                       calibrate, run_generation, tp_connect_group)
     plant = dict(DEFAULT_PLANT, alpha=args.alpha)
     wl = WORKLOADS[args.workload]
     global PROMPT_LEN
@@ -259,9 +259,7 @@ def run_ours(args):
     if tp and ws > 1:
         # one process per GPU: exchange the ranks' IPC handles, then every rank
         # runs the same engine loop (identical draft bundles, redundant acceptance)
-        handles = [None] * ws
-        dist.all_gather_object(handles, tgt.tp_handle())
-        tgt.tp_connect(handles)
+        tp_connect_group(tgt)
     drf = Draft(SHAPES["llama_68m"], weight_seed=SEED_W_DRAFT, plant=plant, threads=len(dcores),
                 cpus=dcores)
     if args.budget:

@@ -22,6 +22,7 @@ __all__ = [
     "StateError",
     "SHAPES", "Target", "Draft", "EngineConfig", "GenerationResult", "IterationRecord",
     "run_generation", "run_vanilla", "run_sps", "run_duo", "calibrate", "choose_budget",
+    "tp_connect_group",
     "ConfigError", "DegenerateTiming", "DeviceError", "DuoError",
 ]
 
@@ -350,6 +351,19 @@ class GenerationResult:
     d2h_bytes: int = 0
     gpu_launches: int = 0
     device_ttft_ms: float = 0.0
+
+
+def tp_connect_group(target, group=None) -> None:
+    """Connect this process's rank of a tensor-parallel group (one process per
+    GPU): all-gather every rank's IPC handle over torch.distributed (any
+    backend) and open them in rank order (include/duodec_b200.h dd_tp_connect)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world != target.tp_size or dist.get_rank(group) != target.tp_rank:
+        raise ConfigError("process group rank / size must match the target's tp_rank / tp_size")
+    handles = [None] * world
+    dist.all_gather_object(handles, target.tp_handle(), group=group)
+    target.tp_connect(handles)
 
 
 def run_generation(target, draft: Optional[Draft], prompt: Sequence[int],
