@@ -13,7 +13,7 @@ import numpy as np
 import torch.distributed as dist
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from paper_2503_00784_b200 import Target  # noqa: E402
+from paper_2503_00784_b200 import Target, tp_connect_group  # noqa: E402
 
 
 def main(out_dir: str, spec: str) -> None:
@@ -23,9 +23,7 @@ def main(out_dir: str, spec: str) -> None:
     dist.init_process_group("gloo", rank=rank, world_size=world)
     t = Target(cfg["shape"], weight_seed=cfg["seed"], plant=cfg["plant"], max_seq=512,
                device=int(os.environ.get("DD_TP_DEVICE", "0")), tp_rank=rank, tp_size=world)
-    handles = [None] * world
-    dist.all_gather_object(handles, t.tp_handle())
-    t.tp_connect(handles)
+    tp_connect_group(t)
     t.prefill(cfg["prompt"])
     t.score(cfg["new"])
     np.save(Path(out_dir) / f"logits_r{rank}.npy", t.logits(0, len(cfg["new"])))
