@@ -970,11 +970,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                             epi_bar();  // every partial store happens-before the release
                             if (tid == 0)
                                 asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
-                                             ::"l"(&a.epi.counters[tile]) : "memory");
+                                             ::"l"(&a.epi.counters[tile * kCounterStride]) : "memory");
                         } else {
                             if (tid == 0) {
-                                while (ld_acquire(&a.epi.counters[tile]) < nseg - 1) __nanosleep(32);
-                                a.epi.counters[tile] = 0;
+                                while (ld_acquire(&a.epi.counters[tile * kCounterStride]) < nseg - 1) __nanosleep(32);
+                                a.epi.counters[tile * kCounterStride] = 0;
                                 pass_stamp(P, p, 5);  // debug: reducer saw every partial
                             }
                             epi_bar();
@@ -1034,7 +1034,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     mbar_arrive(&tempty[b]);
                     epi_bar();
                     if (tid == 0) {  // release this segment's partial, acquire the others'
-                        const int prev = atom_add_acq_rel(&a.epi.counters[tile], 1);
+                        const int prev = atom_add_acq_rel(&a.epi.counters[tile * kCounterStride], 1);
                         s_last = (prev == nseg - 1);
                     }
                     epi_bar();
@@ -1069,7 +1069,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                             apply_epilogue(a, tile, t0, tn, red, tid, s_part);
                             epi_bar();
                         }
-                        if (tid == 0) a.epi.counters[tile] = 0;
+                        if (tid == 0) a.epi.counters[tile * kCounterStride] = 0;
                         publish = true;
                     }
                 }

@@ -67,6 +67,7 @@ struct PassParams {
 constexpr int kPassThreads = 256;
 constexpr int kAttnChunk = 64;    // keys staged per attention step
 constexpr int kAttnGroups = 4;    // chunk groups per (head, query tile)
+constexpr int kCounterStride = 32;  // ints: one 128-byte line per stream-K tile counter
 constexpr int kFlagStride = 32;   // ints: one 128-byte line per flag replica
 constexpr int kFlagReplicas = 8;  // every flag is published to 8 lines; CTA c polls replica c % 8
                                   // (148 pollers on one line serialise in its L2 slice)

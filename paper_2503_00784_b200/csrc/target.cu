@@ -279,7 +279,7 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
         a.max_seg = pass_max_seg(ctx, a.tiles, a.nkb);
         a.tmem_buf = tmem_buf_for(nt);
         a.ws = ctx->pass_ws + (gidx & 1) * ctx->pass_ws_half;
-        ep.counters = ctx->pass_counters + (gidx & 1) * 512;
+        ep.counters = ctx->pass_counters + (gidx & 1) * 512 * kCounterStride;
         a.epi = ep;
         p.out_flag = reserve(a.tiles);
         ++gidx;
@@ -663,8 +663,8 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         }
         ctx->pass_ws_half = half;
         CK(cudaMalloc(&ctx->pass_ws, sizeof(float) * 2 * half));
-        CK(cudaMalloc(&ctx->pass_counters, sizeof(int) * 2 * 512));
-        CK(cudaMemset(ctx->pass_counters, 0, sizeof(int) * 2 * 512));
+        CK(cudaMalloc(&ctx->pass_counters, sizeof(int) * 2 * 512 * kCounterStride));
+        CK(cudaMemset(ctx->pass_counters, 0, sizeof(int) * 2 * 512 * kCounterStride));
         CK(cudaMalloc(&ctx->attn_part, sizeof(float) * pass_attn_part_floats(m)));
         CK(cudaMalloc(&ctx->attn_cnt, sizeof(int) * pass_attn_cnt_ints(m)));
         CK(cudaMemset(ctx->attn_cnt, 0, sizeof(int) * pass_attn_cnt_ints(m)));
