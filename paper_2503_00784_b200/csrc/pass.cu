@@ -962,11 +962,17 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                         // The others store their partial and bump the tile counter with a
                         // fire-and-forget release; the reducer waits for them (normally
                         // already done), adds them in segment order to its own registers.
+                        // partial layout [segment][row][Wp] (Wp = W rounded up to 4): one
+                        // 16-byte store / load per 4 tokens
+                        const int Wp = (W + 3) & ~3;
                         if (seg != 0) {
-                            float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * W * 128;
+                            float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * Wp * 128 +
+                                          static_cast<size_t>(row) * Wp;
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (j < W) part[static_cast<size_t>(j) * 128 + row] = v[j];
+                            for (int q4 = 0; q4 < 4; ++q4)
+                                if (4 * q4 < W)
+                                    reinterpret_cast<float4*>(part)[q4] =
+                                        make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
                             epi_bar();  // every partial store happens-before the release
                             if (tid == 0)
                                 asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
@@ -978,24 +984,31 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                 pass_stamp(P, p, 5);  // debug: reducer saw every partial
                             }
                             epi_bar();
-                            const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * W * 128 + row;
+                            const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * Wp * 128 +
+                                                static_cast<size_t>(row) * Wp;
                             float acc[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) acc[j] = v[j];
                             for (int s0 = 1; s0 < nseg; s0 += 4) {
-                                float pv[4][16];
+                                float4 pv[4][4];
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
 #pragma unroll
-                                    for (int j = 0; j < 16; ++j)
-                                        pv[k][j] = (s0 + k < nseg && j < W)
-                                                       ? __ldcg(base + (static_cast<size_t>(s0 + k) * W + j) * 128)
-                                                       : 0.0f;
+                                    for (int q4 = 0; q4 < 4; ++q4)
+                                        pv[k][q4] = (s0 + k < nseg && 4 * q4 < W)
+                                                        ? __ldcg(reinterpret_cast<const float4*>(
+                                                              base + static_cast<size_t>(s0 + k) * Wp * 128) + q4)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
                                     if (s0 + k < nseg)
 #pragma unroll
-                                        for (int j = 0; j < 16; ++j) acc[j] = __fadd_rn(acc[j], pv[k][j]);
+                                        for (int q4 = 0; q4 < 4; ++q4) {
+                                            acc[4 * q4] = __fadd_rn(acc[4 * q4], pv[k][q4].x);
+                                            acc[4 * q4 + 1] = __fadd_rn(acc[4 * q4 + 1], pv[k][q4].y);
+                                            acc[4 * q4 + 2] = __fadd_rn(acc[4 * q4 + 2], pv[k][q4].z);
+                                            acc[4 * q4 + 3] = __fadd_rn(acc[4 * q4 + 3], pv[k][q4].w);
+                                        }
                             }
                             if (tid == 0) pass_stamp(P, p, 8);  // debug: partials summed
                             fast_tile_epilogue(a, s_fe, s_part, tile, acc, xv, gcol, red, tid);
