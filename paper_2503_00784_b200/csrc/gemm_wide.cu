@@ -24,6 +24,7 @@
 #include "gemm_epi.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace dd {
 
@@ -473,7 +474,14 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 GemmPlan plan_gemm_wide(int n_out, int k) {
     GemmPlan p{};
     // 128-row tiles when 256-row tiles would leave fewer than 64 of them
-    const int nw = (n_out % 256 == 0 && n_out / 256 >= 64) ? 256 : 128;
+    // 128-row weight tiles (measured: 256-row tiles, whose fewer and larger
+    // stream-K partials lengthen the reducers' tails, make a 128-token pass 9%
+    // slower; DD_WIDE_NW=256 restores them where n_out allows)
+    static const int env_nw = getenv("DD_WIDE_NW") ? atoi(getenv("DD_WIDE_NW")) : 128;
+    // CTAs for the d_model-output GEMMs (32 tiles): 96 = exactly 3 stream-K
+    // segments per tile (64: 2 per tile but 57% of the SMs stream; 148: ragged)
+    static const int env_small = getenv("DD_WIDE_SMALL_CTAS") ? atoi(getenv("DD_WIDE_SMALL_CTAS")) : 96;
+    const int nw = (env_nw == 256 && n_out % 256 == 0) ? 256 : 128;
     p.tiles = n_out / nw;
     p.nkb = k / kBlockK;
     const long T = static_cast<long>(p.tiles) * p.nkb;
@@ -483,7 +491,11 @@ GemmPlan plan_gemm_wide(int n_out, int k) {
     p.tmem_cols = 2 * nw;
     // the 4096-output GEMMs have only 32 row tiles: fewer CTAs keep their
     // stream-K segments per tile (and the last arriver's reduction) short
-    p.ctas = static_cast<int>(std::min<long>(p.tiles >= 64 ? kNumSMs : 64, T));
+    static const int env_big = getenv("DD_WIDE_BIG_CTAS") ? atoi(getenv("DD_WIDE_BIG_CTAS")) : 0;
+    int big = kNumSMs;
+    if (env_big == -1) big = p.tiles / ((p.tiles + kNumSMs - 1) / kNumSMs);  // whole tiles per CTA
+    else if (env_big > 0) big = env_big;
+    p.ctas = static_cast<int>(std::min<long>(p.tiles >= 64 ? big : env_small, T));
     int ms = 1;
     for (int t = 0; t < p.tiles; ++t) {
         const int f = gemm_dev::sk_owner(static_cast<long>(t) * p.nkb, T, p.ctas);

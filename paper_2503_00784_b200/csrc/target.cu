@@ -90,10 +90,10 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.page_table = ctx->page_table;
     e.page_size = ctx->page_size;
     e.m = m;
-    // prefill widths (37..128 tokens) run the tokens-on-M GEMM (gemm_wide.cu);
-    // narrower passes are faster on the skinny stream-K GEMM (measured crossover,
-    // scripts/pass_width_probe.py: equal at 17-32, wide ahead from ~40 on 7B and 70B)
-    static const int wide_min = getenv("DD_WIDE_MIN") ? atoi(getenv("DD_WIDE_MIN")) : 37;
+    // passes of 17..128 tokens run the tokens-on-M GEMM (gemm_wide.cu), ahead of
+    // the skinny stream-K GEMM at every width above 16 with 128-row tiles
+    // (scripts/wide_crossover.py: 4.29 vs 4.65 ms at 17, 4.69 vs 5.99 at 40)
+    static const int wide_min = getenv("DD_WIDE_MIN") ? atoi(getenv("DD_WIDE_MIN")) : 17;
     const bool wide = w >= wide_min && w <= 128 && ctx->ws_wide != nullptr;
     auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx,
                     const GemmEpiParams& ep) -> cudaError_t {
