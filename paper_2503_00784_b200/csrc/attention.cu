@@ -103,7 +103,10 @@ void attention_set_trace(unsigned long long* p) { cudaMemcpyToSymbol(g_attn_trac
     } while (0)
 #endif
 
-template <int HD>
+// RANKS = CTAs per (head, query tile): kRanks (a cluster, split-KV + DSMEM
+// merge) for long contexts, 1 (every split in sequence, no merge) when the
+// context fits in two splits.
+template <int HD, int RANKS>
 __global__ void __launch_bounds__(kAttnCtaThreads)
     attn_cluster_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
                         const __nv_bfloat16* __restrict__ kv_pool,
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
     ATT_STAMP(0);
     pdl_wait_();
     pdl_launch_();
-    const int rank = static_cast<int>(cluster_ctarank());
+    const int rank = RANKS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     const int qt = blockIdx.y, head = blockIdx.z;
     const int n0 = ps->n_cached, W = ps->w;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
             qb[ch][3] = pack_bf16(b1.z, b1.w);
         }
 #pragma unroll 1
-        for (int split = rank; split < n_split; split += kRanks) {
+        for (int split = rank; split < n_split; split += RANKS) {
             const int kb = split * kSplitKeys;
             // ---- stage the split's K and V (zero-filled past kmax)
 #pragma unroll 4
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
     }
     // C fragment column 2c (2c+1) of n-tile e -> dim warp*DW + (2c)*NTW + e
     const int dcol = warp * DW + 2 * c * NTW;
-    if (n_split <= 1) {  // uniform over the cluster: rank 0 alone finishes
-        if (rank == 0 && n_split == 1) {
+    if (RANKS == 1 || n_split <= 1) {  // uniform over the cluster: rank 0 alone finishes
+        if (rank == 0 && n_split >= 1) {
             const float ig = 1.0f / l_g, ig8 = 1.0f / l_g8;
             const size_t og = static_cast<size_t>(qt * kQTile + g) * qd + head * HD;
             const size_t og8 = og + static_cast<size_t>(8) * qd;
@@ -303,6 +306,7 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
         }
         return;
     }
+    if constexpr (RANKS > 1) {
     // ---- cluster merge (rank order) through DSMEM; rank r finishes rows r, r + 8
 #pragma unroll
     for (int e = 0; e < NTW; ++e) {
@@ -359,16 +363,18 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
     ATT_STAMP(6);
     cluster_sync();  // keep this CTA's shared memory alive until every rank has read it
     ATT_STAMP(7);
+    }
 }
 
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                     int layer, __nv_bfloat16* o, cudaStream_t s) {
+                     int layer, __nv_bfloat16* o, cudaStream_t s, int ranks) {
     const int qtiles = (w + kQTile - 1) / kQTile;
     const float scale_log2 =
         static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(m.head_dim)));
+    const bool cluster = ranks > 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kRanks, qtiles, m.n_heads);
+    cfg.gridDim = dim3(cluster ? kRanks : 1, qtiles, m.n_heads);
     cfg.blockDim = dim3(kAttnCtaThreads, 1, 1);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -377,28 +383,24 @@ int launch_attention(const PassState* ps, int w, const ModelDims& m, const float
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cluster ? 1 : 0;
+    auto go = [&](auto kernel, size_t smem, bool& attr) {
+        cfg.dynamicSmemBytes = smem;
+        if (!attr) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr = true;
+        }
+        return cudaLaunchKernelEx(&cfg, kernel, ps, m, q, kv_pool, page_table, page_size, layer,
+                                  scale_log2, o);
+    };
     cudaError_t e;
+    static bool a128c = false, a128s = false, a64c = false, a64s = false;
     if (m.head_dim == 128) {
-        static bool attr = false;
-        cfg.dynamicSmemBytes = sizeof(AttnSmem<128>);
-        if (!attr) {
-            cudaFuncSetAttribute(attn_cluster_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(AttnSmem<128>)));
-            attr = true;
-        }
-        e = cudaLaunchKernelEx(&cfg, attn_cluster_kernel<128>, ps, m, q, kv_pool, page_table,
-                               page_size, layer, scale_log2, o);
+        e = cluster ? go(attn_cluster_kernel<128, kRanks>, sizeof(AttnSmem<128>), a128c)
+                    : go(attn_cluster_kernel<128, 1>, sizeof(AttnSmem<128>), a128s);
     } else if (m.head_dim == 64) {
-        static bool attr = false;
-        cfg.dynamicSmemBytes = sizeof(AttnSmem<64>);
-        if (!attr) {
-            cudaFuncSetAttribute(attn_cluster_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(AttnSmem<64>)));
-            attr = true;
-        }
-        e = cudaLaunchKernelEx(&cfg, attn_cluster_kernel<64>, ps, m, q, kv_pool, page_table,
-                               page_size, layer, scale_log2, o);
+        e = cluster ? go(attn_cluster_kernel<64, kRanks>, sizeof(AttnSmem<64>), a64c)
+                    : go(attn_cluster_kernel<64, 1>, sizeof(AttnSmem<64>), a64s);
     } else {
         return -1;
     }

@@ -61,7 +61,7 @@ void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, con
 // returns 0, or nonzero for an unsupported head_dim / launch failure.
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                     int layer, __nv_bfloat16* o, cudaStream_t s);
+                     int layer, __nv_bfloat16* o, cudaStream_t s, int ranks = 8);
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s);
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,

@@ -61,6 +61,18 @@ void gemm_shape(const dd_ctx* c, int id, int* n_out, int* k) {
     }
 }
 
+// CTAs per (head, query tile) of the per-launch attention kernel: one CTA
+// walking the 128-key splits in sequence (no cluster merge, 1/8 of the CTAs)
+// when the (head, query tile) pairs alone fill the GPU or the context spans at
+// most DD_ATTN_SINGLE_MAX splits; else a cluster of 8 with a DSMEM merge
+// (measured: 2K-token prefill 124 -> 101 ms, 128-token pass 5.33 -> 4.87 ms).
+int attn_ranks(const dd_ctx* c, int w) {
+    static const int single_max = getenv("DD_ATTN_SINGLE_MAX") ? atoi(getenv("DD_ATTN_SINGLE_MAX")) : 2;
+    const int splits = (c->n_cached + w - 1) / 128 + 1;
+    const int items = (w + 15) / 16 * c->m.n_heads;
+    return (splits <= single_max || items >= 128) ? 1 : 8;
+}
+
 const GemmPlan& plan_for(dd_ctx* c, int id, int nt) {
     auto key = id * 1000 + nt;
     auto it = c->plans.find(key);
@@ -148,7 +160,7 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         eq.layer = l;
         CK(gemm(kGQkv, L.qkv, &ctx->map_h, eq));
         if (launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table,
-                             ctx->page_size, l, ctx->o, s))
+                             ctx->page_size, l, ctx->o, s, attn_ranks(ctx, w)))
             return ctx_fail(ctx, DD_E_CUDA, "attention launch failed");
         mark(1);
         GemmEpiParams er = e;  // residual add; writes u = bf16(x*g) + ss partials
@@ -459,7 +471,9 @@ int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
     ctx->h2d_bytes += offsetof(PassState, tokens) + sizeof(int32_t) * w;
     CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
     if (ctx->use_graphs) {
-        const int key = w * 2 + (want_logits ? 1 : 0);
+        // per-launch passes bake the attention CTA layout (context-dependent) into the graph
+        const int key = (w * 2 + (want_logits ? 1 : 0)) * 2 +
+                        (!use_pass_kernel(ctx, w) && attn_ranks(ctx, w) == 1 ? 1 : 0);
         auto it = ctx->graphs.find(key);
         if (it == ctx->graphs.end()) {
             if (use_pass_kernel(ctx, w)) {  // device phase table: allocated outside the capture
