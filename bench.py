@@ -48,7 +48,7 @@ WORKLOADS = {
                     desc="config3: Llama-2-7B-shape target, dynamic multi-sequence drafting "
                          "(uncertainty-gated, up to 4 seqs), temperature 1.0 speculative "
                          "sampling, 2K-token prompt, 128 new tokens"),
-    "config5": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4, tp=True,
+    "config5": dict(prompt_len=128, greedy=True, temperature=1.0, max_sequences=4, tp=True, hard_cap=127,
                     desc="config5: Llama-2-70B-shape bf16 target tensor-parallel over the N "
                          "ranks (TP=N, Megatron split, peer-memory reductions) + Llama-68M-shape "
                          "draft on host cores, 128-token prompt, 128 new tokens, greedy, "
@@ -270,8 +270,9 @@ def run_ours(args):
     else:
         # budget_hard_cap (the reference's EngineConfig knob): 16 on the 7B
         # workloads = the widest pass the persistent pass kernel runs (wider
-        # passes take the per-launch path, +30% per pass); none on the 70B shape,
-        # whose long passes favour long drafts
+        # passes take the per-launch path, +30% per pass); 127 on the 70B shape
+        # (long passes favour long drafts; 128 tokens is the widest pass of the
+        # tokens-on-M GEMM)
         coef, budget = calibrate(tgt, drf, probe_len=8, trials=12, hard_cap=wl.get("hard_cap", 256))
     cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=wl["max_sequences"],
                        max_new_tokens=NEW_TOKENS, greedy=wl["greedy"],
