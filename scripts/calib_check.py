@@ -1,5 +1,6 @@
+"""calibrate() on the 7B target and the 68M draft pinned to 12 host cores: c and the budget."""
 import sys, os
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 from paper_2503_00784_b200 import SHAPES, DEFAULT_PLANT, Target, Draft, calibrate
 t = Target(SHAPES["llama2_7b"], weight_seed=1234, plant=DEFAULT_PLANT, max_seq=1024)
 cpus = sorted(os.sched_getaffinity(0))[1:13]

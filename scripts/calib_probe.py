@@ -1,5 +1,6 @@
+"""Draft token time and calibrate() under bench.py's core layout, cold vs warm, caller pinned vs not."""
 import os, sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 import bench
 from paper_2503_00784_b200 import DEFAULT_PLANT, SHAPES, Draft, Target, calibrate
 print(open("/sys/devices/system/cpu/cpu0/topology/thread_siblings_list").read().strip(), open("/sys/devices/system/cpu/cpu2/topology/thread_siblings_list").read().strip())

@@ -1,3 +1,4 @@
+"""Per-launch GEMM time by CTA count (DD_PASS_KERNEL=0 path)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

@@ -1,6 +1,7 @@
+"""Persistent pass kernel above 16 tokens (DD_PASS_MAXW) vs the per-launch path: logits agreement by width."""
 import os, sys
 os.environ["DD_PASS_MAXW"] = "128"
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 import numpy as np
 from paper_2503_00784_b200 import SHAPES, Target
 TINY = SHAPES["tiny"]; PLANT = dict(plant_seed=7, alpha=0.5, gain=1.0, emb_std=1.0)
