@@ -15,6 +15,8 @@
 #include <immintrin.h>
 #include <pthread.h>
 #include <sched.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
@@ -95,6 +97,21 @@ QMat quantize(const std::vector<uint16_t>& w, int rows, int cols, SpinPool& pool
             m.rowsum[r] = sum;
         }
     });
+    if (rows % 32 == 0 && cols % 64 == 0) {
+        m.amx.resize(static_cast<size_t>(rows) * cols);
+        const int kb_n = cols / 64;
+        pool.run([&](int tid, int nt) {
+            for (int nb = tid; nb < rows / 16; nb += nt)
+                for (int kb = 0; kb < kb_n; ++kb) {
+                    int8_t* tile = &m.amx[(static_cast<size_t>(nb) * kb_n + kb) * 1024];
+                    for (int r = 0; r < 16; ++r)      // k / 4 within the block
+                        for (int n = 0; n < 16; ++n)  // output row within the block
+                            for (int j = 0; j < 4; ++j)
+                                tile[r * 64 + n * 4 + j] =
+                                    m.q[static_cast<size_t>(nb * 16 + n) * cols + kb * 64 + 4 * r + j];
+                }
+        });
+    }
     return m;
 }
 
@@ -274,9 +291,85 @@ void matmul4(SpinPool& pool, const Q4Mat& m, const uint16_t* x, float* Y, std::v
     });
 }
 
+// ---- AMX (TDPBUSD) prefill matmul: the same u8 x s8 integer dot products as
+// the VNNI path (exact), 32 tokens x 32 rows per step in four int32 tiles.
+bool amx_ready() {
+    static const bool ok = [] {
+        const char* env = getenv("DD_DRAFT_AMX");
+        if ((env && env[0] == '0') || !__builtin_cpu_supports("amx-int8")) return false;
+        constexpr long kArchReqXcompPerm = 0x1023, kXfeatureXtiledata = 18;  // Linux arch_prctl
+        return syscall(SYS_arch_prctl, kArchReqXcompPerm, kXfeatureXtiledata) == 0;
+    }();
+    return ok;
+}
+
+struct alignas(64) TileCfg {
+    uint8_t palette = 1, start_row = 0, pad[14] = {};
+    uint16_t colsb[16] = {};
+    uint8_t rows[16] = {};
+};
+
+__attribute__((target("amx-tile,amx-int8,avx512f"))) void qdot_amx(
+    const QMat& m, const uint8_t* xq, const float* xs, int w, int n_lo, int n_hi, float* Y) {
+    TileCfg cfg;
+    for (int t = 0; t < 8; ++t) {
+        cfg.colsb[t] = 64;
+        cfg.rows[t] = 16;
+    }
+    _tile_loadconfig(&cfg);
+    const int k = m.cols, kb_n = k / 64;
+    alignas(64) int32_t c[4][16][16];
+    for (int n0 = n_lo; n0 < n_hi; n0 += 32) {
+        const int8_t* b0 = &m.amx[static_cast<size_t>(n0 / 16) * kb_n * 1024];
+        const int8_t* b1 = b0 + static_cast<size_t>(kb_n) * 1024;
+        for (int t0 = 0; t0 < w; t0 += 32) {  // xq holds a multiple of 32 rows
+            _tile_zero(0);
+            _tile_zero(1);
+            _tile_zero(2);
+            _tile_zero(3);
+            for (int kb = 0; kb < kb_n; ++kb) {
+                _tile_loadd(4, xq + static_cast<size_t>(t0) * k + kb * 64, k);
+                _tile_loadd(5, xq + static_cast<size_t>(t0 + 16) * k + kb * 64, k);
+                _tile_loadd(6, b0 + static_cast<size_t>(kb) * 1024, 64);
+                _tile_loadd(7, b1 + static_cast<size_t>(kb) * 1024, 64);
+                _tile_dpbusd(0, 4, 6);
+                _tile_dpbusd(1, 4, 7);
+                _tile_dpbusd(2, 5, 6);
+                _tile_dpbusd(3, 5, 7);
+            }
+            _tile_stored(0, c[0], 64);
+            _tile_stored(1, c[1], 64);
+            _tile_stored(2, c[2], 64);
+            _tile_stored(3, c[3], 64);
+            for (int q = 0; q < 4; ++q) {
+                const int tb = t0 + (q >> 1) * 16, nb = n0 + (q & 1) * 16;
+                for (int i = 0; i < 16 && tb + i < w; ++i)
+                    for (int j = 0; j < 16; ++j) {
+                        const int32_t dot = c[q][i][j] - 128 * m.rowsum[nb + j];
+                        Y[static_cast<size_t>(tb + i) * m.rows + nb + j] =
+                            static_cast<float>(dot) * (xs[tb + i] * m.scale[nb + j]);
+                    }
+            }
+        }
+    }
+    _tile_release();
+}
+
 void matmul(SpinPool& pool, const QMat& m, const uint16_t* X, int w, float* Y,
             std::vector<uint8_t>& xq, std::vector<float>& xs) {
     quantize_acts(pool, X, w, m.cols, xq, xs);
+    if (w >= 16 && !m.amx.empty() && amx_ready()) {
+        // pad the activation rows to a multiple of 32 (rows past w are never stored)
+        const int wp = (w + 31) & ~31;
+        if (xq.size() < static_cast<size_t>(wp) * m.cols) xq.resize(static_cast<size_t>(wp) * m.cols, 128);
+        const int units = m.rows / 32;
+        pool.run([&](int tid, int nt) {
+            const int lo = static_cast<int>(static_cast<int64_t>(units) * tid / nt) * 32;
+            const int hi = static_cast<int>(static_cast<int64_t>(units) * (tid + 1) / nt) * 32;
+            if (lo < hi) qdot_amx(m, xq.data(), xs.data(), w, lo, hi, Y);
+        });
+        return;
+    }
     const int gran = w >= 4 ? 6 : 8;
     const int blocks = (m.rows + gran - 1) / gran;
     pool.run([&](int tid, int nt) {

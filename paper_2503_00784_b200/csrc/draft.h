@@ -40,6 +40,10 @@ struct QMat {
     std::vector<int8_t> q;        // [rows][cols]
     std::vector<float> scale;     // [rows]
     std::vector<int32_t> rowsum;  // [rows] sum of q
+    // AMX copy for prefill-sized matmuls (rows % 32 == 0, cols % 64 == 0):
+    // [rows / 16][cols / 64] tiles of 16 x 64 bytes, row r of a tile holding
+    // the 4 consecutive k of the tile's 16 output rows (TDPBUSD B layout)
+    std::vector<int8_t> amx;
 };
 
 // W4 LM head (the draft's largest matrix, streamed once per drafted token):
