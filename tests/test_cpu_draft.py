@@ -1,4 +1,4 @@
-"""The product's CPU draft model (AVX-512 BF16, host cores) vs the oracle."""
+"""The product's CPU draft model (W8A8 VNNI / AMX, 4-bit LM head, host cores) vs the oracle."""
 import numpy as np
 import pytest
 
@@ -50,3 +50,26 @@ def test_draft_prefill_bit_exact(draft):
     for n in (230, 3, 120, 229):
         assert np.array_equal(draft.logits(ctx[:n]), o[n - 1]), n
     orc.close()
+
+
+def test_draft_prefill_vnni_path_bit_exact(draft, tmp_path):
+    """The VNNI prefill path (DD_DRAFT_AMX=0, the fallback when AMX is absent)
+    gives the same bits as the oracle too (the AMX path runs above when present)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2503_00784_b200 import Draft\n"
+        "d = Draft(%r, weight_seed=31, plant=%r, threads=4, max_seq=256)\n"
+        "ctx = np.random.default_rng(2).integers(0, %d, 230).tolist()\n"
+        "np.save(%r, d.logits(ctx))\n" % (str(root), SHAPE, PLANT, SHAPE["vocab"], str(tmp_path / "g.npy")))
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "DD_DRAFT_AMX": "0"},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    orc = OracleLlama(SHAPE, weight_seed=31, plant=PLANT, max_seq=256, threads=4, w8a8=True)
+    o = orc.forward(np.random.default_rng(2).integers(0, SHAPE["vocab"], 230).tolist())
+    orc.close()
+    assert np.array_equal(np.load(tmp_path / "g.npy"), o[-1])
