@@ -60,7 +60,17 @@ typedef struct dd_model_desc {
     float rope_theta; /* 1e4 for Llama-2  */
     int max_seq;      /* KV capacity in tokens */
     int page_size;    /* tokens per KV page (0 -> 16) */
+    int precision;    /* DD_PREC_*; target only (the CPU draft ignores it) */
 } dd_model_desc;
+
+/* Target arithmetic (north star: "per-position target logits match within a
+ * stated bf16 tolerance (fp32-accumulate mode within 1e-4 relative)").
+ * BF16: bf16 weights, activations and KV, fp32 accumulation (the fast path).
+ * FP32ACC: activations carried as bf16 hi + lo pairs into two tcgen05 MMAs
+ * per k-step (one TMEM accumulator), fp32 KV cache and fp32 attention; one
+ * launch per GEMM / attention, tensor_parallel size 1, max_seq <= 49152. */
+#define DD_PREC_BF16 0
+#define DD_PREC_FP32ACC 1
 
 /* Synthetic random-init weights with an optional planted shared bigram
  * (SURVEY.md §7 hard part 1): a fraction `alpha` of tokens t get the LM-head
@@ -116,8 +126,10 @@ int dd_score(dd_ctx* ctx, const int32_t* tokens, int w);
 int dd_kv_len(const dd_ctx* ctx, int* n_cached);
 /* Roll the cache back to n_valid tokens (KV rollback after a rejection). */
 int dd_kv_truncate(dd_ctx* ctx, int n_valid);
-/* In-place compaction: move cache slots src_pos[i] -> dst_pos[i] (i < n),
- * in order; used to keep an accepted non-chain branch contiguous. */
+/* In-place compaction (north star (c)): move cache slots src_pos[i] ->
+ * dst_pos[i] for every layer, K and V, in one launch; dst strictly
+ * increasing with dst <= src, n <= 256 (keeps an accepted branch contiguous
+ * after its rejected siblings are dropped; the caller then truncates). */
 int dd_kv_compact(dd_ctx* ctx, const int32_t* src_pos, const int32_t* dst_pos, int n);
 
 /* Copy logits rows [row0, row0+rows) of the last pass to host memory. */
@@ -232,6 +244,20 @@ void dd_draft_destroy(dd_draft* d);
 int dd_draft_logits(dd_draft* d, const int32_t* ctx_tokens, int n, float* logits);
 /* Median wall time of one single-token draft forward (calibrate denominator). */
 int dd_draft_time_token(dd_draft* d, int trials, float* median_ms);
+/* The draft's q(. | ctx) (fp32, vocab) with the temperature / greedy rule
+ * applied (one-hot at the lowest-id argmax when greedy); returns the argmax
+ * in *argmax.  Test seam for the drafting parity tests. */
+int dd_draft_dist(dd_draft* d, const int32_t* ctx_tokens, int n, double temperature, int greedy,
+                  float* q, int* argmax);
+/* draft_dynamic (proj/src/drafting.cpp:71-136) as run by the engine's draft
+ * worker: sequences are written back to back into tokens (capacity budget),
+ * their lengths into seq_len (capacity max_sequences); *counter is the draft
+ * RandomStream counter, advanced in place.  Test seam (bit-exact against the
+ * reference's drafting). */
+int dd_draft_dynamic(dd_draft* d, const int32_t* ctx_tokens, int n, int budget,
+                     int max_sequences, double temperature, int greedy, uint64_t seed,
+                     uint64_t* counter, int32_t* tokens, int32_t* seq_len, int* n_seqs,
+                     double* threshold, int* forwards);
 
 /* ------------------------------------------------------------ engine */
 #define DD_BUDGET_FIXED 0
@@ -251,6 +277,12 @@ typedef struct dd_engine_config { /* EngineConfig (engine.hpp:43-60) */
     int calib_probe_len;
     int calib_trials;
     int threaded;       /* DuoExecution::threaded (1) / sequential (0)         */
+    /* WorkerHooks (engine.hpp:36-41, engine.cpp:430-432, 455-466): when
+     * jitter_max_us > 0, sleep a pseudo-random 0..jitter_max_us microseconds
+     * (splitmix64 of jitter_seed, iteration and role) before each draft step
+     * and each target step -- the determinism tests' scheduling jitter. */
+    uint64_t jitter_seed;
+    int jitter_max_us;
 } dd_engine_config;
 
 typedef struct dd_iteration_record { /* IterationRecord (engine.hpp:62-70) */

@@ -28,6 +28,10 @@ def lib():
                                                        C.c_float, C.c_int]
         L.orc_llama_free.argtypes = [C.c_void_p]
         L.orc_llama_set_quant.argtypes = [C.c_void_p, C.c_int]
+        L.orc_llama_set_pbf16.argtypes = [C.c_void_p, C.c_int]
+        L.orc_llama_set_fp32.argtypes = [C.c_void_p, C.c_int]
+        L.orc_llama_kv_compact.argtypes = [C.c_void_p, np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                           np.ctypeslib.ndpointer(np.int32, flags="C"), C.c_int]
         L.orc_llama_len.argtypes = [C.c_void_p]
         L.orc_llama_truncate.argtypes = [C.c_void_p, C.c_int]
         L.orc_llama_tensor.restype = C.POINTER(C.c_uint16)
@@ -44,7 +48,7 @@ class OracleLlama:
     """CPU Llama restatement with the product's synthetic-weight recipe."""
 
     def __init__(self, shape: dict, weight_seed: int, plant: dict | None = None,
-                 max_seq: int = 512, threads: int = 8, w8a8: bool = False):
+                 max_seq: int = 512, threads: int = 8, w8a8: bool = False, fp32: bool = False):
         plant = plant or {}
         self.shape = dict(shape)
         self.V = shape["vocab"]
@@ -56,6 +60,8 @@ class OracleLlama:
             plant.get("gain", 0.0), plant.get("emb_std", 0.0), threads)
         if w8a8:  # the product CPU draft's numerics (draft.cpp)
             lib().orc_llama_set_quant(self.h, 1)
+        if fp32:  # fp32 activations / KV (the GPU's fp32-accumulate mode)
+            lib().orc_llama_set_fp32(self.h, 1)
 
     def forward(self, tokens, last_only: bool = False) -> np.ndarray:
         t = np.ascontiguousarray(tokens, dtype=np.int32)
@@ -65,6 +71,15 @@ class OracleLlama:
         if rc != 0:
             raise RuntimeError(f"oracle forward failed ({rc})")
         return out
+
+    def set_p_bf16(self, on: bool) -> None:
+        """Diagnostic: round the softmax weights to bf16 before P.V."""
+        lib().orc_llama_set_pbf16(self.h, int(on))
+
+    def kv_compact(self, src, dst) -> None:
+        s = np.ascontiguousarray(src, dtype=np.int32)
+        d = np.ascontiguousarray(dst, dtype=np.int32)
+        lib().orc_llama_kv_compact(self.h, s, d, len(s))
 
     def __len__(self):
         return lib().orc_llama_len(self.h)

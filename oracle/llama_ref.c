@@ -159,6 +159,9 @@ typedef struct orc_llama {
     int32_t* plant_src;
     int32_t* plant_perm;
     int quant;      /* 1: W8A8 matmuls (the product CPU draft's numerics) */
+    int p_bf16;     /* 1: softmax weights rounded to bf16 before P.V (diagnostic) */
+    int fp32;       /* 1: fp32 activations and KV cache (the GPU's fp32acc mode) */
+    float* kvf;     /* fp32 KV cache of fp32 mode, same indexing as kv */
     orc_qmat qhead;
 } orc_llama;
 
@@ -260,6 +263,7 @@ void orc_llama_free(orc_llama* m) {
     free(m->emb);
     free(m->head);
     free(m->kv);
+    free(m->kvf);
     free(m->rope_cos);
     free(m->rope_sin);
     free(m->plant_src);
@@ -296,6 +300,41 @@ static orc_qmat quantize_rows_levels(const uint16_t* w, int rows, int cols, int 
 }
 static orc_qmat quantize_rows(const uint16_t* w, int rows, int cols) {
     return quantize_rows_levels(w, rows, cols, 127);
+}
+
+void orc_llama_set_pbf16(orc_llama* m, int on) { m->p_bf16 = on; }
+
+/* dd_kv_compact restated: move cache slots src[i] -> dst[i] for every layer,
+ * K and V, kv head, in list order (the caller truncates afterwards). */
+void orc_llama_kv_compact(orc_llama* m, const int32_t* src, const int32_t* dst, int n) {
+    for (int k = 0; k < n; ++k)
+        for (int l = 0; l < m->L; ++l)
+            for (int kv = 0; kv < 2; ++kv)
+                for (int h = 0; h < m->Hkv; ++h) {
+                    const size_t a = kv_idx(m, l, kv, h, src[k]), b = kv_idx(m, l, kv, h, dst[k]);
+                    for (int i = 0; i < m->hd; ++i) {
+                        m->kv[b + i] = m->kv[a + i];
+                        if (m->kvf) m->kvf[b + i] = m->kvf[a + i];
+                    }
+                }
+}
+
+/* fp32 mode (the GPU's DD_PREC_FP32ACC): activations are not rounded to bf16
+ * anywhere (GEMM inputs h / o / a, the QK^T query) and the KV cache is fp32;
+ * weights stay the generated bf16 values.  Set before the first forward. */
+int orc_llama_set_fp32(orc_llama* m, int on) {
+    if (m->n_cached != 0) return -1;
+    m->fp32 = on;
+    if (on && !m->kvf)
+        m->kvf = (float*)calloc((size_t)m->L * 2 * m->Hkv * m->max_seq * m->hd, sizeof(float));
+    return 0;
+}
+
+static inline float act(const orc_llama* m, float v) { return m->fp32 ? v : bfr(v); }
+static inline float kv_get(const orc_llama* m, size_t i) { return m->fp32 ? m->kvf[i] : bf2f(m->kv[i]); }
+static inline void kv_put(orc_llama* m, size_t i, float v) {
+    if (m->fp32) m->kvf[i] = v;
+    else m->kv[i] = f2bf(v);
 }
 
 void orc_llama_set_quant(orc_llama* m, int on) {
@@ -450,10 +489,10 @@ static float orc_exp_poly(float x) {
     return p * sc;
 }
 
-static float rmsnorm_bf(const float* x, int d, float eps, float* h) {
+static float rmsnorm_bf(const orc_llama* m, const float* x, int d, float eps, float* h) {
     float ss = 0.0f;
     for (int i = 0; i < d; ++i) ss = fmaf(x[i], x[i], ss);
-    for (int i = 0; i < d; ++i) h[i] = bfr(x[i] * 1.0f);
+    for (int i = 0; i < d; ++i) h[i] = act(m, x[i] * 1.0f);
     return 1.0f / sqrtf(ss / (float)d + eps);
 }
 static void scale_rows(float* y, int w, int n, const float* r) {
@@ -481,12 +520,12 @@ static void attn_range(void* p, int64_t lo, int64_t hi) {
         /* the GPU target feeds bf16(q) to its tensor-core QK^T (attention.cu);
          * the CPU draft (W8A8 mode) keeps q in fp32 */
         float qr[256];
-        for (int i = 0; i < hd; ++i) qr[i] = m->quant ? qv[i] : bfr(qv[i]);
+        for (int i = 0; i < hd; ++i) qr[i] = m->quant ? qv[i] : act(m, qv[i]);
         float mx = -INFINITY;
         for (int j = 0; j < nk; ++j) {
-            const uint16_t* kr = m->kv + kv_idx(m, l, 0, kvh, j);
+            const size_t kr = kv_idx(m, l, 0, kvh, j);
             float acc = 0.0f;
-            for (int i = 0; i < hd; ++i) acc = fmaf(qr[i], bf2f(kr[i]), acc);
+            for (int i = 0; i < hd; ++i) acc = fmaf(qr[i], kv_get(m, kr + i), acc);
             sc[j] = acc * a->scale;
             if (sc[j] > mx) mx = sc[j];
         }
@@ -512,10 +551,12 @@ static void attn_range(void* p, int64_t lo, int64_t hi) {
             }
         }
         const float inv = 1.0f / sum;
+        if (m->p_bf16)
+            for (int j = 0; j < nk; ++j) sc[j] = bfr(sc[j]);
         for (int i = 0; i < hd; ++i) {
             float acc = 0.0f;
-            for (int j = 0; j < nk; ++j) acc = fmaf(sc[j], bf2f(m->kv[kv_idx(m, l, 1, kvh, j) + i]), acc);
-            a->o[(size_t)t * qd + head * hd + i] = bfr(acc * inv);
+            for (int j = 0; j < nk; ++j) acc = fmaf(sc[j], kv_get(m, kv_idx(m, l, 1, kvh, j) + i), acc);
+            a->o[(size_t)t * qd + head * hd + i] = act(m, acc * inv);
         }
         free(sc);
     }
@@ -539,7 +580,7 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
     for (int t = 0; t < w; ++t) {
         if (tokens[t] < 0 || tokens[t] >= V) return -2;
         for (int i = 0; i < d; ++i) x[(size_t)t * d + i] = bf2f(m->emb[(size_t)tokens[t] * d + i]);
-        rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+        rn[t] = rmsnorm_bf(m, x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
     }
     const float scale = (float)(1.0 / sqrt((double)hd));
     for (int l = 0; l < m->L; ++l) {
@@ -561,13 +602,13 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
                         q[(size_t)t * qd + head * hd + i] = lo;
                         q[(size_t)t * qd + head * hd + i + half] = hi;
                     } else {
-                        uint16_t* kd = m->kv + kv_idx(m, l, 0, head - H, pos);
-                        kd[i] = f2bf(lo);
-                        kd[i + half] = f2bf(hi);
+                        const size_t kd = kv_idx(m, l, 0, head - H, pos);
+                        kv_put(m, kd + i, lo);
+                        kv_put(m, kd + i + half, hi);
                     }
                 }
             for (int e = 0; e < kvd; ++e)
-                m->kv[kv_idx(m, l, 1, e / hd, pos) + e % hd] = f2bf(r[qd + kvd + e]);
+                kv_put(m, kv_idx(m, l, 1, e / hd, pos) + e % hd, r[qd + kvd + e]);
         }
         /* attention: query t (pos n0+t) over keys 0..pos */
         {
@@ -578,7 +619,7 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
         else matmul(Ly->o, d, qd, o, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
-            rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+            rn[t] = rmsnorm_bf(m, x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
         }
         if (m->quant) matmul_q(&Ly->qgu, h, w, y);
         else matmul(Ly->gu, 2 * F, d, h, w, y);
@@ -587,13 +628,13 @@ int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits,
             for (int f = 0; f < F; ++f) {
                 const float g = y[(size_t)t * 2 * F + f], u = y[(size_t)t * 2 * F + F + f];
                 const float silu = g / (1.0f + (m->quant ? orc_exp_poly(-g) : expf(-g)));
-                a[(size_t)t * F + f] = bfr(silu * u);
+                a[(size_t)t * F + f] = act(m, silu * u);
             }
         if (m->quant) matmul_q(&Ly->qdn, a, w, y);
         else matmul(Ly->dn, d, F, a, w, y);
         for (int t = 0; t < w; ++t) {
             for (int i = 0; i < d; ++i) x[(size_t)t * d + i] += y[(size_t)t * d + i];
-            rn[t] = rmsnorm_bf(x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
+            rn[t] = rmsnorm_bf(m, x + (size_t)t * d, d, m->eps, h + (size_t)t * d);
         }
     }
     if (logits) {

@@ -34,6 +34,12 @@ SHAPES = {
                       ffn_dim=3072, vocab=32000, rms_eps=1e-5, rope_theta=1e4),
     "tiny": dict(n_layers=4, d_model=512, n_heads=8, n_kv_heads=8, head_dim=64, ffn_dim=1408,
                  vocab=32000, rms_eps=1e-5, rope_theta=1e4),
+    # head_dim-128 parity shapes (the 7B / 70B code paths at oracle-sized
+    # widths): MHA like the 7B, and GQA at the 70B's 8:1 q:kv ratio
+    "mid128": dict(n_layers=2, d_model=1024, n_heads=8, n_kv_heads=8, head_dim=128,
+                   ffn_dim=2816, vocab=32000, rms_eps=1e-5, rope_theta=1e4),
+    "gqa128": dict(n_layers=2, d_model=2048, n_heads=16, n_kv_heads=2, head_dim=128,
+                   ffn_dim=5632, vocab=32000, rms_eps=1e-5, rope_theta=1e4),
     "llama2_70b": dict(n_layers=80, d_model=8192, n_heads=64, n_kv_heads=8, head_dim=128,
                        ffn_dim=28672, vocab=32000, rms_eps=1e-5, rope_theta=1e4),
 }
@@ -71,11 +77,16 @@ def _check(rc: int, handle=None):
     raise cls(msg or f"duodec_b200 error {rc}")
 
 
-def _desc(shape: dict, max_seq: int, page_size: int = 16) -> _L.ModelDesc:
+PRECISIONS = {"bf16": _L.DD_PREC_BF16, "fp32acc": _L.DD_PREC_FP32ACC}
+
+
+def _desc(shape: dict, max_seq: int, page_size: int = 16, precision: str = "bf16") -> _L.ModelDesc:
+    if precision not in PRECISIONS:
+        raise ConfigError(f"unknown precision {precision}")
     return _L.ModelDesc(shape["n_layers"], shape["d_model"], shape["n_heads"],
                         shape.get("n_kv_heads", shape["n_heads"]), shape["head_dim"],
                         shape["ffn_dim"], shape["vocab"], shape.get("rms_eps", 1e-5),
-                        shape.get("rope_theta", 1e4), max_seq, page_size)
+                        shape.get("rope_theta", 1e4), max_seq, page_size, PRECISIONS[precision])
 
 
 def _plant(p: Optional[dict]) -> Optional[_L.PlantDesc]:
@@ -99,12 +110,15 @@ class Target:
 
     def __init__(self, shape: dict, weight_seed: int = 1234, plant: Optional[dict] = None,
                  max_seq: int = 4096, device: int = 0, page_size: int = 16, tp_rank: int = 0,
-                 tp_size: int = 1):
+                 tp_size: int = 1, precision: str = "bf16"):
+        """precision: "bf16" (the fast path) or "fp32acc" (split hi + lo
+        activations, fp32 KV and attention: the 1e-4 reference mode)."""
         self.shape = dict(shape)
         self.vocab = shape["vocab"]
         self.tp_rank, self.tp_size = tp_rank, tp_size
+        self.precision = precision
         h = C.c_void_p()
-        _check(_L.lib().dd_ctx_create_tp(C.byref(_desc(shape, max_seq, page_size)), device,
+        _check(_L.lib().dd_ctx_create_tp(C.byref(_desc(shape, max_seq, page_size, precision)), device,
                                          tp_rank, tp_size, C.byref(h)))
         self.h = h
         pl = _plant(plant)
@@ -275,6 +289,35 @@ class Draft:
                                         out.ctypes.data_as(C.POINTER(C.c_float))))
         return out
 
+    def dist(self, context: Sequence[int], temperature: float = 1.0, greedy: bool = False):
+        """q(. | context) as the engine's drafting sees it -> (q fp32, argmax)."""
+        t = _i32(context)
+        q = np.zeros(self.vocab, dtype=np.float32)
+        am = C.c_int()
+        _check(_L.lib().dd_draft_dist(self.h, _i32p(t), len(t), temperature, int(greedy),
+                                      q.ctypes.data_as(C.POINTER(C.c_float)), C.byref(am)))
+        return q, am.value
+
+    def draft_dynamic(self, context: Sequence[int], budget: int, max_sequences: int,
+                      seed: int, counter: int = 0, temperature: float = 1.0,
+                      greedy: bool = False) -> dict:
+        """The engine's draft_dynamic (proj/src/drafting.cpp:71-136)."""
+        t = _i32(context)
+        toks = np.zeros(budget, dtype=np.int32)
+        lens = np.zeros(max_sequences, dtype=np.int32)
+        cnt = C.c_uint64(counter)
+        ns, fw = C.c_int(), C.c_int()
+        th = C.c_double()
+        _check(_L.lib().dd_draft_dynamic(self.h, _i32p(t), len(t), budget, max_sequences,
+                                         temperature, int(greedy), seed, C.byref(cnt),
+                                         _i32p(toks), _i32p(lens), C.byref(ns), C.byref(th),
+                                         C.byref(fw)))
+        seqs, k = [], 0
+        for i in range(ns.value):
+            seqs.append([int(x) for x in toks[k:k + lens[i]]])
+            k += int(lens[i])
+        return dict(seqs=seqs, threshold=th.value, forwards=fw.value, counter=cnt.value)
+
     def time_token(self, trials: int = 12) -> float:
         ms = C.c_float()
         _check(_L.lib().dd_draft_time_token(self.h, trials, C.byref(ms)))
@@ -312,6 +355,9 @@ class EngineConfig:
     calib_probe_len: int = 8
     calib_trials: int = 12
     threaded: bool = True
+    # WorkerHooks jitter (engine.hpp:36-41): 0 = off
+    jitter_seed: int = 0
+    jitter_max_us: int = 0
 
     def to_c(self) -> _L.EngineConfigC:
         if self.mode not in MODES:
@@ -320,7 +366,8 @@ class EngineConfig:
             MODES[self.mode], self.budget, self.max_sequences, self.max_new_tokens,
             self.temperature, int(self.greedy), self.draft_seed, self.verify_seed,
             _L.DD_BUDGET_CALIBRATED if self.budget_policy == "calibrated" else _L.DD_BUDGET_FIXED,
-            self.budget_hard_cap, self.calib_probe_len, self.calib_trials, int(self.threaded))
+            self.budget_hard_cap, self.calib_probe_len, self.calib_trials, int(self.threaded),
+            self.jitter_seed, self.jitter_max_us)
 
 
 @dataclass
@@ -351,6 +398,32 @@ class GenerationResult:
     d2h_bytes: int = 0
     gpu_launches: int = 0
     device_ttft_ms: float = 0.0
+
+    def iteration_lines(self) -> List[dict]:
+        """`duodec profile` output (proj/tools/main.cpp:202-207, 332-367):
+        one object per iteration with the reference's field names, then the
+        summary object."""
+        out, hist = [], {}
+        for i, it in enumerate(self.iterations):
+            out.append({"draft_ms": it.draft_ms, "target_ms": it.target_ms,
+                        "verify_ms": it.verify_ms, "comm_ms": it.comm_ms,
+                        "tokens_processed": it.tokens_processed, "s": it.sequence_count,
+                        "accepted": it.accepted, "iteration": i})
+            if it.sequence_count > 0:
+                hist[str(it.sequence_count)] = hist.get(str(it.sequence_count), 0) + 1
+        out.append({"summary": True, "iterations": len(self.iterations),
+                    "sequence_histogram": dict(sorted(hist.items(), key=lambda kv: int(kv[0]))),
+                    "tokens": len(self.tokens), "tps": self.tps, "ttft_ms": self.ttft_ms,
+                    "total_ms": self.total_ms})
+        return out
+
+    def to_json(self, mode: str) -> dict:
+        """`duodec generate` output (proj/tools/main.cpp:209-216)."""
+        lines = self.iteration_lines()[:-1]
+        for ln in lines:
+            del ln["iteration"]
+        return {"mode": mode, "tokens": list(self.tokens), "tps": self.tps,
+                "ttft_ms": self.ttft_ms, "total_ms": self.total_ms, "iterations": lines}
 
 
 def tp_connect_group(target, group=None) -> None:

@@ -14,13 +14,14 @@ DD_OK, DD_E_ARG, DD_E_CUDA, DD_E_STATE, DD_E_CAPACITY = 0, -1, -2, -3, -4
 DD_MODE_DUO, DD_MODE_SPS, DD_MODE_VANILLA = 0, 1, 2
 DD_BUDGET_FIXED, DD_BUDGET_CALIBRATED = 0, 1
 DD_TP_HANDLE_BYTES = 64
+DD_PREC_BF16, DD_PREC_FP32ACC = 0, 1
 
 
 class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("d_model", C.c_int), ("n_heads", C.c_int),
                 ("n_kv_heads", C.c_int), ("head_dim", C.c_int), ("ffn_dim", C.c_int),
                 ("vocab", C.c_int), ("rms_eps", C.c_float), ("rope_theta", C.c_float),
-                ("max_seq", C.c_int), ("page_size", C.c_int)]
+                ("max_seq", C.c_int), ("page_size", C.c_int), ("precision", C.c_int)]
 
 
 class PlantDesc(C.Structure):
@@ -46,7 +47,8 @@ class EngineConfigC(C.Structure):
                 ("max_new_tokens", C.c_int), ("temperature", C.c_double), ("greedy", C.c_int),
                 ("draft_seed", C.c_uint64), ("verify_seed", C.c_uint64),
                 ("budget_policy", C.c_int), ("budget_hard_cap", C.c_int),
-                ("calib_probe_len", C.c_int), ("calib_trials", C.c_int), ("threaded", C.c_int)]
+                ("calib_probe_len", C.c_int), ("calib_trials", C.c_int), ("threaded", C.c_int),
+                ("jitter_seed", C.c_uint64), ("jitter_max_us", C.c_int)]
 
 
 class IterationRecordC(C.Structure):
@@ -111,6 +113,11 @@ SIGNATURES = {
     "dd_draft_destroy": (None, [_vp]),
     "dd_draft_logits": (C.c_int, [_vp, _i32p, C.c_int, _f32p]),
     "dd_draft_time_token": (C.c_int, [_vp, C.c_int, _f32p]),
+    "dd_draft_dist": (C.c_int, [_vp, _i32p, C.c_int, C.c_double, C.c_int, _f32p,
+                                C.POINTER(C.c_int)]),
+    "dd_draft_dynamic": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                   C.c_uint64, C.POINTER(C.c_uint64), _i32p, _i32p,
+                                   C.POINTER(C.c_int), _f64p, C.POINTER(C.c_int)]),
     "dd_engine_run": (C.c_int, [_vp, _vp, C.POINTER(EngineConfigC), _i32p, C.c_int,
                                 C.POINTER(GenerationResultC)]),
     "dd_engine_run_tp": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.POINTER(EngineConfigC), _i32p,

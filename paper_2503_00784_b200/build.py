@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libduodec_b200.so"
 
-CU_SOURCES = ["gemm.cu", "gemm_wide.cu", "model.cu", "attention.cu", "pass.cu", "accept.cu", "tp.cu",
+CU_SOURCES = ["gemm.cu", "gemm_wide.cu", "model.cu", "attention.cu", "attention_f32.cu", "pass.cu", "accept.cu", "tp.cu",
               "target.cu"]
 CPP_SOURCES = ["plant.cpp", "draft.cpp", "engine.cpp"]
 
@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             if force or _stale(obj, [CSRC / src, *headers]):
                 _run([_nvcc(), *NVCC_FLAGS, "-c", str(CSRC / src), "-o", str(obj)], log)
             objs.append(obj)
-        for src in CPP_SOURCES + (["stubs.cpp"] if not (CSRC / "engine.cpp").exists() else []):
+        for src in CPP_SOURCES:
             if not (CSRC / src).exists():
                 continue
             obj = BUILD / (src + ".o")

@@ -384,17 +384,19 @@ int launch_attention(const PassState* ps, int w, const ModelDims& m, const float
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = cluster ? 1 : 0;
-    auto go = [&](auto kernel, size_t smem, bool& attr) {
+    const int dev = current_device_slot();
+    auto go = [&](auto kernel, size_t smem, bool* attr) {  // attr: per device (TP ranks of one process)
         cfg.dynamicSmemBytes = smem;
-        if (!attr) {
+        if (!attr[dev]) {
             cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            attr = true;
+            attr[dev] = true;
         }
         return cudaLaunchKernelEx(&cfg, kernel, ps, m, q, kv_pool, page_table, page_size, layer,
                                   scale_log2, o);
     };
     cudaError_t e;
-    static bool a128c = false, a128s = false, a64c = false, a64s = false;
+    static bool a128c[kMaxDevices] = {}, a128s[kMaxDevices] = {}, a64c[kMaxDevices] = {},
+                a64s[kMaxDevices] = {};
     if (m.head_dim == 128) {
         e = cluster ? go(attn_cluster_kernel<128, kRanks>, sizeof(AttnSmem<128>), a128c)
                     : go(attn_cluster_kernel<128, 1>, sizeof(AttnSmem<128>), a128s);

@@ -18,6 +18,14 @@
 namespace dd {
 
 constexpr int kNumSMs = 148;
+constexpr int kMaxDevices = 64;  // per-device launch attributes (one process may drive several GPUs)
+
+// Current device index, clamped into the per-device attribute tables.
+inline int current_device_slot() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev);
+}
 
 // ---------------------------------------------------------------------------
 // splitmix64, identical to RandomStream::next_u64 (reference

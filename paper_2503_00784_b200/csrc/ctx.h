@@ -32,6 +32,7 @@ constexpr int kPsRing = 32;  // pinned PassState staging: a 4K-token prefill enq
 
 struct dd_ctx {
     int device = 0;
+    int sm_count = 0;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
     cudaEvent_t q_ready = nullptr;
     cudaEvent_t ps_done[dd::kPsRing] = {};
@@ -64,6 +65,13 @@ struct dd_ctx {
     float* logits = nullptr;        // [256, vocab]
     CUtensorMap map_h, map_o, map_a;
     CUtensorMap map_h128, map_o128, map_a128;  // 128-row boxes (prefill GEMM)
+    // fp32-accumulate mode (DD_PREC_FP32ACC): lo halves of the GEMM inputs and
+    // an fp32 KV pool; every pass runs the per-launch path
+    bool fp32acc = false;
+    __nv_bfloat16 *h_lo = nullptr, *o_lo = nullptr, *a_lo = nullptr;
+    CUtensorMap map_h_lo, map_o_lo, map_a_lo;
+    float* kv_f32 = nullptr;
+    int32_t* d_compact_dst = nullptr;  // dd_kv_compact destination slots
     dd::GemmPlan wide_plans[5] = {};
     float* ws_wide = nullptr;       // prefill GEMM stream-K partials
 

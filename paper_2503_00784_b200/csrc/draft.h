@@ -110,4 +110,5 @@ struct dd_draft {
     std::unique_ptr<dd::CpuLlama> model;
     std::vector<int> cpus;
     std::string err;
+    bool calib_warmed = false;  // dd_calibrate's 1 s steady-state warm-up ran
 };

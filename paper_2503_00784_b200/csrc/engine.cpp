@@ -49,6 +49,8 @@ void ck(int rc, dd_ctx* ctx) {
     if (rc != DD_OK) throw EngineError(rc, dd_last_error(ctx));
 }
 
+void jitter(const dd_engine_config& c, int iter, int role);
+
 // RandomStream (proj/include/duodec/random.hpp:11-34)
 struct Rng {
     uint64_t seed = 0, counter = 0;
@@ -365,8 +367,10 @@ struct Runner {
                     pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
                 }
                 try {
-                    while (ch.wait_request())
+                    for (int it = 0; ch.wait_request(); ++it) {
+                        jitter(cfg, it, 0);
                         ch.post_reply(draft_dynamic(dm, ch.z, budget, cfg.max_sequences, rng_draft));
+                    }
                 } catch (...) {
                     ch.error = std::current_exception();
                     ch.failed.store(true, std::memory_order_release);
@@ -385,14 +389,18 @@ struct Runner {
                 Bundle bundle;
                 const auto tt = Clock::now();
                 double comm = 0.0;
+                const int it = static_cast<int>(recs.size());
                 if (threaded) {
                     ch.post_request(std::move(z));
+                    jitter(cfg, it, 1);
                     score(pass);
                     const auto tw = Clock::now();
                     bundle = ch.wait_reply();  // rendezvous
                     comm = ms_since(tw);
                 } else {
+                    jitter(cfg, it, 0);
                     bundle = draft_dynamic(dm, z, budget, cfg.max_sequences, rng_draft);
+                    jitter(cfg, it, 1);
                     score(pass);
                 }
                 const auto tv = Clock::now();
@@ -462,6 +470,17 @@ struct Runner {
     }
 };
 
+// WorkerHooks jitter (engine.hpp:36-41): role 0 = before_draft, 1 = before_target
+void jitter(const dd_engine_config& c, int iter, int role) {
+    if (c.jitter_max_us <= 0) return;
+    uint64_t z = c.jitter_seed + (2ull * static_cast<uint64_t>(iter) + role + 1) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    std::this_thread::sleep_for(
+        std::chrono::microseconds(z % (static_cast<uint64_t>(c.jitter_max_us) + 1)));
+}
+
 int choose_budget_impl(double c) { return static_cast<int>(std::max<long>(2, std::lround(c))); }
 
 }  // namespace
@@ -500,10 +519,15 @@ int dd_calibrate(dd_ctx* ctx, dd_draft* draft, int probe_len, int trials, int ha
         // measure the draft in steady state, as run_duo runs it: the first
         // ~second of drafting after the draft's creation runs up to 40% slower
         // on the pool's hosts (clocks, caches), so keep drafting for 1 s first
+        // (once per draft: later calibrations reuse the warmed state)
         const auto t_warm = std::chrono::steady_clock::now();
-        do {
-            rc = dd_draft_time_token(draft, trials, &d_ms);
-        } while (rc == DD_OK && std::chrono::steady_clock::now() - t_warm < std::chrono::seconds(1));
+        if (!draft->calib_warmed) {
+            do {
+                rc = dd_draft_time_token(draft, trials, &d_ms);
+            } while (rc == DD_OK &&
+                     std::chrono::steady_clock::now() - t_warm < std::chrono::seconds(1));
+            draft->calib_warmed = rc == DD_OK;
+        }
         if (rc == DD_OK) rc = dd_draft_time_token(draft, trials, &d_ms);
         if (pin) pthread_setaffinity_np(pthread_self(), sizeof(saved), &saved);
     }
@@ -528,6 +552,16 @@ static int engine_run(const std::vector<dd_ctx*>& ranks, dd_draft* draft,
         return ctx_fail(ctx, DD_E_ARG, "invalid engine configuration");
     if (c.mode != DD_MODE_VANILLA && !draft)
         return ctx_fail(ctx, DD_E_ARG, "sps/duo mode requires a draft model");
+    // run_sps / run_duo throw ConfigError on a vocabulary mismatch (the
+    // acceptance kernel reads q rows at the target's vocabulary stride)
+    if (c.mode != DD_MODE_VANILLA)
+        for (dd_ctx* k : ranks)
+            if (!k || draft->model->vocab() != k->vocab)
+                return ctx_fail(ctx, DD_E_ARG, "draft and target vocabularies differ");
+    // dd_verify tests at most 16 bundle sequences (verify_bundle's draw
+    // schedule would silently lose the rest)
+    if (c.max_sequences > 16)
+        return ctx_fail(ctx, DD_E_ARG, "max_sequences above the verifier's 16-sequence bundle");
     if (ranks.size() > 1 && c.mode != DD_MODE_VANILLA && c.budget_policy == DD_BUDGET_CALIBRATED)
         return ctx_fail(ctx, DD_E_ARG, "a tensor-parallel group needs a fixed budget");
     Runner r;
@@ -537,6 +571,9 @@ static int engine_run(const std::vector<dd_ctx*>& ranks, dd_draft* draft,
     r.cfg = c;
     try {
         r.budget = c.budget;
+        // the reference starts the timeline before resolve_budget
+        // (engine.cpp:444-456), so total_ms / ttft_ms / tps include calibration
+        r.t_start = Clock::now();
         if (c.mode != DD_MODE_VANILLA && c.budget_policy == DD_BUDGET_CALIBRATED) {
             double coef = 0.0;
             ck(dd_kv_truncate(ctx, 0), ctx);
@@ -552,7 +589,6 @@ static int engine_run(const std::vector<dd_ctx*>& ranks, dd_draft* draft,
         r.rng_verify.seed = c.verify_seed;
         for (dd_ctx* k : ranks) k->h2d_bytes = k->d2h_bytes = k->launches = 0;
         ck(ctx_mark(ctx, 0), ctx);
-        r.t_start = Clock::now();
         r.truncate_all(0);
         // SpS drafts before its first pass, so its prefill (overlapping that
         // drafting) stops before c; vanilla and duo score the last prefill chunk.
@@ -605,6 +641,50 @@ static int engine_run(const std::vector<dd_ctx*>& ranks, dd_draft* draft,
 int dd_engine_run(dd_ctx* ctx, dd_draft* draft, const dd_engine_config* cfg,
                   const int32_t* prompt, int n_prompt, dd_generation_result* out) {
     return engine_run({ctx}, draft, cfg, prompt, n_prompt, out);
+}
+
+int dd_draft_dist(dd_draft* d, const int32_t* ctx_tokens, int n, double temperature, int greedy,
+                  float* q, int* argmax) {
+    if (!d || !ctx_tokens || n < 1 || !q || !argmax || (!greedy && !(temperature > 0.0)))
+        return DD_E_ARG;
+    try {
+        DraftModel dm(d->model.get(), temperature, greedy != 0);
+        *argmax = dm.dist(std::vector<int32_t>(ctx_tokens, ctx_tokens + n), q);
+        return DD_OK;
+    } catch (const EngineError& e) {
+        d->err = e.what();
+        return e.code;
+    }
+}
+
+int dd_draft_dynamic(dd_draft* d, const int32_t* ctx_tokens, int n, int budget,
+                     int max_sequences, double temperature, int greedy, uint64_t seed,
+                     uint64_t* counter, int32_t* tokens, int32_t* seq_len, int* n_seqs,
+                     double* threshold, int* forwards) {
+    if (!d || !ctx_tokens || n < 1 || !counter || !tokens || !seq_len || !n_seqs || !threshold ||
+        !forwards || budget < 1 || max_sequences < 1 || (!greedy && !(temperature > 0.0)))
+        return DD_E_ARG;
+    try {
+        DraftModel dm(d->model.get(), temperature, greedy != 0);
+        Rng rng;
+        rng.seed = seed;
+        rng.counter = *counter;
+        Bundle b = draft_dynamic(dm, std::vector<int32_t>(ctx_tokens, ctx_tokens + n), budget,
+                                 max_sequences, rng);
+        int k = 0;
+        for (size_t i = 0; i < b.seqs.size(); ++i) {
+            seq_len[i] = static_cast<int32_t>(b.seqs[i].tokens.size());
+            for (int32_t t : b.seqs[i].tokens) tokens[k++] = t;
+        }
+        *n_seqs = static_cast<int>(b.seqs.size());
+        *threshold = b.threshold;
+        *forwards = b.forwards;
+        *counter = rng.counter;
+        return DD_OK;
+    } catch (const EngineError& e) {
+        d->err = e.what();
+        return e.code;
+    }
 }
 
 int dd_engine_run_tp(dd_ctx* const* ctxs, int n, dd_draft* draft, const dd_engine_config* cfg,

@@ -44,7 +44,8 @@ using namespace gemm_dev;
 
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_sk_kernel(const __nv_bfloat16* __restrict__ w_tiled,
-                   const __grid_constant__ CUtensorMap map_x, GemmArgs a) {
+                   const __grid_constant__ CUtensorMap map_x,
+                   const __grid_constant__ CUtensorMap map_x_lo, GemmArgs a) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const long g0 = sk_begin(c, T, P), g1 = sk_begin(c + 1, T, P);
     const int len = static_cast<int>(g1 - g0);
     const uint32_t b_bytes = static_cast<uint32_t>(a.nt) * 128u;
-    const uint32_t stage_bytes = kABytes + b_bytes;
+    const uint32_t stage_bytes = kABytes + b_bytes * (a.split ? 2u : 1u);
     const int stages = a.stages;
 
     float* red = reinterpret_cast<float*>(smem + stages * stage_bytes);  // [kChunk][128]
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             tr[7] = smid;
         }
         tma_prefetch_desc(&map_x);
+        if (a.split) tma_prefetch_desc(&map_x_lo);
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -154,6 +156,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int kc = static_cast<int>((g0 + i) % a.nkb) * kBlockK;
                 for (int r = 0; r < nbox; ++r)
                     tma_load_2d(sa + kABytes + r * 2048, &map_x, &full[s], kc, r * 16, pol_x);
+                if (a.split)
+                    for (int r = 0; r < nbox; ++r)
+                        tma_load_2d(sa + kABytes + b_bytes + r * 2048, &map_x_lo, &full[s], kc,
+                                    r * 16, pol_x);
             }
         }
     } else if (warp == 1) {
@@ -180,6 +186,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                     for (int k = 0; k < kBlockK / 16; ++k)
                         umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc,
                                   (g != lo || k != 0) ? 1u : 0u);
+                    if (a.split) {  // W.(x_hi + x_lo): the lo halves into the same accumulator
+                        const uint64_t bdesc_lo = sw128_kmajor_desc(sa + kABytes + b_bytes);
+#pragma unroll
+                        for (int k = 0; k < kBlockK / 16; ++k)
+                            umma_bf16(acc, adesc + 2 * k, bdesc_lo + 2 * k, idesc, 1u);
+                    }
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[b]);
@@ -359,14 +371,14 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
     return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-GemmPlan plan_gemm(int n_out, int k, int nt) {
+GemmPlan plan_gemm(int n_out, int k, int nt, int split) {
     static const int env_stages = getenv("DD_GEMM_STAGES") ? atoi(getenv("DD_GEMM_STAGES")) : 0;
     static const int env_ctas = getenv("DD_GEMM_CTAS") ? atoi(getenv("DD_GEMM_CTAS")) : 0;
     GemmPlan p{};
     p.tiles = n_out / kBlockM;
     p.nkb = k / kBlockK;
     const long T = static_cast<long>(p.tiles) * p.nkb;
-    const uint32_t stage_bytes = kABytes + static_cast<uint32_t>(nt) * 128u;
+    const uint32_t stage_bytes = kABytes + static_cast<uint32_t>(nt) * 128u * (split ? 2u : 1u);
     const uint32_t fixed = kChunk * 128 * 4 + 64 * 8 + 1024 + 64;
     const uint32_t budget = 110u * 1024u;
     int stages = static_cast<int>((budget - fixed) / stage_bytes);
@@ -406,12 +418,14 @@ void gemm_set_trace(unsigned long long* buf) { g_trace = buf; }
 
 cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, int n_out, int k,
                         int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
-                        cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
+                        cudaStream_t stream, const CUtensorMap* map_x_lo) {
+    // per device (a process may drive several GPUs: tensor-parallel ranks)
+    static bool attr_set[kMaxDevices] = {};
+    const int dev = current_device_slot();
+    if (!attr_set[dev]) {
         cudaFuncSetAttribute(gemm_sk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              220 * 1024);
-        attr_set = true;
+        attr_set[dev] = true;
     }
     GemmArgs a{};
     a.n_out = n_out;
@@ -430,6 +444,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
     a.prefetch = env_pf;
     static const int env_il = getenv("DD_GEMM_INTERLEAVE") ? atoi(getenv("DD_GEMM_INTERLEAVE")) : 0;
     a.interleave = env_il;
+    a.split = map_x_lo != nullptr ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.ctas, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
@@ -440,7 +455,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_sk_kernel, w_tiled, *map_x, a);
+    return cudaLaunchKernelEx(&cfg, gemm_sk_kernel, w_tiled, *map_x, map_x_lo ? *map_x_lo : *map_x, a);
 }
 
 }  // namespace dd

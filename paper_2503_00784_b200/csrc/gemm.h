@@ -42,6 +42,11 @@ struct GemmEpiParams {
     int ss_tiles;
     float eps;
     int norm_d;            // d of the normalised row
+    // fp32-accumulate mode (DD_PREC_FP32ACC): the consumer GEMM reads its
+    // activations as bf16 hi + lo pairs (two MMAs into one accumulator), so
+    // producers also write lo = bf16(v - hi); K / V go to an fp32 cache.
+    __nv_bfloat16* lo_out; // kEpiResidual: u_lo; kEpiSwiGLU: a_lo; or nullptr
+    float* kv_f32;         // kEpiQkvRope: fp32 KV pool (same addressing), or nullptr
 };
 
 struct GemmArgs {
@@ -56,6 +61,7 @@ struct GemmArgs {
     int tmem_buf;   // TMEM columns per accumulator buffer (2 buffers)
     int prefetch;   // L2 prefetch distance in k-blocks beyond the ring
     int interleave; // timing experiment: lockstep-sequential weight addresses
+    int split;      // 1: activations are hi + lo bf16 pairs (fp32-accumulate mode)
     float* ws;      // [tiles][max_seg][w][128] fp32 segment partials
     GemmEpiParams epi;
     unsigned long long* trace;  // debug: 8 globaltimer stamps per CTA, or nullptr
@@ -74,7 +80,8 @@ struct GemmPlan {
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols,
                    uint32_t box_rows);
 
-GemmPlan plan_gemm(int n_out, int k, int nt);
+// split: fp32-accumulate mode (two activation boxes per stage)
+GemmPlan plan_gemm(int n_out, int k, int nt, int split = 0);
 
 // workspace floats needed by a plan at width w
 size_t gemm_ws_floats(const GemmPlan& p, int w);
@@ -85,9 +92,11 @@ void gemm_set_trace(unsigned long long* buf);
 // w_tiled: weights in the pre-tiled layout of common.cuh (tiled_offset).
 // Launched with programmatic dependent launch: the kernel streams its first
 // weight stages before waiting on the previous kernel in the stream.
+// map_x_lo (fp32-accumulate mode only): the lo halves of the activations;
+// the plan must have been made with split = 1.
 cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, int n_out, int k,
                         int w, int nt, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
-                        cudaStream_t stream);
+                        cudaStream_t stream, const CUtensorMap* map_x_lo = nullptr);
 
 // Prefill GEMM (gemm_wide.cu): tokens on M (<= 128, one TMEM lane each),
 // 256 weight rows on N; map_x128 has 128-row boxes.  n_out % 256 == 0.

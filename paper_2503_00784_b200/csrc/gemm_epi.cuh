@@ -212,9 +212,15 @@ static __device__ void chunk_epilogue_rows(const GemmArgs& a, int tile, int t0, 
             if (t < tn) dst[static_cast<size_t>(t) * a.n_out] = y[t];
         if (e.u_out != nullptr) {
             __nv_bfloat16* u = e.u_out + static_cast<size_t>(t0) * a.n_out + m0 + row;
+            __nv_bfloat16* ulo = e.lo_out ? e.lo_out + static_cast<size_t>(t0) * a.n_out + m0 + row : nullptr;
 #pragma unroll
             for (int t = 0; t < kChunk; ++t) {
-                if (t < tn) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(y[t], gcol));
+                if (t < tn) {
+                    const float uv = __fmul_rn(y[t], gcol);
+                    const __nv_bfloat16 hi = __float2bfloat16_rn(uv);
+                    u[static_cast<size_t>(t) * a.n_out] = hi;
+                    if (ulo) ulo[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fsub_rn(uv, __bfloat162float(hi)));
+                }
                 float sq = __fmul_rn(y[t], y[t]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
@@ -238,8 +244,11 @@ static __device__ void chunk_epilogue_rows(const GemmArgs& a, int tile, int t0, 
                 const int t = idx >> 6, f = idx & 63;
                 const float g = red[t * 128 + f], uu = red[t * 128 + 64 + f];
                 const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-                e.out_bf[static_cast<size_t>(t0 + t) * ffn + tile * 64 + f] =
-                    __float2bfloat16_rn(__fmul_rn(silu, uu));
+                const float av = __fmul_rn(silu, uu);
+                const size_t ai = static_cast<size_t>(t0 + t) * ffn + tile * 64 + f;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(av);
+                e.out_bf[ai] = hi;
+                if (e.lo_out) e.lo_out[ai] = __float2bfloat16_rn(__fsub_rn(av, __bfloat162float(hi)));
             }
         } else {  // kEpiQkvRope
             const ModelDims& md = e.m;
@@ -275,18 +284,24 @@ static __device__ void chunk_epilogue_rows(const GemmArgs& a, int tile, int t0, 
                         qd[half] = hi;
                     } else {
                         const int kh = (grow - q_dim) / hd;
-                        __nv_bfloat16* kd = e.kv_pool +
-                            kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 0, kh, s_slot[t0 + t]) + i;
-                        kd[0] = __float2bfloat16_rn(lo);
-                        kd[half] = __float2bfloat16_rn(hi);
+                        const size_t ko = kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 0, kh, s_slot[t0 + t]) + i;
+                        if (e.kv_f32) {
+                            e.kv_f32[ko] = lo;
+                            e.kv_f32[ko + half] = hi;
+                        } else {
+                            e.kv_pool[ko] = __float2bfloat16_rn(lo);
+                            e.kv_pool[ko + half] = __float2bfloat16_rn(hi);
+                        }
                     }
                 }
             } else {
                 for (int idx = tid; idx < tn * 128; idx += kEpiThreads) {
                     const int t = idx >> 7, r = idx & 127;
                     const int ve = m0 + r - q_dim - kv_dim;
-                    e.kv_pool[kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 1, ve / hd, s_slot[t0 + t]) +
-                              ve % hd] = __float2bfloat16_rn(red[t * 128 + r]);
+                    const size_t vo =
+                        kv_offset(md, e.page_size, s_page[t0 + t], e.layer, 1, ve / hd, s_slot[t0 + t]) + ve % hd;
+                    if (e.kv_f32) e.kv_f32[vo] = red[t * 128 + r];
+                    else e.kv_pool[vo] = __float2bfloat16_rn(red[t * 128 + r]);
                 }
             }
         }

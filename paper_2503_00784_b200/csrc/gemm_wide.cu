@@ -521,11 +521,12 @@ void gemm_wide_set_trace(unsigned long long* buf) {
 cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
                              int w, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                              cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};  // per device: TP ranks of one process
+    const int dev = current_device_slot();
+    if (!attr_set[dev]) {
         cudaFuncSetAttribute(gemm_wide_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         cudaFuncSetAttribute(gemm_wide_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr_set = true;
+        attr_set[dev] = true;
     }
     GemmArgs a{};
     a.n_out = n_out;

@@ -131,7 +131,7 @@ __device__ __forceinline__ void rmsnorm_row(const float* x, const float* gain, i
 // ------------------------------------------------------------ embed + norm
 __global__ void embed_norm_kernel(const PassState* ps, const __nv_bfloat16* emb,
                                   const float* gain, int d, float eps, float* x,
-                                  __nv_bfloat16* h, float* ss) {
+                                  __nv_bfloat16* h, float* ss, __nv_bfloat16* h_lo) {
     // x = E[tok]; deferred RMSNorm producer: h = bf16(x * g) and per-128-row
     // sums of squares ss[t][d/128] (same tree as the GEMM residual epilogue)
     pdl_wait();
@@ -144,7 +144,10 @@ __global__ void embed_norm_kernel(const PassState* ps, const __nv_bfloat16* emb,
         const int i = tile * 128 + (threadIdx.x & 127);
         const float v = __bfloat162float(emb[static_cast<size_t>(tok) * d + i]);
         x[static_cast<size_t>(t) * d + i] = v;
-        h[static_cast<size_t>(t) * d + i] = __float2bfloat16_rn(__fmul_rn(v, gain[i]));
+        const float uv = __fmul_rn(v, gain[i]);
+        const __nv_bfloat16 hi = __float2bfloat16_rn(uv);
+        h[static_cast<size_t>(t) * d + i] = hi;
+        if (h_lo) h_lo[static_cast<size_t>(t) * d + i] = __float2bfloat16_rn(__fsub_rn(uv, __bfloat162float(hi)));
         float sq = __fmul_rn(v, v);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
@@ -161,8 +164,9 @@ __global__ void embed_norm_kernel(const PassState* ps, const __nv_bfloat16* emb,
 }
 
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
-                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s) {
-    launch_pdl(embed_norm_kernel, dim3(w), dim3(256), 0, s, ps, emb, gain, d, eps, x, h, ss);
+                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s,
+                       __nv_bfloat16* h_lo) {
+    launch_pdl(embed_norm_kernel, dim3(w), dim3(256), 0, s, ps, emb, gain, d, eps, x, h, ss, h_lo);
 }
 
 // ------------------------------------------------------------ RMSNorm
@@ -182,32 +186,34 @@ void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, 
 }
 
 // ------------------------------------------------------------ KV compaction
-// Sequentially-ordered slot moves (src -> dst, dst <= src) for every layer,
-// K and V, kv head: one CTA per (move, layer) with moves applied in order
-// by a single launch per move index to respect overlapping chains.
-__global__ void kv_move_kernel(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                               ModelDims m, int src, int dst) {
-    const int layer = blockIdx.x;
-    const int hd = m.head_dim;
-    const int ps = page_table[src / page_size], ss = src % page_size;
-    const int pd = page_table[dst / page_size], sd = dst % page_size;
-    for (int e = threadIdx.x; e < 2 * m.n_kv_heads * hd; e += blockDim.x) {
-        const int kv = e / (m.n_kv_heads * hd);
-        const int rem = e % (m.n_kv_heads * hd);
-        const int h = rem / hd, i = rem % hd;
-        kv_pool[kv_offset(m, page_size, pd, layer, kv, h, sd) + i] =
-            kv_pool[kv_offset(m, page_size, ps, layer, kv, h, ss) + i];
-    }
+// One launch for a whole compaction: CTA = (layer, k|v, kv head), thread =
+// head-dim element, moves applied in list order.  With strictly increasing
+// dst <= src (host-checked), move i's source slot src[i] is never the
+// destination of an earlier move j < i (dst[j] <= src[j] < src[i]), so each
+// thread walking the moves in order is exact without any grid-wide barrier.
+// Element type T: bf16 pool, or the fp32 pool of fp32-accumulate mode.
+template <typename T>
+__global__ void kv_compact_kernel(T* pool, const int32_t* page_table, int page_size, ModelDims m,
+                                  const int32_t* src, const int32_t* dst, int n) {
+    const int layer = blockIdx.x, kv = blockIdx.y, h = blockIdx.z;
+    for (int i = threadIdx.x; i < m.head_dim; i += blockDim.x)
+        for (int k = 0; k < n; ++k) {
+            const int sp = src[k], dp = dst[k];
+            if (sp == dp) continue;
+            const T v = pool[kv_offset(m, page_size, page_table[sp / page_size], layer, kv, h, sp % page_size) + i];
+            pool[kv_offset(m, page_size, page_table[dp / page_size], layer, kv, h, dp % page_size) + i] = v;
+        }
 }
 
-void launch_kv_compact(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                       const ModelDims& m, const int32_t* src_pos, const int32_t* dst_pos, int n,
-                       cudaStream_t s) {
-    for (int i = 0; i < n; ++i) {
-        if (src_pos[i] == dst_pos[i]) continue;
-        kv_move_kernel<<<m.n_layers, 256, 0, s>>>(kv_pool, page_table, page_size, m, src_pos[i],
-                                                  dst_pos[i]);
-    }
+void launch_kv_compact(__nv_bfloat16* kv_pool, float* kv_f32, const int32_t* page_table,
+                       int page_size, const ModelDims& m, const int32_t* src_pos_d,
+                       const int32_t* dst_pos_d, int n, cudaStream_t s) {
+    const dim3 grid(m.n_layers, 2, m.n_kv_heads);
+    if (kv_f32)
+        kv_compact_kernel<float><<<grid, 128, 0, s>>>(kv_f32, page_table, page_size, m, src_pos_d, dst_pos_d, n);
+    else
+        kv_compact_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(kv_pool, page_table, page_size, m, src_pos_d,
+                                                            dst_pos_d, n);
 }
 
 }  // namespace dd

@@ -55,8 +55,17 @@ void launch_init_head(__nv_bfloat16* head, const __nv_bfloat16* emb, const int32
                       cudaStream_t s, uint64_t v0 = 0);
 void launch_fill_f32(float* dst, size_t n, float v, cudaStream_t s);
 
+// h_lo (fp32-accumulate mode): bf16(x*g - h), or nullptr
 void launch_embed_norm(const PassState* ps, int w, const __nv_bfloat16* emb, const float* gain,
-                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s);
+                       int d, float eps, float* x, __nv_bfloat16* h, float* ss, cudaStream_t s,
+                       __nv_bfloat16* h_lo = nullptr);
+constexpr int kMaxF32AttnKeys = 48 * 1024;  // fp32acc mode: scores of one query row in shared memory
+// fp32-accumulate mode attention (attention_f32.cu): fp32 q, fp32 paged KV,
+// fp32 softmax on CUDA cores; writes o as bf16 hi + lo halves.
+int launch_attention_f32(const PassState* ps, int w, const ModelDims& m, const float* q,
+                         const float* kv_f32, const int32_t* page_table, int page_size,
+                         int layer, int max_keys, __nv_bfloat16* o, __nv_bfloat16* o_lo,
+                         cudaStream_t s);
 // Split-KV tensor-core attention with a cluster/DSMEM merge (attention.cu);
 // returns 0, or nonzero for an unsupported head_dim / launch failure.
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
@@ -67,9 +76,10 @@ void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, 
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,
                                     uint64_t seed, float amp, int offset, cudaStream_t s,
                                     uint64_t src_row0 = 0);
-void launch_kv_compact(__nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                       const ModelDims& m, const int32_t* src_pos, const int32_t* dst_pos, int n,
-                       cudaStream_t s);
+// src / dst: device arrays of n slot moves, dst strictly increasing, dst <= src
+void launch_kv_compact(__nv_bfloat16* kv_pool, float* kv_f32, const int32_t* page_table,
+                       int page_size, const ModelDims& m, const int32_t* src_pos_d,
+                       const int32_t* dst_pos_d, int n, cudaStream_t s);
 
 // KV pool addressing: pool[page][layer][k|v][kv_head][page_size][head_dim]
 __host__ __device__ inline size_t kv_offset(const ModelDims& m, int page_size, int page,

@@ -1143,12 +1143,13 @@ int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
 cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
                                const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
                                cudaStream_t s) {
-    static int attr_set = 0;
-    if (attr_set < smem_bytes) {
+    static int attr_set[kMaxDevices] = {};  // per device: TP ranks of one process
+    const int dev = current_device_slot();
+    if (attr_set[dev] < smem_bytes) {
         cudaError_t e = cudaFuncSetAttribute(pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem_bytes);
         if (e != cudaSuccess) return e;
-        attr_set = smem_bytes;
+        attr_set[dev] = smem_bytes;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kNumSMs, 1, 1);

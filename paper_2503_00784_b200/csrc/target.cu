@@ -79,7 +79,7 @@ const GemmPlan& plan_for(dd_ctx* c, int id, int nt) {
     if (it != c->plans.end()) return it->second;
     int n_out, k;
     gemm_shape(c, id, &n_out, &k);
-    return c->plans[key] = plan_gemm(n_out, k, nt);
+    return c->plans[key] = plan_gemm(n_out, k, nt, c->fp32acc ? 1 : 0);
 }
 
 }  // namespace
@@ -112,7 +112,11 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
         int n_out, k;
         gemm_shape(ctx, id, &n_out, &k);
         cudaError_t r;
-        if (wide) {
+        if (ctx->fp32acc) {  // split activations: hi + lo MMAs into one accumulator
+            const CUtensorMap* lo = mx == &ctx->map_h ? &ctx->map_h_lo
+                                    : mx == &ctx->map_o ? &ctx->map_o_lo : &ctx->map_a_lo;
+            r = launch_gemm(mw, mx, n_out, k, w, nt, plan_for(ctx, id, nt), ctx->ws, ep, s, lo);
+        } else if (wide) {
             const CUtensorMap* m128 = mx == &ctx->map_h ? &ctx->map_h128
                                       : mx == &ctx->map_o ? &ctx->map_o128 : &ctx->map_a128;
             r = launch_gemm_wide(mw, m128, n_out, k, w, ctx->wide_plans[id], ctx->ws_wide, ep, s);
@@ -151,29 +155,37 @@ int enqueue_pass_impl(dd_ctx* ctx, int w, bool want_logits, Mark mark) {
     e.eps = m.eps;
     e.norm_d = m.d;
     launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, ctx->ss,
-                      s);
+                      s, ctx->h_lo);
     mark(2);
+    if (ctx->fp32acc) e.kv_f32 = ctx->kv_f32;
     for (int l = 0; l < m.n_layers; ++l) {
         const LayerW& L = ctx->layers[l];
         GemmEpiParams eq = e;
         eq.kind = kEpiQkvRope;
         eq.layer = l;
         CK(gemm(kGQkv, L.qkv, &ctx->map_h, eq));
-        if (launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table,
-                             ctx->page_size, l, ctx->o, s, attn_ranks(ctx, w)))
+        if (ctx->fp32acc) {
+            if (launch_attention_f32(ctx->d_ps, w, m, ctx->q, ctx->kv_f32, ctx->page_table,
+                                     ctx->page_size, l, ctx->max_seq, ctx->o, ctx->o_lo, s))
+                return ctx_fail(ctx, DD_E_CUDA, "fp32 attention launch failed");
+        } else if (launch_attention(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table,
+                                    ctx->page_size, l, ctx->o, s, attn_ranks(ctx, w))) {
             return ctx_fail(ctx, DD_E_CUDA, "attention launch failed");
+        }
         mark(1);
         GemmEpiParams er = e;  // residual add; writes u = bf16(x*g) + ss partials
         er.kind = kEpiResidual;
         er.out = ctx->x;
         er.ss_in = nullptr;
         er.u_out = ctx->h;
+        er.lo_out = ctx->h_lo;
         er.gain = ctx->gain_ones;
         er.ss_out = ctx->ss;
         CK(row_parallel(kGO, L.o, &ctx->map_o, er));
         GemmEpiParams eg = e;
         eg.kind = kEpiSwiGLU;
         eg.out_bf = ctx->a;
+        eg.lo_out = ctx->a_lo;
         CK(gemm(kGGu, L.gu, &ctx->map_h, eg));
         CK(row_parallel(kGDown, L.dn, &ctx->map_a, er));
     }
@@ -533,6 +545,10 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         d.vocab / 128 < tp_size)
         return ctx_fail(nullptr, DD_E_ARG, "shape does not split over the tensor-parallel ranks");
     const int h_l = d.n_heads / tp_size, kv_l = n_kv / tp_size, ffn_l = d.ffn_dim / tp_size;
+    if (d.precision != DD_PREC_BF16 && d.precision != DD_PREC_FP32ACC)
+        return ctx_fail(nullptr, DD_E_ARG, "unknown precision mode");
+    if (d.precision == DD_PREC_FP32ACC && (tp_size != 1 || d.max_seq > kMaxF32AttnKeys))
+        return ctx_fail(nullptr, DD_E_ARG, "fp32-accumulate mode needs tp_size 1 and max_seq <= 49152");
     if (d.n_layers < 1 || d.d_model % 128 || d.head_dim % 32 || d.head_dim > 256 ||
         d.n_heads % std::max(1, n_kv) || (tp_size == 1 && d.ffn_dim % 128) || d.vocab % 128 ||
         (h_l * d.head_dim) % 128 || (kv_l * d.head_dim) % 128 ||
@@ -548,6 +564,8 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         return ctx_fail(nullptr, DD_E_CUDA, "device is not sm_100 (Blackwell)");
     ctx = new dd_ctx();
     ctx->device = cuda_device;
+    ctx->fp32acc = d.precision == DD_PREC_FP32ACC;
+    ctx->sm_count = prop.multiProcessorCount;
     CK(cudaSetDevice(cuda_device));
     ctx->tp_rank = tp_rank;
     ctx->tp_size = tp_size;
@@ -605,6 +623,18 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         make_tmap_bf16(&ctx->map_o128, ctx->o, R, m.q_dim(), 128) ||
         make_tmap_bf16(&ctx->map_a128, ctx->a, R, m.ffn, 128))
         return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    if (ctx->fp32acc) {
+        CK(cudaMalloc(&ctx->h_lo, sizeof(__nv_bfloat16) * R * d_));
+        CK(cudaMalloc(&ctx->o_lo, sizeof(__nv_bfloat16) * R * m.q_dim()));
+        CK(cudaMalloc(&ctx->a_lo, sizeof(__nv_bfloat16) * R * m.ffn));
+        CK(cudaMemset(ctx->h_lo, 0, sizeof(__nv_bfloat16) * R * d_));
+        CK(cudaMemset(ctx->o_lo, 0, sizeof(__nv_bfloat16) * R * m.q_dim()));
+        CK(cudaMemset(ctx->a_lo, 0, sizeof(__nv_bfloat16) * R * m.ffn));
+        if (make_tmap_bf16(&ctx->map_h_lo, ctx->h_lo, R, d_, 16) ||
+            make_tmap_bf16(&ctx->map_o_lo, ctx->o_lo, R, m.q_dim(), 16) ||
+            make_tmap_bf16(&ctx->map_a_lo, ctx->a_lo, R, m.ffn, 16))
+            return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed");
+    }
     size_t ws_floats = 0;
     for (int id = 0; id < kNumGemm; ++id) {
         int n_out, k;
@@ -627,7 +657,8 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
             ctx->wide_plans[id] = plan_gemm_wide(n_out, k);
             wide_floats = std::max(wide_floats, gemm_wide_ws_floats(ctx->wide_plans[id]));
         }
-        if (ok) CK(cudaMalloc(&ctx->ws_wide, sizeof(float) * wide_floats));
+        // (fp32-accumulate mode runs every width on the split-activation GEMM)
+        if (ok && !ctx->fp32acc) CK(cudaMalloc(&ctx->ws_wide, sizeof(float) * wide_floats));
     }
     CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
     CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
@@ -648,7 +679,8 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     // paged KV cache (all pages reserved up front; page table maps logical->physical)
     const size_t kv_elems = static_cast<size_t>(ctx->n_pages) * m.n_layers * 2 * m.n_kv_heads *
                             ctx->page_size * m.head_dim;
-    CK(cudaMalloc(&ctx->kv_pool, sizeof(__nv_bfloat16) * kv_elems));
+    CK(cudaMalloc(&ctx->kv_pool, sizeof(__nv_bfloat16) * (ctx->fp32acc ? 1 : kv_elems)));
+    if (ctx->fp32acc) CK(cudaMalloc(&ctx->kv_f32, sizeof(float) * kv_elems));
     std::vector<int32_t> pt(ctx->n_pages);
     for (int i = 0; i < ctx->n_pages; ++i) pt[i] = i;
     CK(cudaMalloc(&ctx->page_table, sizeof(int32_t) * ctx->n_pages));
@@ -660,7 +692,11 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         const char* env = getenv("DD_PASS_KERNEL");
         // the persistent pass kernel has no cross-rank reduction (tp.h): sharded
         // contexts run one launch per GEMM / attention / reduction
-        ctx->use_pass_kernel = !(env && env[0] == '0') && tp_size == 1;
+        // (fp32-accumulate mode: split activations run on the per-launch GEMM; a
+        // partitioned device with fewer SMs than the persistent grid cannot
+        // co-schedule its 148 CTAs)
+        ctx->use_pass_kernel = !(env && env[0] == '0') && tp_size == 1 && !ctx->fp32acc &&
+                               ctx->sm_count >= kNumSMs;
         // embed + per layer (qkv, attention, o, gate/up, down) + head
         const size_t per_layer = m.qkv_rows() / 128 + m.n_heads * 16 + m.d / 128 + 2 * m.ffn / 128 + m.d / 128;
         const size_t n_flags = m.d / 128 + per_layer * m.n_layers + m.vocab / 128;
@@ -712,6 +748,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     CK(cudaHostAlloc(&ctx->h_out, sizeof(dd_verify_out), cudaHostAllocDefault));
     CK(cudaMalloc(&ctx->q_rows, sizeof(float) * kMaxPassTokens * ctx->vocab));
     CK(cudaMalloc(&ctx->d_tail, sizeof(int32_t) * kMaxPassTokens));
+    CK(cudaMalloc(&ctx->d_compact_dst, sizeof(int32_t) * kMaxPassTokens));
     CK(cudaHostAlloc(&ctx->h_q_stage, sizeof(float) * kMaxPassTokens * ctx->vocab,
                      cudaHostAllocDefault));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -740,7 +777,8 @@ void dd_ctx_destroy(dd_ctx* ctx) {
                    ctx->rope_sin, ctx->d_ps, ctx->row_m, ctx->row_sum, ctx->row_argmax,
                    ctx->ticket, ctx->d_out, ctx->q_rows, ctx->d_tail, ctx->d_probs,
                    ctx->counters, ctx->ss, ctx->ws_wide, ctx->pass_flags, ctx->pass_ws, ctx->pass_counters,
-                   ctx->attn_part, ctx->attn_cnt, ctx->sk_prefix_d, ctx->rank_of_smid_d};
+                   ctx->attn_part, ctx->attn_cnt, ctx->sk_prefix_d, ctx->rank_of_smid_d,
+                   ctx->h_lo, ctx->o_lo, ctx->a_lo, ctx->kv_f32, ctx->d_compact_dst};
     for (void* p : dev)
         if (p) cudaFree(p);
     for (void* p : ctx->tp_opened) cudaIpcCloseMemHandle(p);
@@ -912,13 +950,26 @@ int dd_kv_truncate(dd_ctx* ctx, int n_valid) {
 int dd_kv_compact(dd_ctx* ctx, const int32_t* src_pos, const int32_t* dst_pos, int n) {
     if (!ctx || n < 0 || (n > 0 && (!src_pos || !dst_pos)))
         return ctx_fail(ctx, DD_E_ARG, "bad arguments");
-    for (int i = 0; i < n; ++i)
+    if (n > kMaxPassTokens) return ctx_fail(ctx, DD_E_CAPACITY, "at most 256 moves per compaction");
+    for (int i = 0; i < n; ++i) {
         if (src_pos[i] < 0 || src_pos[i] >= ctx->n_cached || dst_pos[i] < 0 ||
             dst_pos[i] >= ctx->n_cached)
             return ctx_fail(ctx, DD_E_ARG, "compaction slot outside the cache");
+        if (dst_pos[i] > src_pos[i] || (i > 0 && dst_pos[i] <= dst_pos[i - 1]))
+            return ctx_fail(ctx, DD_E_ARG, "compaction needs strictly increasing dst <= src");
+    }
+    if (n == 0) return DD_OK;
     CK(cudaSetDevice(ctx->device));
-    launch_kv_compact(ctx->kv_pool, ctx->page_table, ctx->page_size, ctx->m, src_pos, dst_pos, n,
-                      ctx->stream);
+    // moves staged through the (idle between passes) tail-token buffers
+    int32_t* stage = ctx->h_ps[ctx->ps_slot].tokens;
+    CK(cudaEventSynchronize(ctx->ps_done[ctx->ps_slot]));
+    std::memcpy(stage, src_pos, sizeof(int32_t) * n);
+    CK(cudaMemcpyAsync(ctx->d_tail, stage, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(stage, dst_pos, sizeof(int32_t) * n);
+    CK(cudaMemcpyAsync(ctx->d_compact_dst, stage, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+    launch_kv_compact(ctx->kv_pool, ctx->kv_f32, ctx->page_table, ctx->page_size, ctx->m, ctx->d_tail,
+                      ctx->d_compact_dst, n, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     return DD_OK;

@@ -42,16 +42,18 @@ __device__ __forceinline__ unsigned long long now_ns() {
 // Signal op `expected` to every rank (CTA 0), then wait for every rank's
 // signal.  A peer that never arrives (dead process, mismatched pass
 // sequence) traps after 10 s instead of hanging the GPU.
-__device__ void tp_barrier(const TpPeers& P, int expected) {
+// Flag values are the op's sequence number mod 2^32 (epoch * ops + op + 1
+// wraps after ~13M 70B passes), compared wrap-safely.
+__device__ void tp_barrier(const TpPeers& P, unsigned expected) {
     const int tid = threadIdx.x;
     if (blockIdx.x == 0 && tid < P.size) {
         __threadfence_system();
-        st_release_sys(P.flags[tid] + P.rank * kTpFlagStride, expected);
+        st_release_sys(P.flags[tid] + P.rank * kTpFlagStride, static_cast<int>(expected));
     }
     if (tid < P.size) {
         const int* f = P.flags[P.rank] + tid * kTpFlagStride;
         const unsigned long long t0 = now_ns();
-        while (ld_acquire_sys(f) < expected) {
+        while (static_cast<int>(static_cast<unsigned>(ld_acquire_sys(f)) - expected) < 0) {
             __nanosleep(64);
             if (now_ns() - t0 > 10000000000ull) __trap();
         }
@@ -65,7 +67,8 @@ __global__ void __launch_bounds__(128) tp_reduce_residual_kernel(
     TpPeers P, const PassState* ps, int op, int ops_per_pass, int d, float* x, __nv_bfloat16* u,
     const float* gain, float* ss_out) {
     const int w = ps->w;
-    tp_barrier(P, ps->epoch * ops_per_pass + op + 1);
+    tp_barrier(P, static_cast<unsigned>(ps->epoch) * static_cast<unsigned>(ops_per_pass) +
+                      static_cast<unsigned>(op) + 1u);
     __shared__ float part[4];
     const int tile = blockIdx.x, tid = threadIdx.x, col = tile * 128 + tid;
     const int tiles = d / 128;
@@ -99,7 +102,8 @@ __global__ void __launch_bounds__(256) tp_gather_logits_kernel(TpPeers P, const 
                                                                int op, int ops_per_pass, int vocab,
                                                                float* logits) {
     const int w = ps->w;
-    tp_barrier(P, ps->epoch * ops_per_pass + op + 1);
+    tp_barrier(P, static_cast<unsigned>(ps->epoch) * static_cast<unsigned>(ops_per_pass) +
+                      static_cast<unsigned>(op) + 1u);
     const size_t n = static_cast<size_t>(w) * vocab;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {

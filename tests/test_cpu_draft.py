@@ -73,3 +73,48 @@ def test_draft_prefill_vnni_path_bit_exact(draft, tmp_path):
     o = orc.forward(np.random.default_rng(2).integers(0, SHAPE["vocab"], 230).tolist())
     orc.close()
     assert np.array_equal(np.load(tmp_path / "g.npy"), o[-1])
+
+
+@pytest.mark.parametrize("budget,s_max,temp", [(8, 4, 1.0), (6, 8, 1.0), (5, 2, 0.7),
+                                               (12, 4, 1.5), (3, 4, 1.0), (16, 16, 2.0)])
+def test_engine_draft_dynamic_matches_reference(draft, budget, s_max, temp):
+    """The engine's C++ draft_dynamic (csrc/engine.cpp) vs the restated
+    reference drafting (oracle/protocol.py draft_dynamic, pinned to the
+    compiled reference by test_golden / test_oracle_vs_ref), with the same q
+    rows: sequence count, admission order, even split with the remainder on
+    the top sequence, sampled continuations in sequence-major draw order,
+    probe reuse (forward count), theta, and the draft stream's counter
+    (proj/src/drafting.cpp:71-136)."""
+    from oracle import protocol as P
+    rng = np.random.default_rng(budget * 100 + s_max)
+    multi = 0
+    for trial in range(12):
+        ctx = rng.integers(0, SHAPE["vocab"], int(rng.integers(3, 40))).tolist()
+        seed, counter = int(rng.integers(1, 2**63)), int(rng.integers(0, 1000))
+        got = draft.draft_dynamic(ctx, budget, s_max, seed, counter, temperature=temp)
+
+        def fwd(c):
+            return draft.dist(c, temperature=temp)[0].astype(np.float64)
+        rs = P.RandomStream(seed, counter)
+        want = P.draft_dynamic(fwd, ctx, budget, s_max, rs)
+        assert got["seqs"] == [list(s.tokens) for s in want.sequences], trial
+        assert got["threshold"] == want.threshold
+        assert got["forwards"] == want.forwards_used
+        assert got["counter"] == rs.counter
+        assert sum(map(len, got["seqs"])) == budget
+        multi += len(got["seqs"]) > 1
+    if s_max > 1 and budget > 1:
+        assert multi > 0, "no multi-sequence bundle exercised"
+
+
+def test_engine_draft_dynamic_greedy(draft):
+    """Greedy drafting: one sequence, the draft's argmax chain, no draws."""
+    ctx = [5, 17, 300, 2]
+    got = draft.draft_dynamic(ctx, 6, 4, seed=1, counter=3, greedy=True)
+    assert len(got["seqs"]) == 1 and got["counter"] == 3 + 5
+    chain, c = [], list(ctx)
+    for _ in range(6):
+        t = int(np.argmax(draft.logits(c)))
+        chain.append(t)
+        c.append(t)
+    assert got["seqs"][0] == chain

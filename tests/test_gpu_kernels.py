@@ -86,7 +86,7 @@ def test_tiny_pass_logits_vs_oracle(tiny_pair):
     g = tgt.logits(0, len(new))
     o = orc.forward(new)
     rel = np.abs(g - o).max() / np.abs(o).max()
-    assert rel < 2e-3, f"relative logit error {rel}"
+    assert rel < 5e-4, f"relative logit error {rel}"
     assert (g.argmax(-1) == o.argmax(-1)).mean() >= 6 / 7
 
 
@@ -141,7 +141,8 @@ def test_tiny_pass_logits_all_paths(tiny_pair, w):
     g = tgt.logits(0, w)
     o = orc.forward(new)
     rel = np.abs(g - o).max() / np.abs(o).max()
-    assert rel < 2e-3, f"W={w}: relative logit error {rel}"
+    bar = 5e-4 if w >= 8 else 3e-3  # stated bf16 tolerance (tests/test_gpu_hd128.py)
+    assert rel < bar, f"W={w}: relative logit error {rel}"
 
 
 def test_long_context_attention_vs_oracle(tiny_pair):
@@ -159,7 +160,7 @@ def test_long_context_attention_vs_oracle(tiny_pair):
     g = tgt.logits(0, len(new))
     o = orc.forward(new)
     rel = np.abs(g - o).max() / np.abs(o).max()
-    assert rel < 2e-3, f"relative logit error {rel}"
+    assert rel < 5e-4, f"relative logit error {rel}"
 
 
 def test_pass_kernel_matches_per_launch_path(tiny_pair, monkeypatch):

@@ -87,7 +87,7 @@ def test_tp_logits_vs_oracle(group, w):
     o = orc.forward(new)
     orc.close()
     rel = np.abs(g0 - o).max() / np.abs(o).max()
-    assert rel < 2e-3, f"relative logit error {rel}"
+    assert rel < (5e-4 if w >= 8 else 3e-3), f"relative logit error {rel}"  # bf16 tolerance
     assert (g0.argmax(-1) == o.argmax(-1)).mean() >= 0.85
 
 
@@ -168,4 +168,29 @@ def test_tp_two_processes_ipc(tmp_path):
     orc.forward(spec["prompt"])
     o = orc.forward(spec["new"])
     orc.close()
-    assert np.abs(g0 - o).max() / np.abs(o).max() < 2e-3
+    assert np.abs(g0 - o).max() / np.abs(o).max() < 5e-4
+
+
+@pytest.mark.parametrize("n_ctx,w", [(40, 1), (40, 8), (300, 16), (40, 40)])
+def test_tp_gqa128_vs_oracle(n_ctx, w):
+    """TP=2 on the head_dim-128, 8:1 GQA shape (per rank: 8 q heads over one
+    kv head, the 70B's TP=8 geometry), against the unsharded oracle."""
+    shape = SHAPES["gqa128"]
+    ranks = [Target(shape, weight_seed=SEED, plant=PLANT, max_seq=512, tp_rank=r, tp_size=2)
+             for r in range(2)]
+    Target.tp_connect_local(ranks)
+    rng = np.random.default_rng(500 + n_ctx + w)
+    prompt = rng.integers(0, shape["vocab"], n_ctx).tolist()
+    new = rng.integers(0, shape["vocab"], w).tolist()
+    each(ranks, lambda t: t.prefill(prompt))
+    each(ranks, lambda t: t.score(new))
+    g0, g1 = ranks[0].logits(0, w), ranks[1].logits(0, w)
+    for t in ranks:
+        t.close()
+    assert np.array_equal(g0, g1), "ranks disagree"
+    orc = OracleLlama(shape, weight_seed=SEED, plant=PLANT, max_seq=512, threads=8)
+    orc.forward(prompt, last_only=True)
+    o = orc.forward(new)
+    orc.close()
+    rel = np.abs(g0 - o).max() / np.abs(o).max()
+    assert rel < (5e-4 if w >= 8 else 3e-3), f"relative logit error {rel}"  # bf16 tolerance

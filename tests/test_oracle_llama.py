@@ -68,6 +68,24 @@ def test_oracle_matches_transformers(shape):
     assert cc > 0.999
 
 
+@pytest.mark.parametrize("shape", [SHAPE, GQA], ids=["mha", "gqa"])
+def test_oracle_fp32_mode_matches_transformers(shape):
+    """fp32 mode (no bf16 activation / KV rounding) vs transformers fp32 at
+    the north star's fp32-accumulate bar (1e-4 of max |logit|): pins the
+    forward math itself, not just its bf16 approximation."""
+    orc = OracleLlama(shape, weight_seed=17, plant=PLANT, max_seq=256, threads=4, fp32=True)
+    m, torch = hf_model(orc, shape)
+    rng = np.random.default_rng(0)
+    toks = rng.integers(0, shape["vocab"], 40).tolist()
+    orc.forward(toks[:30])
+    o = orc.forward(toks[30:])
+    with torch.no_grad():
+        h = m(torch.tensor([toks])).logits[0, 30:].numpy()
+    rel = np.abs(o - h).max() / np.abs(h).max()
+    assert rel < 1e-4, rel
+    assert (o.argmax(-1) == h.argmax(-1)).all()
+
+
 def test_oracle_scored_pass_equals_sequential():
     """forward_scored contract (model.hpp:61-65): a W-token pass == W one-token passes."""
     orc = OracleLlama(SHAPE, weight_seed=5, max_seq=128, threads=4)
