@@ -164,26 +164,61 @@ def decode_stats(res):
 
 
 # ---------------------------------------------------------------- CPU side
-def cpu_decode_sample(shape_t, shape_d, plant, budget, threads, sample_tokens, prefilled=None):
-    """The all-CPU restated reference loop (oracle/cpu_engine.py) on host cores:
-    returns (decode tok/s, description, cores)."""
-    from oracle.cpu_engine import run_cpu
+CPU_HARD_CAP = 16  # the config-2 GPU arm's budget_hard_cap: both arms use the same budget rule
+
+
+def cpu_models(plant, threads, max_seq):
+    """The CPU oracle Llama as 7B target and 68M draft (test infrastructure
+    only: the all-CPU reference path the north star times beside the GPU)."""
     from oracle.llama import OracleLlama
-    tgt = prefilled[0] if prefilled else OracleLlama(shape_t, SEED_W_TARGET, plant,
-                                                      max_seq=PROMPT_LEN + 512, threads=threads)
-    drf = prefilled[1] if prefilled else OracleLlama(shape_d, SEED_W_DRAFT, plant,
-                                                      max_seq=PROMPT_LEN + 512, threads=threads)
-    prompt = make_prompt(1)
-    r = run_cpu("duo", tgt, drf, prompt, budget, 4, sample_tokens, greedy=True)
-    first = r["iterations"][0]
-    dec_tok = len(r["tokens"]) - first
+    from paper_2503_00784_b200 import SHAPES
+    tgt = OracleLlama(SHAPES["llama2_7b"], SEED_W_TARGET, plant, max_seq=max_seq, threads=threads)
+    drf = OracleLlama(SHAPES["llama_68m"], SEED_W_DRAFT, plant, max_seq=max_seq,
+                      threads=max(1, min(4, threads // 4)))
+    return tgt, drf
+
+
+def cpu_calibrate(tgt, drf, probe_len=8, trials=3, hard_cap=CPU_HARD_CAP):
+    """calibrate + choose_budget (proj/src/engine.cpp:534-582) on host cores:
+    median target scored pass at probe_len over median single-token draft
+    forward, budget = max(2, round(c)) capped like the GPU arm."""
+    ctx = make_prompt(5, PROMPT_LEN)
+    tgt.truncate(0)
+    tgt.forward(ctx, last_only=True)
+    drf.truncate(0)
+    drf.forward(ctx, last_only=True)
+    tp, td = [], []
+    for i in range(trials):
+        tgt.truncate(PROMPT_LEN)
+        t0 = time.perf_counter()
+        tgt.forward(list(range(probe_len)))
+        tp.append(time.perf_counter() - t0)
+        drf.truncate(PROMPT_LEN)
+        t0 = time.perf_counter()
+        drf.forward([i], last_only=True)
+        td.append(time.perf_counter() - t0)
+    c = statistics.median(tp) / max(1e-9, statistics.median(td))
+    return c, min(max(2, int(c + 0.5)), hard_cap)
+
+
+def cpu_run(mode, tgt, drf, prompt, budget, n_tokens):
+    """One CPU generation (oracle/cpu_engine.py, threaded duo): decode tok/s
+    (tokens after iteration 1 over the time after iteration 1), TTFT, tokens."""
+    from oracle.cpu_engine import run_cpu
+    r = run_cpu(mode, tgt, drf if mode != "vanilla" else None, prompt, budget, 4, n_tokens,
+                greedy=True, threaded=True)
+    dec = len(r["tokens"]) - r["iterations"][0]
     dec_ms = r["total_ms"] - r["ttft_ms"]
-    return dec_tok / (dec_ms / 1e3), r, (tgt, drf)
+    return dict(decode_tps=dec / max(1e-9, dec_ms / 1e3), dec_tokens=dec, dec_ms=dec_ms,
+                ttft_ms=r["ttft_ms"], tokens=r["tokens"])
 
 
 def run_reference(args):
     """--impl reference: the reference's loop restated on the CPU oracle (the
-    reference itself runs only Markov tables), all host threads, rank 0 only."""
+    reference itself runs only Markov tables), all host threads, rank 0 only.
+    Same workload as the GPU arm: config-2 prompts (make_prompt(step + 1)),
+    greedy duo, budget from the same calibrate / choose_budget rule and hard
+    cap, each step a bounded sample (the first --ref-tokens new tokens)."""
     ws, rank, _ = dist_env()
     if ws > 1:
         import torch.distributed as dist
@@ -191,24 +226,21 @@ def run_reference(args):
         if rank != 0:
             dist.barrier()
             return
-    from paper_2503_00784_b200 import DEFAULT_PLANT, SHAPES
+    from paper_2503_00784_b200 import DEFAULT_PLANT
     threads = len(os.sched_getaffinity(0))
-    plant = dict(DEFAULT_PLANT)
-    budget = args.budget or 8
-    from oracle.cpu_engine import run_cpu
-    from oracle.llama import OracleLlama
-    tgt = OracleLlama(SHAPES["llama2_7b"], SEED_W_TARGET, plant, PROMPT_LEN + 512, threads)
-    drf = OracleLlama(SHAPES["llama_68m"], SEED_W_DRAFT, plant, PROMPT_LEN + 512, threads)
-    prompt = make_prompt(1)
+    plant = dict(DEFAULT_PLANT, alpha=args.alpha)
+    tgt, drf = cpu_models(plant, threads, PROMPT_LEN + args.ref_tokens + 64)
+    if args.budget:
+        coef, budget = None, args.budget
+    else:
+        coef, budget = cpu_calibrate(tgt, drf)
     rates = []
     for step in range(args.warmup + args.steps):
-        r = run_cpu("duo", tgt, drf, prompt, budget, 4, args.ref_tokens, greedy=True)
-        dec = len(r["tokens"]) - r["iterations"][0]
-        rate = dec / ((r["total_ms"] - r["ttft_ms"]) / 1e3)
+        r = cpu_run("duo", tgt, drf, make_prompt(step + 1), budget, args.ref_tokens)
         if step >= args.warmup:
-            rates.append((dec, r["total_ms"] - r["ttft_ms"], r["ttft_ms"]))
-    tok = sum(x[0] for x in rates)
-    ms = sum(x[1] for x in rates)
+            rates.append(r)
+    tok = sum(x["dec_tokens"] for x in rates)
+    ms = sum(x["dec_ms"] for x in rates)
     value = tok / (ms / 1e3)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
@@ -216,15 +248,17 @@ def run_reference(args):
         "ms_per_step": round(ms / len(rates), 2), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16 weights / fp32 compute (CPU)", "data": "synthetic",
         "config": {"workload": "config2 on host cores: restated reference duo loop "
-                                "(oracle/cpu_engine.py) with the CPU Llama oracle as target "
-                                "and draft", "prompt_len": PROMPT_LEN,
-                   "decode_tokens_per_step": args.ref_tokens, "budget": budget, "greedy": True,
-                   "alpha": plant["alpha"]},
-        "ttft_p50_ms": round(statistics.median(x[2] for x in rates), 1),
+                                "(oracle/cpu_engine.py, threaded draft worker) with the CPU "
+                                "Llama oracle as 7B target and 68M draft",
+                   "prompt_len": PROMPT_LEN, "prompts": "make_prompt(step + 1), as the GPU arm",
+                   "decode_tokens_per_step": args.ref_tokens, "budget": budget,
+                   "calibrated_c": coef, "budget_hard_cap": CPU_HARD_CAP, "greedy": True,
+                   "alpha": plant["alpha"], "same_config": True},
+        "ttft_p50_ms": round(statistics.median(x["ttft_ms"] for x in rates), 1),
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{args.ref_tokens} new tokens after a 128-token prompt per "
-                                   f"step, decode phase timed (prefill excluded)"},
+                         "sample": f"first {args.ref_tokens} new tokens after the 128-token "
+                                   f"prompt per step (of the GPU arm's 128), decode phase timed"},
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -281,8 +315,11 @@ def run_ours(args):
     def one(step):  # a TP group serves one stream: every rank gets the same prompt
         return run_generation(tgt, drf, make_prompt(1000 * (0 if tp else rank) + step + 1), cfg)
 
+    first_tokens = []
     for s in range(args.warmup):
-        one(s)
+        r0 = one(s)
+        if s == 0:
+            first_tokens = list(r0.tokens)
     if dist:
         dist.barrier()
     results, walls = [], []
@@ -370,16 +407,38 @@ def run_ours(args):
                 "budget": bud, "runs": n_base}
         extra["gpu_baselines"] = base
         if ws == 1 and not args.no_cpu_baseline and args.workload == "config2":
-            thr = os.cpu_count()
+            # the reference's all-CPU path on this box's host cores, same run:
+            # vanilla, SpS and threaded duo at the GPU arm's budget on the
+            # GPU's first prompt (make_prompt(1)), bounded samples
+            n = args.cpu_tokens
+            if len(first_tokens) < n:  # no warm-up step ran make_prompt(1)
+                first_tokens = list(run_generation(tgt, drf, make_prompt(1), cfg).tokens)
+            drf.close()  # the GPU arm's draft pool must not compete for the host cores
+            thr = len(os.sched_getaffinity(0) | set(range(os.cpu_count())))
             os.sched_setaffinity(0, set(range(os.cpu_count())))
-            rate, r, _ = cpu_decode_sample(SHAPES["llama2_7b"], SHAPES["llama_68m"], plant,
-                                           budget, thr, args.cpu_tokens)
+            ctm, cdm = cpu_models(plant, thr, PROMPT_LEN + args.cpu_tokens + 64)
+            cpu = {m: cpu_run(m, ctm, cdm, make_prompt(1), budget if m == "duo" else
+                              max(2, min(budget // 2, 12)), args.cpu_tokens)
+                   for m in ("duo", "vanilla", "sps")}
+            ctm.close()
+            cdm.close()
             extra["cpu_baseline"] = {
-                "value": round(rate, 3), "unit": "tokens/s", "cores": thr, "kind": "port",
-                "sample": f"restated reference duo loop (oracle/cpu_engine.py) with the CPU "
-                          f"Llama oracle as 7B target and 68M draft: {args.cpu_tokens} new "
-                          f"tokens after the 128-token prompt, decode phase timed; "
-                          f"prefill/TTFT {r['ttft_ms'] / 1e3:.1f} s"}
+                "value": round(cpu["duo"]["decode_tps"], 3), "unit": "tokens/s", "cores": thr,
+                "kind": "port",
+                "sample": f"restated reference loop (oracle/cpu_engine.py, threaded duo) with "
+                          f"the CPU Llama oracle as 7B target and 68M draft, prompt "
+                          f"make_prompt(1), first {args.cpu_tokens} new tokens, decode phase "
+                          f"timed; duo budget {budget} (the GPU arm's)",
+                "modes": {m: {"decode_tps": round(v["decode_tps"], 3),
+                              "ttft_ms": round(v["ttft_ms"], 1)} for m, v in cpu.items()}}
+            # greedy parity on the same prompt: the GPU engine's tokens vs the
+            # CPU oracle's (both the target's argmax chain)
+            gpu_tok = first_tokens[:n]
+            eq = {m: next((i for i in range(n) if cpu[m]["tokens"][i] != gpu_tok[i]), n)
+                  for m in ("duo", "vanilla", "sps")}
+            extra["parity"] = {
+                "prompt": "make_prompt(1) (warm-up step 0)", "tokens_compared": n,
+                "equal_prefix": eq, "identical": all(v == n for v in eq.values())}
     if rank == 0:
         line = {
             "metric": {"config2": METRIC, "config3": METRIC_C3, "config5": METRIC_C5}[args.workload],
@@ -436,7 +495,7 @@ def main():
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--cpu-tokens", type=int, default=16)
-    ap.add_argument("--ref-tokens", type=int, default=8)
+    ap.add_argument("--ref-tokens", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     from paper_2503_00784_b200 import DEFAULT_PLANT

@@ -49,10 +49,34 @@ def dist(logits: np.ndarray, T: float, greedy: bool) -> np.ndarray:
 
 def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt, budget: int,
             max_sequences: int, max_new_tokens: int, greedy: bool = True, temperature: float = 1.0,
-            draft_seed: int = 1, verify_seed: int = 2) -> dict:
-    """Returns tokens, ttft_ms, total_ms and per-iteration committed counts."""
+            draft_seed: int = 1, verify_seed: int = 2, threaded: bool = True) -> dict:
+    """Returns tokens, ttft_ms, total_ms and per-iteration committed counts.
+
+    duo with threaded=True runs the draft in a worker thread concurrently with
+    the target pass, one rendezvous per iteration (proj/src/engine.cpp:425-440,
+    DuoExecution::threaded); each role owns its RandomStream, so the tokens
+    equal the sequential execution's.  The oracle releases the GIL inside its
+    forwards (ctypes), and each model runs its own thread count."""
     rd, rv = P.RandomStream(draft_seed), P.RandomStream(verify_seed)
+    worker = None
+    if mode == "duo" and threaded:
+        import queue
+        import threading
+        req, rep = queue.Queue(), queue.Queue()
+
+        def serve():
+            while True:
+                z = req.get()
+                if z is None:
+                    return
+                try:
+                    rep.put(P.draft_dynamic(drf, z, budget, max_sequences, rd))
+                except BaseException as e:  # surfaced on the target thread
+                    rep.put(e)
+        worker = threading.Thread(target=serve, daemon=True)
     drf = CpuDraft(draft, temperature, greedy) if draft is not None else None
+    if worker is not None:
+        worker.start()
     verified = list(prompt)
     n_prompt = len(prompt)
     tail: Optional[P.DraftSequence] = None
@@ -80,11 +104,19 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
             acc, nxt = P.sps_verify(toks, dists, p_rows, rv)
             verified += toks[:acc] + [nxt]
             committed = acc + 1
-        else:  # duo, sequential execution (emits the threaded run's tokens)
+        else:  # duo (threaded: draft of this iteration overlaps the target pass)
             z = list(verified) + (list(tail.tokens) if tail else [])
-            bundle = P.draft_dynamic(drf, z, budget, max_sequences, rd)
             tail_tokens = list(tail.tokens) if tail else []
-            lg = target.forward([verified[-1]] + tail_tokens)
+            if worker is not None:
+                req.put(z)
+                lg = target.forward([verified[-1]] + tail_tokens)
+                bundle = rep.get()  # rendezvous
+                if isinstance(bundle, BaseException):
+                    req.put(None)
+                    raise bundle
+            else:
+                bundle = P.draft_dynamic(drf, z, budget, max_sequences, rd)
+                lg = target.forward([verified[-1]] + tail_tokens)
             p_rows = [dist(r, temperature, greedy) for r in lg]
             committed, usable = 0, True
             if tail is not None:
@@ -114,4 +146,7 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
         if ttft is None:
             ttft = (time.perf_counter() - t0) * 1e3
     total = (time.perf_counter() - t0) * 1e3
+    if worker is not None:
+        req.put(None)
+        worker.join()
     return dict(tokens=verified[n_prompt:], ttft_ms=ttft, total_ms=total, iterations=iters)

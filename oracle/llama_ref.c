@@ -31,6 +31,10 @@ typedef struct {
     int64_t lo, hi;
 } par_job;
 static int g_threads = 1;
+/* per calling thread: the model being run sets its own thread count, so a
+ * target and a draft can run concurrently from two host threads (the
+ * threaded duo loop of oracle/cpu_engine.py) */
+static __thread int tl_threads = 0;
 static void* par_entry(void* p) {
     par_job* j = (par_job*)p;
     j->fn(j->arg, j->lo, j->hi);
@@ -38,7 +42,7 @@ static void* par_entry(void* p) {
 }
 /* static partition of [0, n) over g_threads pthreads */
 static void par_range(int64_t n, range_fn fn, void* arg) {
-    int nt = g_threads;
+    int nt = tl_threads > 0 ? tl_threads : g_threads;
     if (nt > n) nt = (int)n;
     if (nt <= 1) {
         fn(arg, 0, n);
@@ -566,6 +570,7 @@ static void attn_range(void* p, int64_t lo, int64_t hi) {
  * the last row when last_only, written at logits[0..V)). */
 int orc_llama_forward(orc_llama* m, const int32_t* tokens, int w, float* logits, int last_only) {
     if (w < 1 || m->n_cached + w > m->max_seq) return -1;
+    tl_threads = m->n_threads > 0 ? (m->n_threads > 256 ? 256 : m->n_threads) : 1;
     const int d = m->d, hd = m->hd, H = m->H, Hkv = m->Hkv, F = m->F, V = m->V;
     const int qd = H * hd, kvd = Hkv * hd, rows = qd + 2 * kvd, half = hd / 2;
     const int n0 = m->n_cached;
