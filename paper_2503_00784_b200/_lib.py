@@ -6,9 +6,12 @@ is no fallback: if the library is missing, importing the native path raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libduodec_b200.so"
+if os.environ.get("DD_LIB_AB"):  # A/B timing scripts only: an alternative build of the same ABI
+    LIB_PATH = Path(os.environ["DD_LIB_AB"]).resolve()
 
 DD_OK, DD_E_ARG, DD_E_CUDA, DD_E_STATE, DD_E_CAPACITY = 0, -1, -2, -3, -4
 DD_MODE_DUO, DD_MODE_SPS, DD_MODE_VANILLA = 0, 1, 2
@@ -137,6 +140,8 @@ def lib() -> C.CDLL:
             raise ImportError(f"{LIB_PATH} is missing; run paper_2503_00784_b200/build.py")
         L = C.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if os.environ.get("DD_LIB_AB") and not hasattr(L, name):
+                continue  # an older build in an A/B timing run
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args

@@ -525,17 +525,22 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* 
 #pragma unroll
             for (int t = 0; t < kChunk; ++t) {
                 if (t < W) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(v[t], gcol));
-                float sq = __fmul_rn(v[t], v[t]);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
-                if ((tid & 31) == 0) part[(tid >> 5) * kChunk + t] = sq;
+                red[t * 128 + tid] = __fmul_rn(v[t], v[t]);
             }
             epi_bar();
-            if (tid < W) {
-                const float tot = __fadd_rn(__fadd_rn(part[tid], part[kChunk + tid]),
-                                            __fadd_rn(part[2 * kChunk + tid], part[3 * kChunk + tid]));
-                e.ss_out[static_cast<size_t>(tid) * a.tiles + tile] = tot;
+            // sum of squares of the tile's 128 rows per token: 8 threads per token,
+            // 16 consecutive rows each (rolled), then a 3-step shuffle tree (compact
+            // code: this runs once per tile on the phase boundary's critical path)
+            const int t = tid >> 3, j = tid & 7;
+            float sq = 0.0f;
+            if (t < W) {
+                const float* rr = red + t * 128 + j * 16;
+#pragma unroll 1
+                for (int k = 0; k < 16; ++k) sq = __fadd_rn(sq, rr[k]);
             }
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
+            if (t < W && j == 0) e.ss_out[static_cast<size_t>(t) * a.tiles + tile] = sq;
         }
     } else {
         // SwiGLU / RoPE pair rows of different warps: stage once
