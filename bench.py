@@ -286,6 +286,7 @@ def run_ours(args):
     tcore, dcores = core_slice(rank, ws)
     os.sched_setaffinity(0, {tcore})  # target-role thread
     tp = bool(wl.get("tp"))
+    hard_cap = args.hard_cap or wl.get("hard_cap", 256)
     shape_t = SHAPES["llama2_70b"] if tp else SHAPES["llama2_7b"]
     tgt = Target(shape_t, weight_seed=SEED_W_TARGET, plant=plant,
                  max_seq=PROMPT_LEN + NEW_TOKENS + 512, device=local,
@@ -307,7 +308,7 @@ def run_ours(args):
         # passes take the per-launch path, +30% per pass); 127 on the 70B shape
         # (long passes favour long drafts; 128 tokens is the widest pass of the
         # tokens-on-M GEMM)
-        coef, budget = calibrate(tgt, drf, probe_len=8, trials=12, hard_cap=wl.get("hard_cap", 256))
+        coef, budget = calibrate(tgt, drf, probe_len=8, trials=12, hard_cap=hard_cap)
     cfg = EngineConfig(mode=args.mode, budget=budget, max_sequences=wl["max_sequences"],
                        max_new_tokens=NEW_TOKENS, greedy=wl["greedy"],
                        temperature=wl["temperature"])
@@ -454,7 +455,7 @@ def run_ours(args):
                        "seq_len": PROMPT_LEN + NEW_TOKENS,
                        "parallelism": f"tp{ws}" if tp else f"replicas{ws}",
                        "mode": args.mode, "budget": budget, "calibrated_c": coef,
-                       "budget_hard_cap": wl.get("hard_cap", 256),
+                       "budget_hard_cap": hard_cap,
                        "max_sequences": wl["max_sequences"], "greedy": wl["greedy"],
                        "temperature": wl["temperature"], "alpha": plant["alpha"],
                        "seq_hist": seq_hist,
@@ -492,6 +493,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="duo", choices=["duo", "sps", "vanilla"])
     ap.add_argument("--budget", type=int, default=0, help="0 = calibrate on this box")
+    ap.add_argument("--hard-cap", type=int, default=0,
+                    help="budget_hard_cap (0 = the workload's default; the reference's is 256)")
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--cpu-tokens", type=int, default=16)

@@ -490,38 +490,42 @@ __device__ void wait_phase_inputs(const PassParams& P, int x_src, int x_flag, in
 // that live in different warps, so they stage through `red` once.  Phase-level
 // constants (RMSNorm factors, RoPE cos/sin of the W positions, KV pages) come
 // from shared memory, prefetched at phase start.
+constexpr int kFastMaxW = 32;  // decode widths served by the register-resident epilogue
 struct FastEpi {
-    float rn[kChunk];          // RMSNorm factor per token (consumers of h)
-    float cs[kChunk][64];      // RoPE cos / sin at positions n_cached + t
-    float sn[kChunk][64];
-    int page[kChunk], slot[kChunk];
-    float part[4][kChunk];     // cross-warp sum-of-squares partials
+    float rn[kFastMaxW];       // RMSNorm factor per token (consumers of h)
+    float cs[kFastMaxW][64];   // RoPE cos / sin at positions n_cached + t
+    float sn[kFastMaxW][64];
+    int page[kFastMaxW], slot[kFastMaxW];
 };
+// FastEpi lives in the attention K/V staging area (the epilogue warps run GEMM
+// epilogues and attention items one after the other, never both at once)
+static_assert(sizeof(FastEpi) <= 4 * kAttnChunk * 64 * 2, "FastEpi exceeds the K/V staging area");
 
-__device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* part, int tile, float* v,
+// Tokens [t0, t0 + 16) of the pass (W <= 32 runs two chunks).
+__device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, int tile, int t0, float* v,
                                    const float* xv, float gcol, float* red, int tid) {
     const GemmEpiParams& e = a.epi;
-    const int W = a.w;
+    const int W = min(kChunk, a.w - t0);  // tokens of this chunk
     const int m0 = tile * kBlockM;
     if (e.ss_in != nullptr) {
 #pragma unroll
         for (int t = 0; t < kChunk; ++t)
-            if (t < W) v[t] = __fmul_rn(v[t], fe.rn[t]);
+            if (t < W) v[t] = __fmul_rn(v[t], fe.rn[t0 + t]);
     }
     if (e.kind == kEpiStore) {
-        float* dst = e.out + m0 + tid;
+        float* dst = e.out + static_cast<size_t>(t0) * a.n_out + m0 + tid;
 #pragma unroll
         for (int t = 0; t < kChunk; ++t)
             if (t < W) dst[static_cast<size_t>(t) * a.n_out] = v[t];
     } else if (e.kind == kEpiResidual) {
-        float* dst = e.out + m0 + tid;
+        float* dst = e.out + static_cast<size_t>(t0) * a.n_out + m0 + tid;
 #pragma unroll
         for (int t = 0; t < kChunk; ++t) v[t] = t < W ? __fadd_rn(xv[t], v[t]) : 0.0f;
 #pragma unroll
         for (int t = 0; t < kChunk; ++t)
             if (t < W) dst[static_cast<size_t>(t) * a.n_out] = v[t];
         if (e.u_out != nullptr) {
-            __nv_bfloat16* u = e.u_out + m0 + tid;
+            __nv_bfloat16* u = e.u_out + static_cast<size_t>(t0) * a.n_out + m0 + tid;
 #pragma unroll
             for (int t = 0; t < kChunk; ++t) {
                 if (t < W) u[static_cast<size_t>(t) * a.n_out] = __float2bfloat16_rn(__fmul_rn(v[t], gcol));
@@ -540,7 +544,7 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* 
             }
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
-            if (t < W && j == 0) e.ss_out[static_cast<size_t>(t) * a.tiles + tile] = sq;
+            if (t < W && j == 0) e.ss_out[static_cast<size_t>(t0 + t) * a.tiles + tile] = sq;
         }
     } else {
         // SwiGLU / RoPE pair rows of different warps: stage once
@@ -554,7 +558,7 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* 
                 const int t = idx >> 6, f = idx & 63;
                 const float g = red[t * 128 + f], u = red[t * 128 + 64 + f];
                 const float silu = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-                e.out_bf[static_cast<size_t>(t) * ffn + tile * 64 + f] = __float2bfloat16_rn(__fmul_rn(silu, u));
+                e.out_bf[static_cast<size_t>(t0 + t) * ffn + tile * 64 + f] = __float2bfloat16_rn(__fmul_rn(silu, u));
             }
         } else {  // kEpiQkvRope
             const ModelDims& md = e.m;
@@ -566,18 +570,18 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* 
                     const int hl = pr / half, i = pr % half;
                     const int r0 = hl * hd + i;
                     const float av = red[t * 128 + r0], bv = red[t * 128 + r0 + half];
-                    const float c = fe.cs[t][i], sn = fe.sn[t][i];
+                    const float c = fe.cs[t0 + t][i], sn = fe.sn[t0 + t][i];
                     const float lo = __fmaf_rn(av, c, -__fmul_rn(bv, sn));
                     const float hi = __fmaf_rn(bv, c, __fmul_rn(av, sn));
                     const int grow = m0 + r0;
                     if (grow < q_dim) {
-                        float* qd = e.q_out + static_cast<size_t>(t) * q_dim + grow;
+                        float* qd = e.q_out + static_cast<size_t>(t0 + t) * q_dim + grow;
                         qd[0] = lo;
                         qd[half] = hi;
                     } else {
                         const int kh = (grow - q_dim) / hd;
                         __nv_bfloat16* kd =
-                            e.kv_pool + kv_offset(md, e.page_size, fe.page[t], e.layer, 0, kh, fe.slot[t]) + i;
+                            e.kv_pool + kv_offset(md, e.page_size, fe.page[t0 + t], e.layer, 0, kh, fe.slot[t0 + t]) + i;
                         kd[0] = __float2bfloat16_rn(lo);
                         kd[half] = __float2bfloat16_rn(hi);
                     }
@@ -586,7 +590,7 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, float* 
                 for (int idx = tid; idx < W * 128; idx += kEpiThreads) {
                     const int t = idx >> 7, r = idx & 127;
                     const int ve = m0 + r - q_dim - kv_dim;
-                    e.kv_pool[kv_offset(md, e.page_size, fe.page[t], e.layer, 1, ve / hd, fe.slot[t]) + ve % hd] =
+                    e.kv_pool[kv_offset(md, e.page_size, fe.page[t0 + t], e.layer, 1, ve / hd, fe.slot[t0 + t]) + ve % hd] =
                         __float2bfloat16_rn(red[t * 128 + r]);
                 }
             }
@@ -680,7 +684,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     __shared__ float s_r[kChunk];
     __shared__ float s_part[4 * 32];
     __shared__ GemmArgs s_args;
-    __shared__ FastEpi s_fe;
+    FastEpi& s_fe = *reinterpret_cast<FastEpi*>(kv_smem);  // aliases the attention staging area
     __shared__ unsigned long long s_issue[16];  // debug: weight-load issue time per stage
 
     if (threadIdx.x == 0) {
@@ -863,14 +867,20 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 continue;
             }
             if (ph.type == kPhAttn) {
-                const int items = P.m.n_heads * qtiles * kAttnGroups;
+                // only the (head, query tile, group) items that have work, numbered
+                // densely (per head: the query tiles' active group counts in
+                // order), CTA c taking items c, c + nctas, ...
                 const int n0 = P.ps->n_cached;
+                auto active_of = [&](int qt) {
+                    return attn_groups((n0 + min(W, (qt + 1) * 16) - 1) / kAttnChunk + 1, P.attn_cpg);
+                };
+                int per_head = 0;
+                for (int qt = 0; qt < qtiles; ++qt) per_head += active_of(qt);
+                const int items = P.m.n_heads * per_head;
                 for (int item = c; item < items; item += nctas) {
-                    const int grp = item % kAttnGroups;
-                    const int qt = (item / kAttnGroups) % qtiles;
-                    const int head = item / (kAttnGroups * qtiles);
-                    const int kmax = n0 + min(W, (qt + 1) * 16) - 1;
-                    if (grp >= attn_groups(kmax / kAttnChunk + 1, P.attn_cpg)) continue;  // no chunk for this group
+                    const int head = item / per_head;
+                    int grp = item % per_head, qt = 0;
+                    for (int act = active_of(0); grp >= act; act = active_of(++qt)) grp -= act;
                     if (tid == 0) PASS_DBG(6, p * 100000 + item);
                     if (hd == 128)
                         attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);
@@ -887,7 +897,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const long g0 = part.begin(c, static_cast<int>(T)), g1 = part.begin(c + 1, static_cast<int>(T));
             if (g1 <= g0) continue;
             if (tid == 0) s_args = ph.a;
-            const bool fast = W <= kChunk;
+            const bool fast = W <= kFastMaxW;
             if (fast) {
                 // every producer tile of this phase's input is complete before
                 // the phase-level constants are read (lanes poll in parallel)
@@ -954,55 +964,85 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * P.tmem_buf);
                 bool publish = false;
                 if (fast) {
-                    float v[16];
-                    tmem_ld16(t_lane, v);
-                    tc_fence_before();
-                    mbar_arrive(&tempty[b]);
+                    // tokens in chunks of 16 (W <= 32: two chunks), one TMEM load each
+                    const int nch = (W + kChunk - 1) / kChunk;
+                    // partial layout [segment][row][Wp] (Wp = W rounded up to 4): one
+                    // 16-byte store / load per 4 tokens
+                    const int Wp = (W + 3) & ~3;
+                    auto next_xv = [&](int t0) {  // residual rows of a later chunk
+                        if (!resid) return;
+#pragma unroll
+                        for (int t = 0; t < kChunk; ++t)
+                            xv[t] = t0 + t < W
+                                        ? __ldcg(a.epi.out + static_cast<size_t>(t0 + t) * a.n_out + tile * kBlockM + tid)
+                                        : 0.0f;
+                    };
                     if (nseg == 1) {
-                        fast_tile_epilogue(a, s_fe, s_part, tile, v, xv, gcol, red, tid);
+#pragma unroll 1
+                        for (int ch = 0; ch < nch; ++ch) {
+                            float v[16];
+                            tmem_ld16(t_lane + ch * kChunk, v);
+                            if (ch == nch - 1) {
+                                tc_fence_before();
+                                mbar_arrive(&tempty[b]);
+                            }
+                            if (ch > 0) {
+                                epi_bar();  // `red` of the previous chunk consumed
+                                next_xv(ch * kChunk);
+                            }
+                            fast_tile_epilogue(a, s_fe, tile, ch * kChunk, v, xv, gcol, red, tid);
+                        }
                         publish = true;
-                    } else {
+                    } else if (seg != 0) {
                         // Segment 0 (the tile's first k-blocks) sits at the END of its
                         // CTA's range, so it finishes last: it is the designated reducer.
                         // The others store their partial and bump the tile counter with a
                         // fire-and-forget release; the reducer waits for them (normally
                         // already done), adds them in segment order to its own registers.
-                        // partial layout [segment][row][Wp] (Wp = W rounded up to 4): one
-                        // 16-byte store / load per 4 tokens
-                        const int Wp = (W + 3) & ~3;
-                        if (seg != 0) {
-                            float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * Wp * 128 +
-                                          static_cast<size_t>(row) * Wp;
+                        float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * Wp * 128 +
+                                      static_cast<size_t>(row) * Wp;
+#pragma unroll 1
+                        for (int ch = 0; ch < nch; ++ch) {
+                            float v[16];
+                            tmem_ld16(t_lane + ch * kChunk, v);
 #pragma unroll
                             for (int q4 = 0; q4 < 4; ++q4)
-                                if (4 * q4 < W)
-                                    reinterpret_cast<float4*>(part)[q4] =
+                                if (ch * kChunk + 4 * q4 < W)
+                                    reinterpret_cast<float4*>(part)[ch * 4 + q4] =
                                         make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
-                            epi_bar();  // every partial store happens-before the release
-                            if (tid == 0)
-                                asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
-                                             ::"l"(&a.epi.counters[tile * kCounterStride]) : "memory");
-                        } else {
-                            if (tid == 0) {
-                                while (ld_acquire(&a.epi.counters[tile * kCounterStride]) < nseg - 1) __nanosleep(32);
-                                a.epi.counters[tile * kCounterStride] = 0;
-                                pass_stamp(P, p, 5);  // debug: reducer saw every partial
-                            }
-                            epi_bar();
-                            const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * Wp * 128 +
-                                                static_cast<size_t>(row) * Wp;
+                        }
+                        tc_fence_before();
+                        mbar_arrive(&tempty[b]);
+                        epi_bar();  // every partial store happens-before the release
+                        if (tid == 0)
+                            asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
+                                         ::"l"(&a.epi.counters[tile * kCounterStride]) : "memory");
+                    } else {
+                        if (tid == 0) {
+                            while (ld_acquire(&a.epi.counters[tile * kCounterStride]) < nseg - 1) __nanosleep(32);
+                            a.epi.counters[tile * kCounterStride] = 0;
+                            pass_stamp(P, p, 5);  // debug: reducer saw every partial
+                        }
+                        epi_bar();
+                        const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * Wp * 128 +
+                                            static_cast<size_t>(row) * Wp;
+#pragma unroll 1
+                        for (int ch = 0; ch < nch; ++ch) {
                             float acc[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) acc[j] = v[j];
+                            tmem_ld16(t_lane + ch * kChunk, acc);
+                            if (ch == nch - 1) {
+                                tc_fence_before();
+                                mbar_arrive(&tempty[b]);
+                            }
                             for (int s0 = 1; s0 < nseg; s0 += 4) {
                                 float4 pv[4][4];
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
 #pragma unroll
                                     for (int q4 = 0; q4 < 4; ++q4)
-                                        pv[k][q4] = (s0 + k < nseg && 4 * q4 < W)
+                                        pv[k][q4] = (s0 + k < nseg && ch * kChunk + 4 * q4 < W)
                                                         ? __ldcg(reinterpret_cast<const float4*>(
-                                                              base + static_cast<size_t>(s0 + k) * Wp * 128) + q4)
+                                                              base + static_cast<size_t>(s0 + k) * Wp * 128) + ch * 4 + q4)
                                                         : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
@@ -1016,10 +1056,14 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                         }
                             }
                             if (tid == 0) pass_stamp(P, p, 8);  // debug: partials summed
-                            fast_tile_epilogue(a, s_fe, s_part, tile, acc, xv, gcol, red, tid);
-                            if (tid == 0) pass_stamp(P, p, 9);
-                            publish = true;
+                            if (ch > 0) {
+                                epi_bar();
+                                next_xv(ch * kChunk);
+                            }
+                            fast_tile_epilogue(a, s_fe, tile, ch * kChunk, acc, xv, gcol, red, tid);
                         }
+                        if (tid == 0) pass_stamp(P, p, 9);
+                        publish = true;
                     }
                 } else if (nseg == 1) {
                     for (int t0 = 0; t0 < a.w; t0 += kChunk) {

@@ -74,7 +74,7 @@ def _run(pair, n_ctx, w, seed):
     return _compare(name, g, o, f"ctx={n_ctx} W={w}")
 
 
-@pytest.mark.parametrize("w", [1, 8, 16, 17, 40, 128, 200])
+@pytest.mark.parametrize("w", [1, 8, 16, 17, 24, 32, 33, 40, 128, 200])
 def test_hd128_all_widths(pair, w):
     _run(pair, 33, w, 1000 + w)
 
@@ -90,7 +90,7 @@ def test_hd128_width_invariance(pair):
     name, shape, tgt, _ = pair
     rng = np.random.default_rng(9)
     ctx = rng.integers(0, shape["vocab"], 150).tolist()
-    new = rng.integers(0, shape["vocab"], 12).tolist()
+    new = rng.integers(0, shape["vocab"], 27).tolist()
     tgt.truncate(0)
     tgt.prefill(ctx)
     tgt.score(new)

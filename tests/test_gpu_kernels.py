@@ -124,11 +124,11 @@ def test_kv_truncate_rollback(tiny_pair):
     assert tgt.kv_len() == len(ctx) + 3
 
 
-@pytest.mark.parametrize("w", [1, 8, 16, 17, 40, 49, 128, 200])
+@pytest.mark.parametrize("w", [1, 8, 16, 17, 25, 32, 40, 49, 128, 200])
 def test_tiny_pass_logits_all_paths(tiny_pair, w):
-    """Every pass width vs the oracle: decode widths run the persistent pass
-    kernel, 49..128 the tokens-on-M prefill GEMM, the others the per-launch
-    skinny GEMM."""
+    """Every pass width vs the oracle: decode widths (<= 32) run the persistent
+    pass kernel, 33..128 the tokens-on-M prefill GEMM, the others the
+    per-launch skinny GEMM."""
     tgt, orc = tiny_pair
     rng = np.random.default_rng(100 + w)
     ctx = rng.integers(0, TINY["vocab"], 33).tolist()
