@@ -366,6 +366,247 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
     }
 }
 
+// Prefill attention (long prompts, enqueue_prefill_big): CTA = (head, 64-query
+// tile), warp w owns queries [16 w, 16 w + 16) of the tile and computes its own
+// S = Q K^T (16 x 64 keys per chunk), online softmax and O += P V over all head
+// dims, so the K / V chunks staged in shared memory (cp.async, double-buffered,
+// the same swizzles as above) are shared by 64 queries and no warp repeats
+// another's work.  Causal: a chunk past a warp's last query is skipped, the
+// CTA stops at its last query's key.  Heavier (later) query tiles launch first.
+template <int HD>
+__global__ void __launch_bounds__(kAttnCtaThreads)
+    attn_prefill_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
+                        const __nv_bfloat16* __restrict__ kv_pool, const int32_t* __restrict__ page_table,
+                        int page_size, int layer, float scale_log2, __nv_bfloat16* __restrict__ o) {
+    constexpr int kKeys = 64;      // keys per staged chunk
+    constexpr int NCH = HD / 32;   // 32-dim chunks of QK^T (2 k-steps each)
+    constexpr int CHK = HD / 8;    // 16-byte chunks per K/V row
+    constexpr int NT = HD / 8;     // PV n-tiles: thread g owns dims [g NT, g NT + NT)
+    constexpr int NW = NT / 2;     // 32-bit words of those dims per key row
+    extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+    auto ks = [&](int b) { return reinterpret_cast<__nv_bfloat16(*)[HD]>(attn_smem_raw + b * 2 * kKeys * HD * 2); };
+    auto vs = [&](int b) {
+        return reinterpret_cast<__nv_bfloat16(*)[HD]>(attn_smem_raw + (b * 2 + 1) * kKeys * HD * 2);
+    };
+    pdl_wait_();
+    pdl_launch_();
+    const int n0 = ps->n_cached, W = ps->w;
+    const int qtiles = (W + 63) / 64;
+    const int qt = qtiles - 1 - static_cast<int>(blockIdx.x), head = blockIdx.y;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, c = lane & 3;
+    const int kvh = head / (md.n_heads / md.n_kv_heads);
+    const int qd = md.q_dim();
+    const int kmax = n0 + min(W, 64 * (qt + 1)) - 1;  // last key of this CTA
+    const int n_chunks = kmax / kKeys + 1;
+    const int row_g = 64 * qt + 16 * warp + g, row_g8 = row_g + 8;  // query rows of this thread
+    const int pos_g = n0 + row_g, pos_g8 = n0 + row_g8;
+    const int warp_last = n0 + min(W - 1, 64 * qt + 16 * warp + 15);  // last key any row of the warp sees
+
+    auto stage = [&](int chunk, int b) {
+        __nv_bfloat16(*kd)[HD] = ks(b);
+        __nv_bfloat16(*vd)[HD] = vs(b);
+        const int kb = chunk * kKeys;
+        for (int idx = tid; idx < kKeys * CHK; idx += kAttnCtaThreads) {
+            const int kk = idx / CHK, ch = idx % CHK;
+            const int key = kb + kk;
+            const bool ok = key <= kmax;
+            const int kc = ok ? key : 0;
+            const int page = page_table[kc / page_size], slot = kc % page_size;
+            cp_async16(&kd[kk][k_chunk(kk, ch) * 8],
+                       kv_pool + kv_offset(md, page_size, page, layer, 0, kvh, slot) + ch * 8, ok ? 16u : 0u);
+            cp_async16(&vd[kk][v_chunk<HD>(kk, ch) * 8],
+                       kv_pool + kv_offset(md, page_size, page, layer, 1, kvh, slot) + ch * 8, ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage(0, 0);
+
+    uint32_t qa[NCH][4], qb[NCH][4];
+    {
+        const bool v_g = row_g < W, v_g8 = row_g8 < W;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            const int d0 = head * HD + ch * 32 + c * 8;
+            float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, b0 = a0, b1 = a0;
+            if (v_g) {
+                const float4* src = reinterpret_cast<const float4*>(q + static_cast<size_t>(row_g) * qd + d0);
+                a0 = __ldg(src);
+                a1 = __ldg(src + 1);
+            }
+            if (v_g8) {
+                const float4* src = reinterpret_cast<const float4*>(q + static_cast<size_t>(row_g8) * qd + d0);
+                b0 = __ldg(src);
+                b1 = __ldg(src + 1);
+            }
+            qa[ch][0] = pack_bf16(a0.x, a0.y);
+            qa[ch][1] = pack_bf16(a0.z, a0.w);
+            qa[ch][2] = pack_bf16(a1.x, a1.y);
+            qa[ch][3] = pack_bf16(a1.z, a1.w);
+            qb[ch][0] = pack_bf16(b0.x, b0.y);
+            qb[ch][1] = pack_bf16(b0.z, b0.w);
+            qb[ch][2] = pack_bf16(b1.x, b1.y);
+            qb[ch][3] = pack_bf16(b1.z, b1.w);
+        }
+    }
+    float acc[NT][4];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+    float m_g = -INFINITY, m_g8 = -INFINITY, l_g = 0.f, l_g8 = 0.f;
+
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+        const int b = chunk & 1;
+        if (chunk + 1 < n_chunks) {
+            stage(chunk + 1, b ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int kb = chunk * kKeys;
+        if (kb <= warp_last) {
+            __nv_bfloat16(*kd)[HD] = ks(b);
+            __nv_bfloat16(*vd)[HD] = vs(b);
+            float sc[kKeys / 8][4];
+#pragma unroll
+            for (int j = 0; j < kKeys / 8; ++j) {
+                sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+                const int kk = 8 * j + g;
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const uint4 kr = *reinterpret_cast<const uint4*>(&kd[kk][k_chunk(kk, 4 * ch + c) * 8]);
+                    const uint32_t a0[4] = {qa[ch][0], qb[ch][0], qa[ch][1], qb[ch][1]};
+                    mma_bf16(sc[j], a0, kr.x, kr.y);
+                    const uint32_t a1[4] = {qa[ch][2], qb[ch][2], qa[ch][3], qb[ch][3]};
+                    mma_bf16(sc[j], a1, kr.z, kr.w);
+                }
+            }
+            float mx_g = -INFINITY, mx_g8 = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < kKeys / 8; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int key = kb + 8 * j + 2 * c + e;
+                    sc[j][e] = key <= pos_g ? sc[j][e] * scale_log2 : -INFINITY;
+                    sc[j][2 + e] = key <= pos_g8 ? sc[j][2 + e] * scale_log2 : -INFINITY;
+                    mx_g = fmaxf(mx_g, sc[j][e]);
+                    mx_g8 = fmaxf(mx_g8, sc[j][2 + e]);
+                }
+#pragma unroll
+            for (int off = 1; off <= 2; off <<= 1) {
+                mx_g = fmaxf(mx_g, __shfl_xor_sync(0xffffffffu, mx_g, off));
+                mx_g8 = fmaxf(mx_g8, __shfl_xor_sync(0xffffffffu, mx_g8, off));
+            }
+            const float mn_g = fmaxf(m_g, mx_g), mn_g8 = fmaxf(m_g8, mx_g8);
+            const float base_g = mn_g == -INFINITY ? 0.f : mn_g;
+            const float base_g8 = mn_g8 == -INFINITY ? 0.f : mn_g8;
+            const float cr_g = fast_exp2(m_g - base_g), cr_g8 = fast_exp2(m_g8 - base_g8);
+            m_g = mn_g;
+            m_g8 = mn_g8;
+            l_g *= cr_g;
+            l_g8 *= cr_g8;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                acc[t][0] *= cr_g;
+                acc[t][1] *= cr_g;
+                acc[t][2] *= cr_g8;
+                acc[t][3] *= cr_g8;
+            }
+#pragma unroll
+            for (int kst = 0; kst < kKeys / 16; ++kst) {
+                uint32_t pa[4];
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const float* sj = sc[2 * kst + jj];
+                    const float p0 = fast_exp2(sj[0] - base_g), p1 = fast_exp2(sj[1] - base_g);
+                    const float p2 = fast_exp2(sj[2] - base_g8), p3 = fast_exp2(sj[3] - base_g8);
+                    l_g += p0 + p1;
+                    l_g8 += p2 + p3;
+                    pa[jj * 2 + 0] = pack_bf16(p0, p1);
+                    pa[jj * 2 + 1] = pack_bf16(p2, p3);
+                }
+                uint32_t vw[4][NW];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int kk = 16 * kst + 2 * c + (r & 1) + (r >> 1) * 8;
+                    if constexpr (HD == 128) {
+                        const uint4 x0 = *reinterpret_cast<const uint4*>(&vd[kk][v_chunk<HD>(kk, 2 * g) * 8]);
+                        const uint4 x1 = *reinterpret_cast<const uint4*>(&vd[kk][v_chunk<HD>(kk, 2 * g + 1) * 8]);
+                        vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
+                        vw[r][4] = x1.x; vw[r][5] = x1.y; vw[r][6] = x1.z; vw[r][7] = x1.w;
+                    } else {
+                        const uint4 x0 = *reinterpret_cast<const uint4*>(&vd[kk][v_chunk<HD>(kk, g) * 8]);
+                        vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < NT; ++e) {
+                    const uint32_t sel = (e & 1) ? 0x7632 : 0x5410;
+                    const uint32_t b0 = __byte_perm(vw[0][e >> 1], vw[1][e >> 1], sel);
+                    const uint32_t b1 = __byte_perm(vw[2][e >> 1], vw[3][e >> 1], sel);
+                    mma_bf16(acc[e], pa, b0, b1);
+                }
+            }
+        }
+        __syncthreads();  // buffer b is refilled by the next iteration's stage
+    }
+#pragma unroll
+    for (int off = 1; off <= 2; off <<= 1) {
+        l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
+        l_g8 += __shfl_xor_sync(0xffffffffu, l_g8, off);
+    }
+    // C fragment (row g / g + 8, col 2c + h) of tile e is dim (2c + h) * NT + e
+    const float ig = 1.0f / l_g, ig8 = 1.0f / l_g8;
+    if (row_g < W) {
+        __nv_bfloat16* og = o + static_cast<size_t>(row_g) * qd + head * HD;
+#pragma unroll
+        for (int e = 0; e < NT; ++e) {
+            og[(2 * c) * NT + e] = __float2bfloat16_rn(acc[e][0] * ig);
+            og[(2 * c + 1) * NT + e] = __float2bfloat16_rn(acc[e][1] * ig);
+        }
+    }
+    if (row_g8 < W) {
+        __nv_bfloat16* og = o + static_cast<size_t>(row_g8) * qd + head * HD;
+#pragma unroll
+        for (int e = 0; e < NT; ++e) {
+            og[(2 * c) * NT + e] = __float2bfloat16_rn(acc[e][2] * ig8);
+            og[(2 * c + 1) * NT + e] = __float2bfloat16_rn(acc[e][3] * ig8);
+        }
+    }
+}
+
+int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, const float* q,
+                             const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                             int layer, __nv_bfloat16* o, cudaStream_t s) {
+    const float scale_log2 =
+        static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(m.head_dim)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((w + 63) / 64, m.n_heads, 1);
+    cfg.blockDim = dim3(kAttnCtaThreads, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int dev = current_device_slot();
+    static bool a128[kMaxDevices] = {}, a64[kMaxDevices] = {};
+    auto go = [&](auto kernel, int hd, bool* attr) {
+        const size_t smem = static_cast<size_t>(4) * 64 * hd * 2;
+        cfg.dynamicSmemBytes = smem;
+        if (!attr[dev]) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr[dev] = true;
+        }
+        return cudaLaunchKernelEx(&cfg, kernel, ps, m, q, kv_pool, page_table, page_size, layer, scale_log2, o);
+    };
+    cudaError_t e;
+    if (m.head_dim == 128) e = go(attn_prefill_kernel<128>, 128, a128);
+    else if (m.head_dim == 64) e = go(attn_prefill_kernel<64>, 64, a64);
+    else return -1;
+    return e == cudaSuccess ? 0 : -2;
+}
+
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                      int layer, __nv_bfloat16* o, cudaStream_t s, int ranks) {

@@ -248,8 +248,12 @@ struct Runner {
     void truncate_all(int n) {
         for (dd_ctx* r : ranks) ck(dd_kv_truncate(r, n), r);
     }
-    void prefill(const int32_t* tokens, int n) {  // chunk-major: no rank runs ahead
-        for (int i = 0; i < n; i += dd::kPrefillChunk) {
+    void prefill(const int32_t* tokens, int n) {
+        if (ranks.size() == 1) {  // dd_prefill picks the pass sizes (one pass for a long prompt)
+            ck(dd_prefill(ctx, tokens, n), ctx);
+            return;
+        }
+        for (int i = 0; i < n; i += dd::kPrefillChunk) {  // chunk-major: no rank runs ahead
             const int w = std::min(dd::kPrefillChunk, n - i);
             for (dd_ctx* r : ranks) ck(dd_prefill(r, tokens + i, w), r);
         }

@@ -108,4 +108,9 @@ cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* ma
                              int w, const GemmPlan& plan, float* ws, const GemmEpiParams& epi,
                              cudaStream_t stream);
 
+// Multi-tile prefill GEMM (gemm_wide.cu): w <= kMaxPrefillTokens tokens in
+// 128-token tiles x 256-row weight tiles, full K per unit (no stream-K).
+cudaError_t launch_gemm_prefill(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
+                                int w, const GemmEpiParams& epi, cudaStream_t stream);
+
 }  // namespace dd

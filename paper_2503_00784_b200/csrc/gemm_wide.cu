@@ -122,6 +122,147 @@ __device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float* v
 
 }  // namespace
 
+// Fused epilogue of one NW-row weight tile for this thread's token (TMEM lane
+// row; `tok` = the token's row in the pass, `valid` = tok < w): segment sums,
+// RMSNorm scaling, and the store / residual + deferred-norm producer / SwiGLU /
+// RoPE + paged-KV append of gemm_epi.cuh, written thread-locally.  Shared by the
+// stream-K wide GEMM and the multi-tile prefill GEMM.
+template <int NW>
+__device__ __forceinline__ void wide_tile_epilogue(const GemmArgs& a, uint32_t t_lane, const float* pbase,
+                                                   int nsum, size_t seg_stride, int tile, int tok, bool valid,
+                                                   float rn, int page, int slot, int pos) {
+    constexpr int kWideN = NW;
+    constexpr int kHalves = WideCfg<NW>::kHalves;
+    const GemmEpiParams& e = a.epi;
+    const int tiles128 = a.n_out / 128;
+    const int m0 = tile * kWideN;
+    if (e.kind == kEpiStore || e.kind == kEpiResidual) {
+        for (int h = 0; h < kHalves; ++h) {  // 128-row halves (ss tiles)
+            float ss = 0.0f;
+            for (int c1 = h * 128; c1 < h * 128 + 128; c1 += 32) {
+                // residual rows requested first, then 2 chunks of partial sums
+                // and accumulators in one round trip
+                float4 xr[2][4];
+                if (e.kind == kEpiResidual && valid)
+#pragma unroll
+                    for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4)
+                            xr[ch][q4] = __ldcg(reinterpret_cast<const float4*>(
+                                                    e.out + static_cast<size_t>(tok) * a.n_out + m0 + c1 + 16 * ch) + q4);
+                float v2[2][16];
+                load_cols_n<2, 2>(t_lane, c1, pbase, nsum, seg_stride, v2);
+                if (!valid) continue;
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {
+                    const int c0 = c1 + 16 * ch;
+                    float* v = v2[ch];
+                    if (e.ss_in != nullptr)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rn);
+                    float* dst = e.out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
+                    if (e.kind == kEpiResidual) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            v[4 * q4] = __fadd_rn(xr[ch][q4].x, v[4 * q4]);
+                            v[4 * q4 + 1] = __fadd_rn(xr[ch][q4].y, v[4 * q4 + 1]);
+                            v[4 * q4 + 2] = __fadd_rn(xr[ch][q4].z, v[4 * q4 + 2]);
+                            v[4 * q4 + 3] = __fadd_rn(xr[ch][q4].w, v[4 * q4 + 3]);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    if (e.kind == kEpiResidual && e.u_out != nullptr) {
+                        float uv[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            uv[j] = __fmul_rn(v[j], e.gain[m0 + c0 + j]);
+                            ss = __fmaf_rn(v[j], v[j], ss);
+                        }
+                        store_bf16x16(e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0, uv);
+                    }
+                }
+            }
+            if (e.kind == kEpiResidual && e.u_out != nullptr && valid)
+                e.ss_out[static_cast<size_t>(tok) * tiles128 + kHalves * tile + h] = ss;
+        }
+    } else if (e.kind == kEpiSwiGLU) {
+        const int ffn = a.n_out / 2;
+        for (int h = 0; h < kHalves; ++h)
+            for (int k = 0; k < 4; ++k) {
+                float g[16], up[16];
+                load_cols(t_lane, h * 128 + 16 * k, pbase, nsum, seg_stride, g);
+                load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nsum, seg_stride, up);
+                if (!valid) continue;
+                float av[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float gv = __fmul_rn(g[j], rn), uv = __fmul_rn(up[j], rn);
+                    // fast exp / divide: prefill-only activations (the decode
+                    // epilogue keeps the IEEE forms the oracle mirrors)
+                    const float silu = __fdividef(gv, 1.0f + __expf(-gv));
+                    av[j] = __fmul_rn(silu, uv);
+                }
+                store_bf16x16(e.out_bf + static_cast<size_t>(tok) * ffn + (kHalves * tile + h) * 64 + 16 * k, av);
+            }
+    } else {  // kEpiQkvRope
+        const ModelDims& md = e.m;
+        const int hd = md.head_dim, half = hd / 2;
+        const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
+        for (int h = 0; h < kHalves; ++h) {
+            const int r0 = m0 + h * 128;  // first weight row of this 128-row half
+            if (r0 < q_dim + kv_dim) {
+                // pairs (i, i + half) of every head in the half
+                for (int hb = 0; hb < 128; hb += hd)
+                    for (int i0 = 0; i0 < half; i0 += 16) {
+                        float lo_v[16], hi_v[16];
+                        load_cols(t_lane, h * 128 + hb + i0, pbase, nsum, seg_stride, lo_v);
+                        load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nsum, seg_stride, hi_v);
+                        if (!valid) continue;
+                        const int grow = r0 + hb;  // first row of the head
+                        float lo16[16], hi16[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int i = i0 + j;
+                            const float av = __fmul_rn(lo_v[j], rn), bv = __fmul_rn(hi_v[j], rn);
+                            const float cs = e.rope_cos[static_cast<size_t>(pos) * half + i];
+                            const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
+                            lo16[j] = __fmaf_rn(av, cs, -__fmul_rn(bv, sn));
+                            hi16[j] = __fmaf_rn(bv, cs, __fmul_rn(av, sn));
+                        }
+                        if (grow < q_dim) {
+                            float* qd = e.q_out + static_cast<size_t>(tok) * q_dim + grow + i0;
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                reinterpret_cast<float4*>(qd)[q4] =
+                                    make_float4(lo16[4 * q4], lo16[4 * q4 + 1], lo16[4 * q4 + 2], lo16[4 * q4 + 3]);
+                                reinterpret_cast<float4*>(qd + half)[q4] =
+                                    make_float4(hi16[4 * q4], hi16[4 * q4 + 1], hi16[4 * q4 + 2], hi16[4 * q4 + 3]);
+                            }
+                        } else {
+                            __nv_bfloat16* kd = e.kv_pool +
+                                kv_offset(md, e.page_size, page, e.layer, 0, (grow - q_dim) / hd, slot) + i0;
+                            store_bf16x16(kd, lo16);
+                            store_bf16x16(kd + half, hi16);
+                        }
+                    }
+            } else {
+                for (int c0 = 0; c0 < 128; c0 += 16) {
+                    float v[16];
+                    load_cols(t_lane, h * 128 + c0, pbase, nsum, seg_stride, v);
+                    if (!valid) continue;
+                    float vv[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) vv[j] = __fmul_rn(v[j], rn);
+                    const int ve = r0 + c0 - q_dim - kv_dim;  // 16 dims of one kv head
+                    store_bf16x16(e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd, vv);
+                }
+            }
+        }
+    }
+}
+
 template <int NW>
 __global__ void __launch_bounds__(kWideThreads, 1)
     gemm_wide_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap map_x,
@@ -333,132 +474,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
                 nsum = nseg;
             }
             const float* pbase = tile_part + static_cast<size_t>(tok) * 4;
-            const int m0 = tile * kWideN;
-            if (e.kind == kEpiStore || e.kind == kEpiResidual) {
-                for (int h = 0; h < kHalves; ++h) {  // 128-row halves (ss tiles)
-                    float ss = 0.0f;
-                    for (int c1 = h * 128; c1 < h * 128 + 128; c1 += 32) {
-                        // residual rows requested first, then 2 chunks of partial sums
-                        // and accumulators in one round trip
-                        float4 xr[2][4];
-                        if (e.kind == kEpiResidual && valid)
-#pragma unroll
-                            for (int ch = 0; ch < 2; ++ch)
-#pragma unroll
-                                for (int q4 = 0; q4 < 4; ++q4)
-                                    xr[ch][q4] = __ldcg(reinterpret_cast<const float4*>(
-                                                            e.out + static_cast<size_t>(tok) * a.n_out + m0 + c1 + 16 * ch) + q4);
-                        float v2[2][16];
-                        load_cols_n<2, 2>(t_lane, c1, pbase, nsum, seg_stride, v2);
-                        if (!valid) continue;
-#pragma unroll
-                        for (int ch = 0; ch < 2; ++ch) {
-                            const int c0 = c1 + 16 * ch;
-                            float* v = v2[ch];
-                            if (e.ss_in != nullptr)
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rn);
-                            float* dst = e.out + static_cast<size_t>(tok) * a.n_out + m0 + c0;
-                            if (e.kind == kEpiResidual) {
-#pragma unroll
-                                for (int q4 = 0; q4 < 4; ++q4) {
-                                    v[4 * q4] = __fadd_rn(xr[ch][q4].x, v[4 * q4]);
-                                    v[4 * q4 + 1] = __fadd_rn(xr[ch][q4].y, v[4 * q4 + 1]);
-                                    v[4 * q4 + 2] = __fadd_rn(xr[ch][q4].z, v[4 * q4 + 2]);
-                                    v[4 * q4 + 3] = __fadd_rn(xr[ch][q4].w, v[4 * q4 + 3]);
-                                }
-                            }
-#pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                            if (e.kind == kEpiResidual && e.u_out != nullptr) {
-                                float uv[16];
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) {
-                                    uv[j] = __fmul_rn(v[j], e.gain[m0 + c0 + j]);
-                                    ss = __fmaf_rn(v[j], v[j], ss);
-                                }
-                                store_bf16x16(e.u_out + static_cast<size_t>(tok) * a.n_out + m0 + c0, uv);
-                            }
-                        }
-                    }
-                    if (e.kind == kEpiResidual && e.u_out != nullptr && valid)
-                        e.ss_out[static_cast<size_t>(tok) * tiles128 + kHalves * tile + h] = ss;
-                }
-            } else if (e.kind == kEpiSwiGLU) {
-                const int ffn = a.n_out / 2;
-                for (int h = 0; h < kHalves; ++h)
-                    for (int k = 0; k < 4; ++k) {
-                        float g[16], up[16];
-                        load_cols(t_lane, h * 128 + 16 * k, pbase, nsum, seg_stride, g);
-                        load_cols(t_lane, h * 128 + 64 + 16 * k, pbase, nsum, seg_stride, up);
-                        if (!valid) continue;
-                        float av[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float gv = __fmul_rn(g[j], rn), uv = __fmul_rn(up[j], rn);
-                            // fast exp / divide: prefill-only activations (the decode
-                            // epilogue keeps the IEEE forms the oracle mirrors)
-                            const float silu = __fdividef(gv, 1.0f + __expf(-gv));
-                            av[j] = __fmul_rn(silu, uv);
-                        }
-                        store_bf16x16(e.out_bf + static_cast<size_t>(tok) * ffn + (kHalves * tile + h) * 64 + 16 * k, av);
-                    }
-            } else {  // kEpiQkvRope
-                const ModelDims& md = e.m;
-                const int hd = md.head_dim, half = hd / 2;
-                const int q_dim = md.q_dim(), kv_dim = md.kv_dim();
-                for (int h = 0; h < kHalves; ++h) {
-                    const int r0 = m0 + h * 128;  // first weight row of this 128-row half
-                    if (r0 < q_dim + kv_dim) {
-                        // pairs (i, i + half) of every head in the half
-                        for (int hb = 0; hb < 128; hb += hd)
-                            for (int i0 = 0; i0 < half; i0 += 16) {
-                                float lo_v[16], hi_v[16];
-                                load_cols(t_lane, h * 128 + hb + i0, pbase, nsum, seg_stride, lo_v);
-                                load_cols(t_lane, h * 128 + hb + i0 + half, pbase, nsum, seg_stride, hi_v);
-                                if (!valid) continue;
-                                const int grow = r0 + hb;  // first row of the head
-                                float lo16[16], hi16[16];
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) {
-                                    const int i = i0 + j;
-                                    const float av = __fmul_rn(lo_v[j], rn), bv = __fmul_rn(hi_v[j], rn);
-                                    const float cs = e.rope_cos[static_cast<size_t>(pos) * half + i];
-                                    const float sn = e.rope_sin[static_cast<size_t>(pos) * half + i];
-                                    lo16[j] = __fmaf_rn(av, cs, -__fmul_rn(bv, sn));
-                                    hi16[j] = __fmaf_rn(bv, cs, __fmul_rn(av, sn));
-                                }
-                                if (grow < q_dim) {
-                                    float* qd = e.q_out + static_cast<size_t>(tok) * q_dim + grow + i0;
-#pragma unroll
-                                    for (int q4 = 0; q4 < 4; ++q4) {
-                                        reinterpret_cast<float4*>(qd)[q4] =
-                                            make_float4(lo16[4 * q4], lo16[4 * q4 + 1], lo16[4 * q4 + 2], lo16[4 * q4 + 3]);
-                                        reinterpret_cast<float4*>(qd + half)[q4] =
-                                            make_float4(hi16[4 * q4], hi16[4 * q4 + 1], hi16[4 * q4 + 2], hi16[4 * q4 + 3]);
-                                    }
-                                } else {
-                                    __nv_bfloat16* kd = e.kv_pool +
-                                        kv_offset(md, e.page_size, page, e.layer, 0, (grow - q_dim) / hd, slot) + i0;
-                                    store_bf16x16(kd, lo16);
-                                    store_bf16x16(kd + half, hi16);
-                                }
-                            }
-                    } else {
-                        for (int c0 = 0; c0 < 128; c0 += 16) {
-                            float v[16];
-                            load_cols(t_lane, h * 128 + c0, pbase, nsum, seg_stride, v);
-                            if (!valid) continue;
-                            float vv[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) vv[j] = __fmul_rn(v[j], rn);
-                            const int ve = r0 + c0 - q_dim - kv_dim;  // 16 dims of one kv head
-                            store_bf16x16(e.kv_pool + kv_offset(md, e.page_size, page, e.layer, 1, ve / hd, slot) + ve % hd, vv);
-                        }
-                    }
-                }
-            }
+            wide_tile_epilogue<NW>(a, t_lane, pbase, nsum, seg_stride, tile, tok, valid, rn, page, slot, pos);
             tc_fence_before();
             mbar_arrive(&tempty[b]);
         }
@@ -553,6 +569,217 @@ cudaError_t launch_gemm_wide(const __nv_bfloat16* w_tiled, const CUtensorMap* ma
     cfg.numAttrs = 1;
     if (plan.tmem_cols == 512) return cudaLaunchKernelEx(&cfg, gemm_wide_kernel<256>, w_tiled, *map_x128, a);
     return cudaLaunchKernelEx(&cfg, gemm_wide_kernel<128>, w_tiled, *map_x128, a);
+}
+
+}  // namespace dd
+
+// ---------------------------------------------------------------- prefill GEMM
+// Long prompts: one pass over up to kMaxPrefillTokens
+// tokens so every weight tile is streamed from HBM once for the whole prompt
+// instead of once per 128-token chunk.  Work unit = (128-token tile m, NW-row
+// weight tile n) over the full K; units are numbered n-major (m fastest), so
+// the CTAs running at the same time share a few weight tiles (one HBM read,
+// then L2 hits) while the prompt's activations (w x K bf16) stay L2-resident.
+// No stream-K: with >= 148 units every SM has whole units.  Same warp roles,
+// TMEM double buffer and thread-local epilogue (wide_tile_epilogue) as the
+// stream-K wide GEMM above; TMEM lane = token row of the unit's m tile.
+namespace dd {
+
+template <int NW>
+__global__ void __launch_bounds__(kWideThreads, 1)
+    gemm_prefill_kernel(const __nv_bfloat16* __restrict__ w_tiled, const __grid_constant__ CUtensorMap map_x,
+                        GemmArgs a) {
+    constexpr int kHalves = WideCfg<NW>::kHalves;
+    constexpr uint32_t kWBytes = WideCfg<NW>::kWBytes;
+    constexpr uint32_t kStageBytes = WideCfg<NW>::kStageBytes;
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int P = gridDim.x, c = blockIdx.x;
+    const int m_tiles = (a.w + kWideM - 1) / kWideM;
+    const int units = m_tiles * (a.n_out / NW);
+    const int nkb = a.nkb;
+    const int S = a.stages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&map_x);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<2 * NW>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer ----------------
+            const uint64_t pol_w = policy_evict_normal();  // reused by the other m tiles
+            const uint64_t pol_x = policy_evict_last();
+            int s = 0;
+            uint32_t ph = 0, n_issued = 0;
+            bool waited = false;
+            for (int u = c; u < units; u += P) {
+                const int n = u / m_tiles, m = u % m_tiles;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    uint8_t* st = smem + s * kStageBytes;
+                    if (n_issued >= static_cast<uint32_t>(S)) mbar_wait(&empty[s], ph ^ 1u);
+                    mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+                    for (int hh = 0; hh < kHalves; ++hh)
+                        bulk_load(st + hh * kABytes,
+                                  w_tiled + (static_cast<size_t>(kHalves * n + hh) * nkb + kb) * 8192, kABytes,
+                                  &full[s], pol_w);
+                    if (!waited) {  // weights never depend on the previous kernel; activations do
+                        asm volatile("griddepcontrol.wait;" ::: "memory");
+                        waited = true;
+                    }
+                    tma_load_2d(st + kWBytes, &map_x, &full[s], kb * kBlockK, m * kWideM, pol_x);
+                    ++n_issued;
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer ----------------
+            const uint32_t idesc = idesc_bf16_f32(kWideM, NW);
+            int s = 0;
+            uint32_t ph = 0;
+            int j = 0;
+            for (int u = c; u < units; u += P, ++j) {
+                const int b = j & 1;
+                if (j >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>(((j >> 1) - 1) & 1));
+                tc_fence_after();
+                const uint32_t acc = tmem + static_cast<uint32_t>(b * NW);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t sw = smem_u32(smem + s * kStageBytes);
+                    const uint64_t bdesc = sw128_kmajor_desc(sw);
+                    const uint64_t adesc = sw128_kmajor_desc(sw + kWBytes);
+#pragma unroll
+                    for (int k = 0; k < kBlockK / 16; ++k)
+                        umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != 0 || k != 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                umma_commit(&tfull[b]);
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2..5: thread = token row ----------------
+        const int q = warp & 3;
+        const int row = q * 32 + lane;  // TMEM lane
+        const GemmEpiParams& e = a.epi;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        int j = 0;
+        for (int u = c; u < units; u += P, ++j) {
+            const int n = u / m_tiles, m = u % m_tiles;
+            const int tok = m * kWideM + row;
+            const bool valid = tok < a.w;
+            float rn = 1.0f;
+            if (e.ss_in != nullptr && valid) {
+                const float* ssr = e.ss_in + static_cast<size_t>(tok) * e.ss_tiles;
+                float acc = 0.0f;
+                for (int i0 = 0; i0 < e.ss_tiles; i0 += 16) {
+                    float v16[16];
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj) v16[jj] = i0 + jj < e.ss_tiles ? __ldcg(ssr + i0 + jj) : 0.0f;
+#pragma unroll
+                    for (int jj = 0; jj < 16; ++jj)
+                        if (i0 + jj < e.ss_tiles) acc = __fadd_rn(acc, v16[jj]);
+                }
+                rn = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(e.norm_d)), e.eps));
+            }
+            int page = 0, slot = 0, pos = 0;
+            if (e.kind == kEpiQkvRope && valid) {
+                pos = e.ps->n_cached + tok;
+                page = e.page_table[pos / e.page_size];
+                slot = pos % e.page_size;
+            }
+            const int b = j & 1;
+            mbar_wait(&tfull[b], static_cast<uint32_t>((j >> 1) & 1));
+            __syncwarp();
+            tc_fence_after();
+            const uint32_t t_lane = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * NW);
+            wide_tile_epilogue<NW>(a, t_lane, nullptr, 1, 0, n, tok, valid, rn, page, slot, pos);
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<2 * NW>(tmem);
+#endif
+}
+
+cudaError_t launch_gemm_prefill(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x128, int n_out, int k,
+                                int w, const GemmEpiParams& epi, cudaStream_t stream) {
+    static bool attr_set[kMaxDevices] = {};  // per device: TP ranks of one process
+    const int dev = current_device_slot();
+    constexpr int kStages = 4;
+    // 256-row weight tiles (a 128x256x16 MMA per 12 KiB of shared-memory operands
+    // instead of 128x128x16 per 8 KiB) unless 128-row tiles fill the persistent
+    // grid's waves much better (measured: 128-row tiles cost ~35% per flop)
+    const int m_tiles = (w + kWideM - 1) / kWideM;
+    auto wave_eff = [&](int nw) {
+        const int u = m_tiles * (n_out / nw);
+        return static_cast<double>(u) / (((u + kNumSMs - 1) / kNumSMs) * kNumSMs);
+    };
+    const bool nw256 = n_out % 256 == 0 && wave_eff(256) >= wave_eff(128) - 0.2;
+    const uint32_t stage = nw256 ? WideCfg<256>::kStageBytes : WideCfg<128>::kStageBytes;
+    const int smem = static_cast<int>(kStages * stage + 1024 + 64 * 8);
+    if (!attr_set[dev]) {
+        cudaFuncSetAttribute(gemm_prefill_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(gemm_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        attr_set[dev] = true;
+    }
+    GemmArgs a{};
+    a.n_out = n_out;
+    a.k = k;
+    a.w = w;
+    a.nt = kWideM;
+    a.nkb = k / kBlockK;
+    a.tiles = n_out / (nw256 ? 256 : 128);
+    a.stages = kStages;
+    a.epi = epi;
+    const int units = ((w + kWideM - 1) / kWideM) * a.tiles;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(std::min(units, kNumSMs), 1, 1);
+    cfg.blockDim = dim3(kWideThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (nw256) return cudaLaunchKernelEx(&cfg, gemm_prefill_kernel<256>, w_tiled, *map_x128, a);
+    return cudaLaunchKernelEx(&cfg, gemm_prefill_kernel<128>, w_tiled, *map_x128, a);
 }
 
 }  // namespace dd

@@ -29,14 +29,15 @@ struct ModelDims {
 
 // Per-pass state shared by every kernel of a pass (device memory, updated by a
 // single small H2D copy before each pass so captured graphs stay valid).
-constexpr int kMaxPassTokens = 256;
-constexpr int kPrefillChunk = 128;  // dd_prefill's pass width: the tokens-on-M GEMM's tile height
+constexpr int kMaxPassTokens = 256;      // scored passes (logits rows)
+constexpr int kPrefillChunk = 128;       // prompt chunking of tensor-parallel / fp32acc contexts
+constexpr int kMaxPrefillTokens = 2048;  // one prefill pass (gemm_prefill_kernel): weights streamed once
 struct PassState {
     int n_cached;  // tokens already in the KV cache (absolute position of row 0)
     int w;         // tokens in this pass
     int epoch;     // pass sequence number (dataflow flags of the persistent pass kernel)
     int pad;
-    int32_t tokens[kMaxPassTokens];
+    int32_t tokens[kMaxPrefillTokens];  // only the first w are uploaded
 };
 
 // ---------------------------------------------------------------- kernels
@@ -71,6 +72,10 @@ int launch_attention_f32(const PassState* ps, int w, const ModelDims& m, const f
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                      int layer, __nv_bfloat16* o, cudaStream_t s, int ranks = 8);
+// Long-prompt prefill attention (64-query tiles, one warp per 16 queries).
+int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, const float* q,
+                             const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
+                             int layer, __nv_bfloat16* o, cudaStream_t s);
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s);
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,

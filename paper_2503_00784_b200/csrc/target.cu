@@ -460,6 +460,93 @@ double ctx_elapsed_ms(dd_ctx* ctx, int which) {
     return ms;
 }
 
+// One-launch-per-op prefill of a long prompt chunk (w <= kMaxPrefillTokens):
+// embedding, per layer the multi-tile prefill GEMMs (fused RoPE + KV append,
+// residual + deferred-RMSNorm producer, SwiGLU) and the causal attention over
+// the paged cache; no LM head (prefill keeps no logits).
+int enqueue_prefill_big(dd_ctx* ctx, int w) {
+    const ModelDims& m = ctx->m;
+    cudaStream_t s = ctx->stream;
+    GemmEpiParams e{};
+    e.counters = ctx->counters;
+    e.ps = ctx->d_ps;
+    e.rope_cos = ctx->rope_cos;
+    e.rope_sin = ctx->rope_sin;
+    e.q_out = ctx->q;
+    e.kv_pool = ctx->kv_pool;
+    e.page_table = ctx->page_table;
+    e.page_size = ctx->page_size;
+    e.m = m;
+    e.ss_in = ctx->ss;
+    e.ss_tiles = m.d / 128;
+    e.eps = m.eps;
+    e.norm_d = m.d;
+    auto gemm = [&](int id, const __nv_bfloat16* mw, const CUtensorMap* mx, const GemmEpiParams& ep) {
+        int n_out, k;
+        gemm_shape(ctx, id, &n_out, &k);
+        return launch_gemm_prefill(mw, mx, n_out, k, w, ep, s);
+    };
+    launch_embed_norm(ctx->d_ps, w, ctx->emb, ctx->gain_ones, m.d, m.eps, ctx->x, ctx->h, ctx->ss, s);
+    for (int l = 0; l < m.n_layers; ++l) {
+        const LayerW& L = ctx->layers[l];
+        GemmEpiParams eq = e;
+        eq.kind = kEpiQkvRope;
+        eq.layer = l;
+        CK(gemm(kGQkv, L.qkv, &ctx->map_h128, eq));
+        if (launch_attention_prefill(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size,
+                                     l, ctx->o, s))
+            return ctx_fail(ctx, DD_E_CUDA, "attention launch failed");
+        GemmEpiParams er = e;
+        er.kind = kEpiResidual;
+        er.out = ctx->x;
+        er.ss_in = nullptr;
+        er.u_out = ctx->h;
+        er.gain = ctx->gain_ones;
+        er.ss_out = ctx->ss;
+        CK(gemm(kGO, L.o, &ctx->map_o128, er));
+        GemmEpiParams eg = e;
+        eg.kind = kEpiSwiGLU;
+        eg.out_bf = ctx->a;
+        CK(gemm(kGGu, L.gu, &ctx->map_h128, eg));
+        CK(gemm(kGDown, L.dn, &ctx->map_a128, er));
+    }
+    CK(cudaGetLastError());
+    return DD_OK;
+}
+
+// The multi-tile prefill GEMM serves unsharded bf16 contexts; below
+// DD_BIG_PREFILL_MIN tokens the 128-token chunked path is faster (too few
+// (token tile, weight tile) units to fill the GPU).
+bool use_big_prefill(const dd_ctx* ctx, int n) {
+    static const int min_n = getenv("DD_BIG_PREFILL_MIN") ? atoi(getenv("DD_BIG_PREFILL_MIN")) : 512;
+    return ctx->tp_size == 1 && !ctx->fp32acc && n >= min_n;
+}
+
+int run_prefill_big(dd_ctx* ctx, const int32_t* tokens, int w) {
+    if (w < 1 || w > kMaxPrefillTokens) return ctx_fail(ctx, DD_E_CAPACITY, "prefill width out of range");
+    if (ctx->n_cached + w > ctx->max_seq) return ctx_fail(ctx, DD_E_CAPACITY, "KV cache capacity exceeded");
+    for (int i = 0; i < w; ++i)
+        if (tokens[i] < 0 || tokens[i] >= ctx->vocab) return ctx_fail(ctx, DD_E_ARG, "token outside vocabulary");
+    const int slot = ctx->ps_slot;
+    ctx->ps_slot = (slot + 1) % kPsRing;
+    CK(cudaEventSynchronize(ctx->ps_done[slot]));
+    PassState* hp = ctx->h_ps + slot;
+    hp->n_cached = ctx->n_cached;
+    hp->w = w;
+    hp->epoch = ++ctx->epoch;
+    std::memcpy(hp->tokens, tokens, sizeof(int32_t) * w);
+    const size_t bytes = offsetof(PassState, tokens) + sizeof(int32_t) * w;
+    CK(cudaMemcpyAsync(ctx->d_ps, hp, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->h2d_bytes += bytes;
+    CK(cudaEventRecord(ctx->ps_done[slot], ctx->stream));
+    int rc = enqueue_prefill_big(ctx, w);
+    if (rc != DD_OK) return rc;
+    ctx->launches += 1 + 5 * static_cast<uint64_t>(ctx->m.n_layers);
+    ctx->n_cached += w;
+    ctx->last_w = 0;
+    return DD_OK;
+}
+
 // Upload pass state, then replay (or capture) the graph for width w.
 int run_pass(dd_ctx* ctx, const int32_t* tokens, int w, bool want_logits) {
     if (w < 1 || w > kMaxPassTokens) return ctx_fail(ctx, DD_E_CAPACITY, "pass width out of range");
@@ -607,7 +694,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     launch_fill_f32(ctx->gain_ones, gain_n, 1.0f, ctx->stream);
 
     // activations (kMaxPassTokens rows so every TMA box stays in bounds)
-    const size_t R = kMaxPassTokens;
+    const size_t R = kMaxPrefillTokens;  // activation rows: one prefill pass (logits keep kMaxPassTokens)
     CK(cudaMalloc(&ctx->x, sizeof(float) * R * d_));
     CK(cudaMalloc(&ctx->h, sizeof(__nv_bfloat16) * R * d_));
     CK(cudaMalloc(&ctx->q, sizeof(float) * R * m.q_dim()));
@@ -663,7 +750,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     CK(cudaMalloc(&ctx->counters, sizeof(int) * 4096));
     CK(cudaMemset(ctx->counters, 0, sizeof(int) * 4096));
     CK(cudaMalloc(&ctx->ss, sizeof(float) * R * (m.d / 128)));
-    CK(cudaMalloc(&ctx->logits, sizeof(float) * R * ctx->vocab));
+    CK(cudaMalloc(&ctx->logits, sizeof(float) * kMaxPassTokens * ctx->vocab));
     if (tp_size > 1) {
         int max_lv = 0;
         for (int r = 0; r < tp_size; ++r) max_lv = std::max(max_lv, ctx->tp_v0[r + 1] - ctx->tp_v0[r]);
@@ -918,6 +1005,18 @@ int dd_prefill(dd_ctx* ctx, const int32_t* tokens, int n) {
     if (!ctx || (!tokens && n > 0) || n < 0) return ctx_fail(ctx, DD_E_ARG, "bad arguments");
     if (!ctx->weights_ready) return ctx_fail(ctx, DD_E_STATE, "weights not initialised");
     CK(cudaSetDevice(ctx->device));
+    if (use_big_prefill(ctx, n)) {
+        // long prompt: passes of up to kMaxPrefillTokens, equal sizes (weights
+        // streamed once per pass, not once per 128-token chunk)
+        const int passes = (n + kMaxPrefillTokens - 1) / kMaxPrefillTokens;
+        for (int i = 0, p = 0; p < passes; ++p) {
+            const int w = (n - i) / (passes - p);
+            int rc = run_prefill_big(ctx, tokens + i, w);
+            if (rc != DD_OK) return rc;
+            i += w;
+        }
+        return DD_OK;
+    }
     for (int i = 0; i < n; i += kPrefillChunk) {
         const int w = std::min(kPrefillChunk, n - i);
         int rc = run_pass(ctx, tokens + i, w, false);

@@ -124,3 +124,13 @@ def test_hd128_greedy_chain(pair):
     clear = (top2[:, 1] - top2[:, 0]) > 1e-3 * scale
     assert clear.sum() >= 40, f"{name}: only {clear.sum()} clear positions"
     assert (o.argmax(-1) == np.array(chain))[clear].all(), name
+
+
+@pytest.mark.parametrize("n_ctx", [600, 1500])
+def test_hd128_long_prompt_prefill(pair, n_ctx):
+    """A long prompt runs one multi-tile prefill pass (gemm_prefill_kernel:
+    128-token x 256-row tiles, weights streamed once for the prompt, >= 512
+    tokens) instead of 128-token chunks; the cache it writes is then scored at
+    decode and wide widths against the oracle."""
+    for w in (8, 40):
+        _run(pair, n_ctx, w, 3000 + n_ctx + w)
