@@ -81,6 +81,7 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
     n_prompt = len(prompt)
     tail: Optional[P.DraftSequence] = None
     iters = []
+    recs = []  # IterationRecord (tokens_processed, accepted, sequence_count)
     t0 = time.perf_counter()
     target.truncate(0)
     if n_prompt > 1:
@@ -90,7 +91,7 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
         if mode == "vanilla":
             lg = target.forward([verified[-1]])
             verified.append(P.sample(dist(lg[0], temperature, greedy), rv.next_uniform()))
-            committed = 1
+            committed, accepted, n_seq = 1, 0, 0
         elif mode == "sps":
             toks, dists, ctx = [], [], list(verified)
             for _ in range(budget):
@@ -103,7 +104,7 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
             p_rows = [dist(r, temperature, greedy) for r in lg]
             acc, nxt = P.sps_verify(toks, dists, p_rows, rv)
             verified += toks[:acc] + [nxt]
-            committed = acc + 1
+            committed, accepted, n_seq = acc + 1, acc, 1
         else:  # duo (threaded: draft of this iteration overlaps the target pass)
             z = list(verified) + (list(tail.tokens) if tail else [])
             tail_tokens = list(tail.tokens) if tail else []
@@ -118,15 +119,18 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
                 bundle = P.draft_dynamic(drf, z, budget, max_sequences, rd)
                 lg = target.forward([verified[-1]] + tail_tokens)
             p_rows = [dist(r, temperature, greedy) for r in lg]
-            committed, usable = 0, True
+            committed, accepted, usable = 0, 0, True
+            n_seq = len(bundle.sequences)
             if tail is not None:
                 out = P.verify_prefix(tail.tokens, tail.dists, p_rows[:len(tail.tokens)], rv)
                 if out.all_accepted:
                     verified += tail.tokens
                     committed += len(tail.tokens)
+                    accepted += len(tail.tokens)
                 else:
                     verified += tail.tokens[:out.reject_index] + [out.resample]
                     committed += out.reject_index + 1
+                    accepted += out.reject_index
                     usable = False
                 tail = None
             if usable:
@@ -135,6 +139,7 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
                     seq = bundle.sequences[bo.seq_index]
                     verified.append(seq.tokens[0])
                     committed += 1
+                    accepted += 1
                     if len(seq.tokens) > 1:
                         tail = P.DraftSequence(seq.tokens[1:], seq.dists[1:],
                                                float(seq.dists[1][seq.tokens[1]]))
@@ -143,10 +148,12 @@ def run_cpu(mode: str, target: OracleLlama, draft: Optional[OracleLlama], prompt
                     committed += 1
         target.truncate(len(verified) - 1)
         iters.append(committed)
+        recs.append((committed, accepted, n_seq))
         if ttft is None:
             ttft = (time.perf_counter() - t0) * 1e3
     total = (time.perf_counter() - t0) * 1e3
     if worker is not None:
         req.put(None)
         worker.join()
-    return dict(tokens=verified[n_prompt:], ttft_ms=ttft, total_ms=total, iterations=iters)
+    return dict(tokens=verified[n_prompt:], ttft_ms=ttft, total_ms=total, iterations=iters,
+                records=recs)

@@ -70,8 +70,10 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
 // replica `rep` of flag (base + idx)
 __device__ __forceinline__ int* flag_at(int* flags, int base, int idx, int rep) {
@@ -87,10 +89,13 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
     asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// One release fence, then relaxed stores to every replica: each replica's
+// store is ordered after the data by the fence (a release store to replica 0
+// alone would leave the pollers of replicas 1..7 formally unsynchronised).
 __device__ __forceinline__ void st_release_flag(int* flags, int base, int idx, int v) {
-    st_release(flag_at(flags, base, idx, 0), v);  // release orders the replicas after the data
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #pragma unroll
-    for (int r = 1; r < kFlagReplicas; ++r)
+    for (int r = 0; r < kFlagReplicas; ++r)
         asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flag_at(flags, base, idx, r)), "r"(v) : "memory");
 }
 __device__ __forceinline__ void wait_flag(const int* p, int epoch) {
@@ -475,7 +480,7 @@ __device__ void wait_phase_inputs(const PassParams& P, int x_src, int x_flag, in
         const int key = (k_lo + i / per_key) % n_keys;
         const int idx = x_src == kXAttn ? key * 16 + i % per_key : key;
         const int* f = flag_poll(P.flags, x_flag, idx);
-        while (__ldcg(f) - epoch < 0) __nanosleep(64);
+        while (ld_relaxed(f) - epoch < 0) __nanosleep(64);
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     __syncwarp();
@@ -653,6 +658,10 @@ struct Partition {
 
 }  // namespace
 
+// NCHUNK = 16-token chunks of the register-resident epilogue: 1 (W <= 16, the
+// decode widths of every budget up to 16) or 2 (17 <= W <= 32); separate
+// instantiations keep the common one free of the second chunk's registers.
+template <int NCHUNK>
 __global__ void __launch_bounds__(kPassThreads, 1)
     pass_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_o,
                 const __grid_constant__ CUtensorMap map_a, const __grid_constant__ PassParams P) {
@@ -897,7 +906,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             const long g0 = part.begin(c, static_cast<int>(T)), g1 = part.begin(c + 1, static_cast<int>(T));
             if (g1 <= g0) continue;
             if (tid == 0) s_args = ph.a;
-            const bool fast = W <= kFastMaxW;
+            const bool fast = W <= NCHUNK * kChunk;
             if (fast) {
                 // every producer tile of this phase's input is complete before
                 // the phase-level constants are read (lanes poll in parallel)
@@ -965,7 +974,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 bool publish = false;
                 if (fast) {
                     // tokens in chunks of 16 (W <= 32: two chunks), one TMEM load each
-                    const int nch = (W + kChunk - 1) / kChunk;
+                    const int nch = NCHUNK == 1 ? 1 : (W + kChunk - 1) / kChunk;
                     // partial layout [segment][row][Wp] (Wp = W rounded up to 4): one
                     // 16-byte store / load per 4 tokens
                     const int Wp = (W + 3) & ~3;
@@ -1192,13 +1201,14 @@ int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
 cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
                                const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
                                cudaStream_t s) {
-    static int attr_set[kMaxDevices] = {};  // per device: TP ranks of one process
+    static int attr_set[kMaxDevices][2] = {};  // per device: TP ranks of one process
     const int dev = current_device_slot();
-    if (attr_set[dev] < smem_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes);
+    const int two = p.nt > kChunk ? 1 : 0;
+    if (attr_set[dev][two] < smem_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(two ? pass_kernel<2> : pass_kernel<1>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         if (e != cudaSuccess) return e;
-        attr_set[dev] = smem_bytes;
+        attr_set[dev][two] = smem_bytes;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kNumSMs, 1, 1);
@@ -1210,7 +1220,8 @@ cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, pass_kernel, map_h, map_o, map_a, p);
+    return two ? cudaLaunchKernelEx(&cfg, pass_kernel<2>, map_h, map_o, map_a, p)
+               : cudaLaunchKernelEx(&cfg, pass_kernel<1>, map_h, map_o, map_a, p);
 }
 
 }  // namespace dd
