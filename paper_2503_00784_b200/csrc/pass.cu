@@ -774,7 +774,26 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 pass_stamp(P, p, 0);
                 for (int g = g0; g < g1; ++g, src += 8192) {
                     if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
-                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                    if (rp.n >= static_cast<uint32_t>(S)) {
+                        // A ring slot that stays busy for longer than a streaming step
+                        // means the consumer is stalled on a phase boundary (activations
+                        // not yet published): HBM would idle, so pull the next blocks
+                        // into L2 now (bounded distance; in steady streaming the
+                        // window stays at P.prefetch and prefetches never compete
+                        // with the current phase's loads).
+                        if (P.stall_pf > P.prefetch && !mbar_test_wait(&empty[rp.s], rp.ph ^ 1u)) {
+                            const long long t_w = clock64();
+                            bool fired = false;
+                            while (!mbar_test_wait(&empty[rp.s], rp.ph ^ 1u)) {
+                                if (!fired && clock64() - t_w > P.stall_cycles) {
+                                    pf_advance(rp.n + static_cast<uint32_t>(S + P.stall_pf));
+                                    fired = true;
+                                }
+                            }
+                        } else {
+                            mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                        }
+                    }
                     mbar_arrive_expect_tx(&full[rp.s], kABytes);
                     bulk_load(smem + rp.s * stage_bytes, src, kABytes, &full[rp.s], pol_w);
                     rp.next(S);

@@ -41,6 +41,8 @@ struct PassParams {
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
     int attn_cpg;  // attention: 64-key chunks per group before an item is split
+    int stall_pf;      // L2 prefetch distance (k-blocks beyond the ring) once the ring stalls
+    int stall_cycles;  // a wait on a ring slot longer than this is a stall (clock64 cycles)
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 
