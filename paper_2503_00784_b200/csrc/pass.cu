@@ -152,7 +152,7 @@ __device__ __forceinline__ int attn_groups(int n_chunks, int cpg) {
 
 template <int HD>
 __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_smem, int* s_bcast,
-                          int head, int qt, int grp, int epoch, int tid) {
+                          int head, int qt, int grp, int epoch, int tid, int pidx) {
     constexpr int NCH = HD / 32;
     constexpr int CHK = HD / 8;
     constexpr int DW = HD / 4;
@@ -168,7 +168,8 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     const int g = lane >> 2, c = lane & 3;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
     const int qd = md.q_dim();
-    // two K/V chunk buffers: chunk i + 1 is staged while chunk i is computed
+    // kAttnBufs K/V chunk buffers: up to kAttnBufs - 1 chunks are in flight
+    // while one is computed
     constexpr int kBufBytes = 2 * kAttnChunk * HD * 2;
     auto ks_of = [&](int b) {
         return reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + b * kBufBytes);
@@ -176,33 +177,68 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     auto vs_of = [&](int b) {
         return reinterpret_cast<__nv_bfloat16(*)[HD]>(kv_smem + b * kBufBytes + kAttnChunk * HD * 2);
     };
+    // staging addresses: thread = one 16-byte column chunk `sch` of keys
+    // skk0 + 128 / CHK * i; a key's K (V) row is the page base + the
+    // (layer, k|v, kv head, slot) offset, the page base one 64-bit multiply per
+    // key (page table read once per key, L1-resident)
+    const int sch = tid % CHK, skk0 = tid / CHK;
+    const size_t page_elems = kv_offset(md, P.page_size, 1, 0, 0, 0, 0);
+    const uint32_t k_off = static_cast<uint32_t>(kv_offset(md, P.page_size, 0, ph.layer, 0, kvh, 0)) + sch * 8;
+    const uint32_t v_off = static_cast<uint32_t>(kv_offset(md, P.page_size, 0, ph.layer, 1, kvh, 0)) + sch * 8;
     auto stage = [&](int chunk, int b) {
         __nv_bfloat16(*ks)[HD] = ks_of(b);
         __nv_bfloat16(*vs)[HD] = vs_of(b);
         const int kb = chunk * kAttnChunk;
-        for (int idx = tid; idx < kAttnChunk * CHK; idx += 128) {
-            const int kk = idx / CHK, ch = idx % CHK;
+#pragma unroll
+        for (int i = 0; i < kAttnChunk * CHK / 128; ++i) {
+            const int kk = skk0 + (128 / CHK) * i;
             const int key = kb + kk;
             const bool ok = key <= kmax;
             const int kc = ok ? key : 0;
-            const int page = P.page_table[kc / P.page_size], slot = kc % P.page_size;
-            cp_async16(&ks[kk][k_chunk(kk, ch) * 8],
-                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 0, kvh, slot) + ch * 8,
-                       ok ? 16u : 0u);
-            cp_async16(&vs[kk][v_chunk<HD>(kk, ch) * 8],
-                       P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot) + ch * 8,
-                       ok ? 16u : 0u);
+            const __nv_bfloat16* pg = P.kv_pool + static_cast<size_t>(__ldg(P.page_table + kc / P.page_size)) * page_elems;
+            const uint32_t so = static_cast<uint32_t>(kc % P.page_size) * HD;
+            cp_async16(&ks[kk][k_chunk(kk, sch) * 8], pg + k_off + so, ok ? 16u : 0u);
+            cp_async16(&vs[kk][v_chunk<HD>(kk, sch) * 8], pg + v_off + so, ok ? 16u : 0u);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
+    // chunks of this group: grp, grp + active, ... (cnt of them)
+    const int n_mine = (n_chunks - grp + active - 1) / active;
+    int issued = 0;
+    auto issue = [&]() {
+        stage(grp + issued * active, issued % kAttnBufs);
+        ++issued;
+    };
+    // Keys cached before this pass do not depend on the QKV phase: their
+    // chunks are in flight before the flags are polled, so only the chunk(s)
+    // holding this pass's keys wait for the QKV epilogue.
+    if (tid == 0) pass_stamp(P, pidx, 0);  // debug: item entered
+    // The cached keys' later chunks (beyond the cp.async window) are pulled
+    // into L2 now, one bulk prefetch per contiguous page run of K and of V:
+    // the chunk loop then stages them at L2 rather than HBM latency.
+    {
+        const int run = min(P.page_size, kAttnChunk);  // keys per contiguous run
+        const int runs_per_chunk = kAttnChunk / run;
+        const int n_runs = max(0, n_mine - (kAttnBufs - 1)) * runs_per_chunk;
+        for (int r = tid; r < n_runs; r += 128) {
+            const int chunk = grp + (kAttnBufs - 1 + r / runs_per_chunk) * active;
+            const int key = chunk * kAttnChunk + (r % runs_per_chunk) * run;
+            if (key + run > n0) continue;  // this pass's keys: written by the QKV epilogue
+            const int page = P.page_table[key / P.page_size], slot = key % P.page_size;
+            prefetch_l2(P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 0, kvh, slot), run * HD * 2);
+            prefetch_l2(P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot), run * HD * 2);
+        }
+    }
+    while (issued < min(n_mine, kAttnBufs - 1) && (grp + issued * active + 1) * kAttnChunk <= n0) issue();
     // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
     if (tid < 3) {  // q, k and v tiles polled in parallel
         const int row = tid == 0 ? head * HD : tid == 1 ? qd + kvh * HD : qd + md.kv_dim() + kvh * HD;
         wait_flag(flag_poll(P.flags, ph.qkv_flag, row / 128), epoch);
     }
     epi_bar();
-    stage(grp, 0);  // the first chunk's K / V are in flight while Q is loaded
+    if (tid == 0) pass_stamp(P, pidx, 1);  // debug: QKV flags seen
+    while (issued < min(n_mine, kAttnBufs - 1)) issue();  // in flight while Q is loaded
 
     const int pos_g = n0 + qt * 16 + g, pos_g8 = pos_g + 8;
     const bool v_g = qt * 16 + g < W, v_g8 = qt * 16 + g + 8 < W;
@@ -237,14 +273,17 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
 
     for (int i = 0, chunk = grp; chunk < n_chunks; ++i, chunk += active) {
         const int kb = chunk * kAttnChunk;
-        const int b = i & 1;
-        if (chunk + active < n_chunks) {
-            stage(chunk + active, b ^ 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        const int b = i % kAttnBufs;
+        if (issued < n_mine) issue();  // into the buffer chunk i - 1 released
+        // chunk i landed: at most (issued - 1 - i) younger groups pending
+        switch (issued - 1 - i) {
+            case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+            case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+            case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+            default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
         }
         epi_bar();
+        if (tid == 0 && i == 0) pass_stamp(P, pidx, 2);  // debug: first chunk staged
         __nv_bfloat16(*ks)[HD] = ks_of(b);
         __nv_bfloat16(*vs)[HD] = vs_of(b);
         float s[NJ][4];
@@ -335,6 +374,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
         l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
         l_g8 += __shfl_xor_sync(0xffffffffu, l_g8, off);
     }
+    if (tid == 0) pass_stamp(P, pidx, 4);  // debug: chunks done
     const int dcol = warp * DW + 2 * c * NTW;  // C columns 2c / 2c+1 -> dims dcol + e / + NTW + e
     const int flag_idx = head * 16 + qt;
     if (active == 1) {
@@ -353,7 +393,11 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
             }
         }
         epi_bar();  // every thread's o stores happen-before thread 0's release
-        if (tid == 0) st_release_flag(P.flags, ph.out_flag, flag_idx, epoch);
+        if (tid == 0) {
+            pass_stamp(P, pidx, 5);  // debug: o stored
+            st_release_flag(P.flags, ph.out_flag, flag_idx, epoch);
+            pass_stamp(P, pidx, 6);  // debug: published
+        }
         return;
     }
     // partials: [head][qt][grp] x (16 rows x (HD + 2)), unnormalised O, m, l
@@ -504,7 +548,7 @@ struct FastEpi {
 };
 // FastEpi lives in the attention K/V staging area (the epilogue warps run GEMM
 // epilogues and attention items one after the other, never both at once)
-static_assert(sizeof(FastEpi) <= 4 * kAttnChunk * 64 * 2, "FastEpi exceeds the K/V staging area");
+static_assert(sizeof(FastEpi) <= kAttnBufs * 2 * kAttnChunk * 64 * 2, "FastEpi exceeds the K/V staging area");
 
 // Tokens [t0, t0 + 16) of the pass (W <= 32 runs two chunks).
 __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, int tile, int t0, float* v,
@@ -667,8 +711,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 const __grid_constant__ CUtensorMap map_a, const __grid_constant__ PassParams P) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // 1024-byte aligned by pointer arithmetic on the __shared__ array (not an
+    // integer round trip), so the compiler keeps the shared address space and
+    // emits LDS/STS for every access derived from it
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nctas = gridDim.x;
     int c;  // this CTA's rank in the stream-K partition
@@ -683,7 +729,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const uint32_t stage_bytes = kABytes + b_bytes;
     const int hd = P.m.head_dim;
     uint8_t* kv_smem = smem + S * stage_bytes;                          // attention K/V chunk
-    float* red = reinterpret_cast<float*>(kv_smem + 4 * kAttnChunk * hd * 2);  // [kChunk][128]
+    float* red = reinterpret_cast<float*>(kv_smem + kAttnBufs * 2 * kAttnChunk * hd * 2);  // [kChunk][128]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -774,26 +820,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 pass_stamp(P, p, 0);
                 for (int g = g0; g < g1; ++g, src += 8192) {
                     if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
-                    if (rp.n >= static_cast<uint32_t>(S)) {
-                        // A ring slot that stays busy for longer than a streaming step
-                        // means the consumer is stalled on a phase boundary (activations
-                        // not yet published): HBM would idle, so pull the next blocks
-                        // into L2 now (bounded distance; in steady streaming the
-                        // window stays at P.prefetch and prefetches never compete
-                        // with the current phase's loads).
-                        if (P.stall_pf > P.prefetch && !mbar_test_wait(&empty[rp.s], rp.ph ^ 1u)) {
-                            const long long t_w = clock64();
-                            bool fired = false;
-                            while (!mbar_test_wait(&empty[rp.s], rp.ph ^ 1u)) {
-                                if (!fired && clock64() - t_w > P.stall_cycles) {
-                                    pf_advance(rp.n + static_cast<uint32_t>(S + P.stall_pf));
-                                    fired = true;
-                                }
-                            }
-                        } else {
-                            mbar_wait(&empty[rp.s], rp.ph ^ 1u);
-                        }
-                    }
+                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
                     mbar_arrive_expect_tx(&full[rp.s], kABytes);
                     bulk_load(smem + rp.s * stage_bytes, src, kABytes, &full[rp.s], pol_w);
                     rp.next(S);
@@ -911,9 +938,9 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     for (int act = active_of(0); grp >= act; act = active_of(++qt)) grp -= act;
                     if (tid == 0) PASS_DBG(6, p * 100000 + item);
                     if (hd == 128)
-                        attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);
+                        attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid, p);
                     else
-                        attn_item<64>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid);
+                        attn_item<64>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid, p);
                 }
                 if (tid == 0) pass_stamp(P, p, 3);
                 continue;
@@ -1207,7 +1234,7 @@ size_t pass_attn_cnt_ints(const ModelDims& m) { return static_cast<size_t>(m.n_h
 
 int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
     const int stage_bytes = static_cast<int>(kABytes) + nt * 128;
-    const int fixed = 1024 /* align */ + 4 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
+    const int fixed = 1024 /* align */ + kAttnBufs * 2 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
     const int budget = 225 * 1024 - 2048 /* static shared */;
     static const int cap = getenv("DD_PASS_STAGES") ? atoi(getenv("DD_PASS_STAGES")) : 8;
     int s = (budget - fixed) / stage_bytes;

@@ -40,9 +40,7 @@ struct PassParams {
     int nt;
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
-    int attn_cpg;  // attention: 64-key chunks per group before an item is split
-    int stall_pf;      // L2 prefetch distance (k-blocks beyond the ring) once the ring stalls
-    int stall_cycles;  // a wait on a ring slot longer than this is a stall (clock64 cycles)
+    int attn_cpg;  // attention: kAttnChunk-key chunks per group before an item is split
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 
@@ -67,7 +65,9 @@ struct PassParams {
 };
 
 constexpr int kPassThreads = 256;
-constexpr int kAttnChunk = 64;    // keys staged per attention step
+constexpr int kAttnChunk = 32;    // keys staged per attention step
+constexpr int kAttnBufs = 4;      // K/V chunk buffers (up to 3 chunks in flight)
+static_assert(kAttnBufs == 4, "attn_item's cp.async wait ladder assumes 4 buffers");
 constexpr int kAttnGroups = 4;    // chunk groups per (head, query tile)
 constexpr int kCounterStride = 32;  // ints: one 128-byte line per stream-K tile counter
 constexpr int kFlagStride = 32;   // ints: one 128-byte line per flag replica

@@ -391,17 +391,11 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.tmem_buf = tmem_buf_for(p.nt);
     static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 4;
     p.prefetch = env_pf;
-    // up to 6 chunks (384 keys) per attention group: below that the groups'
+    // up to 12 chunks (384 keys) per attention group: below that the groups'
     // partial round trip and combine cost more than running the chunks in
     // sequence (scripts/pass_ab.py with DD_ATTN_CPG)
-    static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 6;
+    static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 12;
     p.attn_cpg = env_cpg;
-    // L2 prefetch on a stalled ring (phase boundaries, attention): distance and
-    // the wait (cycles) that counts as a stall
-    static const int env_spf = getenv("DD_PASS_STALL_PF") ? atoi(getenv("DD_PASS_STALL_PF")) : 0;
-    static const int env_scy = getenv("DD_PASS_STALL_CYC") ? atoi(getenv("DD_PASS_STALL_CYC")) : 2000;
-    p.stall_pf = env_spf;
-    p.stall_cycles = env_scy;
     const int smem = pass_smem_bytes(m, p.nt, &p.stages);
     if (smem < 0) return ctx_fail(ctx, DD_E_ARG, "pass kernel shared memory plan failed");
     p.ps = ctx->d_ps;
