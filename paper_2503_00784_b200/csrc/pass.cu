@@ -64,6 +64,22 @@ __device__ __forceinline__ void pass_stamp(const PassParams& P, int p, int k) {
 namespace {
 
 constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
+#ifndef DD_ACC_BUFS
+#define DD_ACC_BUFS 4
+#endif
+#ifndef DD_PUB_OFFLOAD
+#define DD_PUB_OFFLOAD 1
+#endif
+constexpr int kAccBufs = DD_ACC_BUFS;  // TMEM accumulators: the MMA runs up to kAccBufs tile segments ahead of the epilogue
+// Publish ring: the epilogue hands every gpu-scope release (stream-K partial
+// counters, tile flags) to warp 3, so its own threads never wait for the
+// release's memory barrier before starting the next tile.
+constexpr int kPubSlots = 8;
+enum PubKind { kPubExit = 0, kPubCount = 1, kPubFlag = 2 };
+struct PubAction {
+    int kind, base, idx, phase;
+    int* ptr;
+};
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -234,7 +250,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
     if (tid < 3) {  // q, k and v tiles polled in parallel
         const int row = tid == 0 ? head * HD : tid == 1 ? qd + kvh * HD : qd + md.kv_dim() + kvh * HD;
-        wait_flag(flag_poll(P.flags, ph.qkv_flag, row / 128), epoch);
+        if (!(P.nodep & 4)) wait_flag(flag_poll(P.flags, ph.qkv_flag, row / 128), epoch);
     }
     epi_bar();
     if (tid == 0) pass_stamp(P, pidx, 1);  // debug: QKV flags seen
@@ -494,37 +510,61 @@ __device__ void embed_tile(const PassParams& P, int tile, int W, float* part /* 
     }
 }
 
+// One sub-phase of a GEMM phase (PassPhase.kg x PassPhase.tg grid, k-group major).
+struct SubPhase {
+    int tiles, nkb, T;  // tile count, k-blocks per tile, blocks
+    int tile0, kb0;     // first global tile / k-block
+    int ki;             // k-group index
+    bool last_k;        // the k-group that completes its tiles
+};
+__device__ __forceinline__ SubPhase sub_of(const PassPhase& ph, int sp) {
+    SubPhase s;
+    const int i = sp / ph.tg, j = sp - i * ph.tg;
+    s.tiles = ph.a.tiles / ph.tg;
+    s.nkb = ph.a.nkb / ph.kg;
+    s.T = s.tiles * s.nkb;
+    s.tile0 = j * s.tiles;
+    s.kb0 = i * s.nkb;
+    s.ki = i;
+    s.last_k = i == ph.kg - 1;
+    return s;
+}
 
-// Wait until every producer flag feeding this CTA's k-blocks of a GEMM phase
-// is published.  Run by the whole activation-producer warp: the distinct
-// producer keys of the range form one contiguous (wrapping) run, each lane
-// spins on its own subset of flags (weak L2 loads), then acq_rel fences and a
-// warp sync order every TMA read that follows (plus the generic -> async proxy
-// fence for the TMA engine).
-__device__ void wait_phase_inputs(const PassParams& P, int x_src, int x_flag, int nkb, int g0, int g1,
-                                  int epoch, int qtiles, int lane) {
+// Inputs of one sub-phase's k-range [g0, g1): the k-blocks it covers form one
+// run (or two, when the range wraps into the next tile) inside the k-group;
+// each lane spins on its own subset of the producer flags of those k-blocks
+// (weak L2 loads), then acq_rel fences and a warp sync order every TMA read
+// that follows (plus the generic -> async proxy fence for the TMA engine).
+__device__ void wait_sub_inputs(const PassParams& P, int x_src, int x_flag, const SubPhase& s, int g0, int g1,
+                                int epoch, int qtiles, int lane) {
     const int hd_shift = P.m.head_dim == 128 ? 7 : 6;
     auto key_of = [&](int kb) {
         return x_src == kXNormed ? kb >> 1 : x_src == kXSwiglu ? kb : (kb * 64) >> hd_shift;
     };
-    const int n_keys = x_src == kXNormed ? nkb >> 1 : x_src == kXSwiglu ? nkb : (nkb * 64) >> hd_shift;
-    const int n = min(g1 - g0, nkb);
-    const int kb0 = g0 % nkb;
-    int k_lo, count;
-    if (n == nkb) {
-        k_lo = 0;
-        count = n_keys;
+    const int n = min(g1 - g0, s.nkb);
+    int lo[2], hi[2], runs = 1;
+    if (n == s.nkb) {
+        lo[0] = s.kb0;
+        hi[0] = s.kb0 + s.nkb - 1;
     } else {
-        k_lo = key_of(kb0);
-        const int k_hi = key_of((kb0 + n - 1) % nkb);
-        count = (k_hi - k_lo + n_keys) % n_keys + 1;
+        const int a = s.kb0 + g0 % s.nkb, e = a + n - 1, top = s.kb0 + s.nkb - 1;
+        lo[0] = a;
+        hi[0] = min(e, top);
+        if (e > top) {
+            lo[1] = s.kb0;
+            hi[1] = e - s.nkb;
+            runs = 2;
+        }
     }
     const int per_key = x_src == kXAttn ? qtiles : 1;
-    for (int i = lane; i < count * per_key; i += 32) {
-        const int key = (k_lo + i / per_key) % n_keys;
-        const int idx = x_src == kXAttn ? key * 16 + i % per_key : key;
-        const int* f = flag_poll(P.flags, x_flag, idx);
-        while (ld_relaxed(f) - epoch < 0) __nanosleep(64);
+    for (int r = 0; r < runs; ++r) {
+        const int k_lo = key_of(lo[r]), count = key_of(hi[r]) - k_lo + 1;
+        for (int i = lane; i < count * per_key; i += 32) {
+            const int key = k_lo + i / per_key;
+            const int idx = x_src == kXAttn ? key * 16 + i % per_key : key;
+            const int* f = flag_poll(P.flags, x_flag, idx);
+            while (!(P.nodep & 1) && ld_relaxed(f) - epoch < 0) __nanosleep(64);
+        }
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     __syncwarp();
@@ -733,8 +773,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + kAccBufs;
+    uint64_t* pfull = tempty + kAccBufs;  // publish ring (epilogue -> warp 3)
+    uint64_t* pempty = pfull + kPubSlots;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + kPubSlots);
+    __shared__ PubAction s_pub[kPubSlots];
     __shared__ int s_last;
     __shared__ float s_r[kChunk];
     __shared__ float s_part[4 * 32];
@@ -747,9 +790,13 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             mbar_init(&full[s], 2);  // weight producer + activation producer
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kAccBufs; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], kEpiThreads);
+        }
+        for (int b = 0; b < kPubSlots; ++b) {
+            mbar_init(&pfull[b], 1);
+            mbar_init(&pempty[b], 1);
         }
         fence_barrier_init();
         tma_prefetch_desc(&map_h);
@@ -757,7 +804,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         tma_prefetch_desc(&map_a);
     }
     if (warp == 1) {
-        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * 2);
+        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * kAccBufs);
         if (cols <= 64) tmem_alloc<64>(tmem_slot);
         else if (cols <= 128) tmem_alloc<128>(tmem_slot);
         else if (cols <= 256) tmem_alloc<256>(tmem_slot);
@@ -781,29 +828,41 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             // ---------------- weight producer ----------------
             const uint64_t pol_w = policy_evict_first();
             // L2 prefetch cursor runs P.prefetch blocks ahead of the ring loads,
-            // across phase boundaries, so HBM keeps streaming while a phase
+            // across (sub-)phase boundaries, so HBM keeps streaming while a phase
             // waits for its activations
-            int pf_p = 0;
-            long pf_g = -1, pf_g1 = -1;
-            const __nv_bfloat16* pf_w = nullptr;
+            int pf_p = -1, pf_sp = 0, pf_nsp = 0, pf_g = 0, pf_g1 = 0, pf_lkb = 0, pf_nkb = 1;
+            const __nv_bfloat16* pf_src = nullptr;
+            size_t pf_skip = 0;
             uint32_t pf_it = 0;
             auto pf_advance = [&](uint32_t target) {
                 while (pf_it < target) {
-                    if (pf_g >= pf_g1) {  // next GEMM phase with work
-                        for (; pf_p < P.n_phases; ++pf_p) {
-                            const PassPhase& q = P.phases[pf_p];
-                            if (q.type != kPhGemm) continue;
-                            const long T = static_cast<long>(q.a.tiles) * q.a.nkb;
-                            const Partition pq{q.begins, nctas};
-                            pf_g = pq.begin(c, static_cast<int>(T));
-                            pf_g1 = pq.begin(c + 1, static_cast<int>(T));
-                            pf_w = q.w;
-                            if (pf_g < pf_g1) break;
+                    while (pf_g >= pf_g1) {  // next sub-phase with work
+                        if (pf_sp >= pf_nsp) {
+                            if (pf_p >= P.n_phases) return;
+                            do {
+                                ++pf_p;
+                            } while (pf_p < P.n_phases && P.phases[pf_p].type != kPhGemm);
+                            if (pf_p >= P.n_phases) return;
+                            pf_sp = 0;
+                            pf_nsp = P.phases[pf_p].kg * P.phases[pf_p].tg;
                         }
-                        if (pf_p >= P.n_phases) return;
-                        ++pf_p;
+                        const PassPhase& q = P.phases[pf_p];
+                        const SubPhase sq = sub_of(q, pf_sp++);
+                        const Partition pq{q.begins, nctas};
+                        pf_g = pq.begin(c, sq.T);
+                        pf_g1 = pq.begin(c + 1, sq.T);
+                        const int lt = pf_g / sq.nkb;
+                        pf_lkb = pf_g - lt * sq.nkb;
+                        pf_nkb = sq.nkb;
+                        pf_src = q.w + (static_cast<size_t>(sq.tile0 + lt) * q.a.nkb + sq.kb0 + pf_lkb) * 8192;
+                        pf_skip = static_cast<size_t>(q.a.nkb - sq.nkb) * 8192;
                     }
-                    prefetch_l2(pf_w + pf_g * 8192, kABytes);
+                    prefetch_l2(pf_src, kABytes);
+                    pf_src += 8192;
+                    if (++pf_lkb == pf_nkb) {
+                        pf_lkb = 0;
+                        pf_src += pf_skip;
+                    }
                     ++pf_g;
                     ++pf_it;
                 }
@@ -812,18 +871,31 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             for (int p = 0; p < P.n_phases; ++p) {
                 const PassPhase& ph = P.phases[p];
                 if (ph.type != kPhGemm) continue;
-                const long T = static_cast<long>(ph.a.tiles) * ph.a.nkb;
                 const Partition part{ph.begins, nctas};
-                const int g0 = part.begin(c, static_cast<int>(T));
-                const int g1 = part.begin(c + 1, static_cast<int>(T));
-                const __nv_bfloat16* src = ph.w + static_cast<size_t>(g0) * 8192;
+                const int nsp = ph.kg * ph.tg;
                 pass_stamp(P, p, 0);
-                for (int g = g0; g < g1; ++g, src += 8192) {
-                    if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
-                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
-                    mbar_arrive_expect_tx(&full[rp.s], kABytes);
-                    bulk_load(smem + rp.s * stage_bytes, src, kABytes, &full[rp.s], pol_w);
-                    rp.next(S);
+                for (int sp = 0; sp < nsp; ++sp) {
+                    const SubPhase sb = sub_of(ph, sp);
+                    const int g0 = part.begin(c, sb.T);
+                    const int g1 = part.begin(c + 1, sb.T);
+                    if (g1 <= g0) continue;
+                    const int lt = g0 / sb.nkb;
+                    int lkb = g0 - lt * sb.nkb;
+                    const __nv_bfloat16* src =
+                        ph.w + (static_cast<size_t>(sb.tile0 + lt) * ph.a.nkb + sb.kb0 + lkb) * 8192;
+                    const size_t skip = static_cast<size_t>(ph.a.nkb - sb.nkb) * 8192;
+                    for (int g = g0; g < g1; ++g) {
+                        if (P.prefetch > 0) pf_advance(rp.n + static_cast<uint32_t>(S + P.prefetch));
+                        if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                        mbar_arrive_expect_tx(&full[rp.s], kABytes);
+                        bulk_load(smem + rp.s * stage_bytes, src, kABytes, &full[rp.s], pol_w);
+                        rp.next(S);
+                        src += 8192;
+                        if (++lkb == sb.nkb) {
+                            lkb = 0;
+                            src += skip;
+                        }
+                    }
                 }
                 pass_stamp(P, p, 11);
             }
@@ -837,29 +909,32 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         for (int p = 0; p < P.n_phases; ++p) {
             const PassPhase& ph = P.phases[p];
             if (ph.type != kPhGemm) continue;
-            const int nkb = ph.a.nkb;
-            const long T = static_cast<long>(ph.a.tiles) * nkb;
             const Partition part{ph.begins, nctas};
-            const int g0 = part.begin(c, static_cast<int>(T));
-            const int g1 = part.begin(c + 1, static_cast<int>(T));
-            if (g1 <= g0) continue;
+            const CUtensorMap* mx = ph.x_map == 0 ? &map_h : ph.x_map == 1 ? &map_o : &map_a;
+            const int nsp = ph.kg * ph.tg;
             if (lane == 0) pass_stamp(P, p, 7);
-            wait_phase_inputs(P, ph.x_src, ph.x_flag, nkb, g0, g1, epoch, qtiles, lane);
-            if (lane == 0) {
-                pass_stamp(P, p, 1);
-                const CUtensorMap* mx = ph.x_map == 0 ? &map_h : ph.x_map == 1 ? &map_o : &map_a;
-                int kb = g0 % nkb;
-                for (int g = g0; g < g1; ++g) {
-                    if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
-                    mbar_arrive_expect_tx(&full[rp.s], b_bytes);
-                    uint8_t* sb = smem + rp.s * stage_bytes + kABytes;
-                    for (int r = 0; r < nbox; ++r)
-                        tma_load_2d(sb + r * 2048, mx, &full[rp.s], kb * kBlockK, r * 16, pol_x);
-                    rp.next(S);
-                    if (++kb == nkb) kb = 0;
+            for (int sp = 0; sp < nsp; ++sp) {
+                const SubPhase sb = sub_of(ph, sp);
+                const int g0 = part.begin(c, sb.T);
+                const int g1 = part.begin(c + 1, sb.T);
+                if (g1 <= g0) continue;
+                wait_sub_inputs(P, ph.x_src, ph.x_flag, sb, g0, g1, epoch, qtiles, lane);
+                if (lane == 0) {
+                    if (sp == 0) pass_stamp(P, p, 1);
+                    int kb = sb.kb0 + g0 % sb.nkb;
+                    const int kb_end = sb.kb0 + sb.nkb;
+                    for (int g = g0; g < g1; ++g) {
+                        if (rp.n >= static_cast<uint32_t>(S)) mbar_wait(&empty[rp.s], rp.ph ^ 1u);
+                        mbar_arrive_expect_tx(&full[rp.s], b_bytes);
+                        uint8_t* sbuf = smem + rp.s * stage_bytes + kABytes;
+                        for (int r = 0; r < nbox; ++r)
+                            tma_load_2d(sbuf + r * 2048, mx, &full[rp.s], kb * kBlockK, r * 16, pol_x);
+                        rp.next(S);
+                        if (++kb == kb_end) kb = sb.kb0;
+                    }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -870,34 +945,36 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             for (int p = 0; p < P.n_phases; ++p) {
                 const PassPhase& ph = P.phases[p];
                 if (ph.type != kPhGemm) continue;
-                const int nkb = ph.a.nkb;
-                const long T = static_cast<long>(ph.a.tiles) * nkb;
                 const Partition part{ph.begins, nctas};
-                const int g0 = part.begin(c, static_cast<int>(T));
-                const int g1 = part.begin(c + 1, static_cast<int>(T));
-                if (g1 <= g0) continue;
-                const int tile_lo = g0 / nkb, tile_hi = (g1 - 1) / nkb;
-                for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
-                    const int lo = max(g0, tile * nkb);
-                    const int hi = min(g1, (tile + 1) * nkb);
-                    const int b = u & 1;
-                    if (u >= 2) mbar_wait(&tempty[b], ((u >> 1) - 1) & 1u);
-                    tc_fence_after();
-                    const uint32_t acc = tmem + static_cast<uint32_t>(b * P.tmem_buf);
-                    for (int g = lo; g < hi; ++g) {
-                        mbar_wait(&full[rp.s], rp.ph);
+                const int nsp = ph.kg * ph.tg;
+                for (int sp = 0; sp < nsp; ++sp) {
+                    const SubPhase sb = sub_of(ph, sp);
+                    const int g0 = part.begin(c, sb.T);
+                    const int g1 = part.begin(c + 1, sb.T);
+                    if (g1 <= g0) continue;
+                    const int tile_lo = g0 / sb.nkb, tile_hi = (g1 - 1) / sb.nkb;
+                    for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
+                        const int lo = max(g0, tile * sb.nkb);
+                        const int hi = min(g1, (tile + 1) * sb.nkb);
+                        const int b = u & (kAccBufs - 1);
+                        if (u >= kAccBufs) mbar_wait(&tempty[b], ((u / kAccBufs) - 1) & 1u);
                         tc_fence_after();
-                        const uint32_t sa = smem_u32(smem + rp.s * stage_bytes);
-                        const uint64_t adesc = sw128_kmajor_desc(sa);
-                        const uint64_t bdesc = sw128_kmajor_desc(sa + kABytes);
+                        const uint32_t acc = tmem + static_cast<uint32_t>(b * P.tmem_buf);
+                        for (int g = lo; g < hi; ++g) {
+                            mbar_wait(&full[rp.s], rp.ph);
+                            tc_fence_after();
+                            const uint32_t sa = smem_u32(smem + rp.s * stage_bytes);
+                            const uint64_t adesc = sw128_kmajor_desc(sa);
+                            const uint64_t bdesc = sw128_kmajor_desc(sa + kABytes);
 #pragma unroll
-                        for (int k = 0; k < kBlockK / 16; ++k)
-                            umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc,
-                                      (g != lo || k != 0) ? 1u : 0u);
-                        umma_commit(&empty[rp.s]);
-                        rp.next(S);
+                            for (int k = 0; k < kBlockK / 16; ++k)
+                                umma_bf16(acc, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                          (g != lo || k != 0) ? 1u : 0u);
+                            umma_commit(&empty[rp.s]);
+                            rp.next(S);
+                        }
+                        umma_commit(&tfull[b]);
                     }
-                    umma_commit(&tfull[b]);
                 }
                 pass_stamp(P, p, 2);
             }
@@ -908,6 +985,26 @@ __global__ void __launch_bounds__(kPassThreads, 1)
         const int q = warp & 3;                  // TMEM lane quarter
         const int row = q * 32 + lane;
         uint32_t u = 0;
+        uint32_t pub_n = 0;  // (thread 0) publish-ring cursor
+        auto post_pub = [&](int kind, int base, int idx, int* ptr, int ph_idx) {
+            if (!DD_PUB_OFFLOAD) {
+                if (kind == kPubCount) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ptr) : "memory");
+                else if (kind == kPubFlag) {
+                    st_release_flag(P.flags, base, idx, epoch);
+                    pass_stamp(P, ph_idx, 6);
+                }
+                return;
+            }
+            const int sl = static_cast<int>(pub_n % kPubSlots);
+            if (pub_n >= static_cast<uint32_t>(kPubSlots)) mbar_wait(&pempty[sl], ((pub_n / kPubSlots) - 1) & 1u);
+            s_pub[sl].kind = kind;
+            s_pub[sl].base = base;
+            s_pub[sl].idx = idx;
+            s_pub[sl].phase = ph_idx;
+            s_pub[sl].ptr = ptr;
+            mbar_arrive(&pfull[sl]);  // release (CTA scope): the slot and every store before the epi_bar
+            ++pub_n;
+        };
         for (int p = 0; p < P.n_phases; ++p) {
             const PassPhase& ph = P.phases[p];
             if (tid == 0) PASS_DBG(4, p);
@@ -946,267 +1043,302 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 continue;
             }
             // GEMM epilogue
-            const int nkb = ph.a.nkb;
-            const long T = static_cast<long>(ph.a.tiles) * nkb;
             const Partition part{ph.begins, nctas};
-            const long g0 = part.begin(c, static_cast<int>(T)), g1 = part.begin(c + 1, static_cast<int>(T));
-            if (g1 <= g0) continue;
+            const int nsp = ph.kg * ph.tg, kg = ph.kg;
             if (tid == 0) s_args = ph.a;
-            const bool fast = W <= NCHUNK * kChunk;
-            if (fast) {
-                // every producer tile of this phase's input is complete before
-                // the phase-level constants are read (lanes poll in parallel)
-                const int hd_shift = P.m.head_dim == 128 ? 7 : 6;
-                const int n_keys = ph.x_src == kXNormed ? nkb >> 1 : ph.x_src == kXSwiglu ? nkb
-                                                                     : (nkb * 64) >> hd_shift;
-                const int per_key = ph.x_src == kXAttn ? qtiles : 1;
-                for (int i = tid; i < n_keys * per_key; i += kEpiThreads) {
-                    const int key = i / per_key;
-                    const int idx = ph.x_src == kXAttn ? key * 16 + i % per_key : key;
-                    wait_flag(flag_poll(P.flags, ph.x_flag, idx), epoch);
-                }
-                epi_bar();
-                const GemmEpiParams& ep = ph.a.epi;
-                if (ep.ss_in != nullptr && tid < W) {
-                    const float* ssr = ep.ss_in + static_cast<size_t>(tid) * ep.ss_tiles;
-                    float acc = 0.0f;
-                    for (int i0 = 0; i0 < ep.ss_tiles; i0 += 16) {
-                        float v16[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v16[j] = i0 + j < ep.ss_tiles ? __ldcg(ssr + i0 + j) : 0.0f;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (i0 + j < ep.ss_tiles) acc = __fadd_rn(acc, v16[j]);
-                    }
-                    s_fe.rn[tid] = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(ep.norm_d)), ep.eps));
-                }
-                if (ep.kind == kEpiQkvRope) {
-                    const int half = P.m.head_dim / 2;
-                    const int n0 = P.ps->n_cached;
-                    for (int idx = tid; idx < W * half; idx += kEpiThreads) {
-                        const int t = idx / half, i = idx % half;
-                        s_fe.cs[t][i] = ep.rope_cos[static_cast<size_t>(n0 + t) * half + i];
-                        s_fe.sn[t][i] = ep.rope_sin[static_cast<size_t>(n0 + t) * half + i];
-                    }
-                    if (tid < W) {
-                        const int pos = n0 + tid;
-                        s_fe.page[tid] = ep.page_table[pos / ep.page_size];
-                        s_fe.slot[tid] = pos % ep.page_size;
-                    }
-                }
-            }
             epi_bar();
             const GemmArgs& a = s_args;
+            const bool fast = W <= NCHUNK * kChunk;
             const bool resid = a.epi.kind == kEpiResidual;
-            const int tile_lo = static_cast<int>(g0 / nkb), tile_hi = static_cast<int>((g1 - 1) / nkb);
-            for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
-                int nseg, seg;
-                part.segments(tile, nkb, static_cast<int>(T), c, &nseg, &seg);
-                const int b = u & 1;
-                float xv[kChunk];
-                float gcol = 1.0f;
-                if (fast && resid) {  // residual rows of this tile, before the accumulator lands
+            bool consts = false;  // phase-level constants loaded (at the CTA's first sub-phase of the last k-group, before its tiles land)
+            for (int sp = 0; sp < nsp; ++sp) {
+                const SubPhase sb = sub_of(ph, sp);
+                const int g0 = part.begin(c, sb.T), g1 = part.begin(c + 1, sb.T);
+                if (g1 <= g0) continue;
+                if (sb.last_k && fast && !consts) {
+                    // every producer tile of this phase's input is complete before
+                    // the phase-level constants are read (lanes poll in parallel)
+                    consts = true;
+                    const int hd_shift = P.m.head_dim == 128 ? 7 : 6;
+                    const int nkb = ph.a.nkb;
+                    const int n_keys = ph.x_src == kXNormed ? nkb >> 1 : ph.x_src == kXSwiglu ? nkb
+                                                                         : (nkb * 64) >> hd_shift;
+                    const int per_key = ph.x_src == kXAttn ? qtiles : 1;
+                    for (int i = tid; i < n_keys * per_key; i += kEpiThreads) {
+                        const int key = i / per_key;
+                        const int idx = ph.x_src == kXAttn ? key * 16 + i % per_key : key;
+                        if (!(P.nodep & 2)) wait_flag(flag_poll(P.flags, ph.x_flag, idx), epoch);
+                    }
+                    epi_bar();
+                    const GemmEpiParams& ep = a.epi;
+                    if (ep.ss_in != nullptr && tid < W) {
+                        const float* ssr = ep.ss_in + static_cast<size_t>(tid) * ep.ss_tiles;
+                        float acc = 0.0f;
+                        for (int i0 = 0; i0 < ep.ss_tiles; i0 += 16) {
+                            float v16[16];
 #pragma unroll
-                    for (int t = 0; t < kChunk; ++t)
-                        xv[t] = t < W ? __ldcg(a.epi.out + static_cast<size_t>(t) * a.n_out + tile * kBlockM + tid) : 0.0f;
-                    if (a.epi.u_out != nullptr) gcol = a.epi.gain[tile * kBlockM + tid];
+                            for (int j = 0; j < 16; ++j) v16[j] = i0 + j < ep.ss_tiles ? __ldcg(ssr + i0 + j) : 0.0f;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (i0 + j < ep.ss_tiles) acc = __fadd_rn(acc, v16[j]);
+                        }
+                        s_fe.rn[tid] = 1.0f / sqrtf(__fadd_rn(__fdiv_rn(acc, static_cast<float>(ep.norm_d)), ep.eps));
+                    }
+                    if (ep.kind == kEpiQkvRope) {
+                        const int half = P.m.head_dim / 2;
+                        const int n0 = P.ps->n_cached;
+                        for (int idx = tid; idx < W * half; idx += kEpiThreads) {
+                            const int t = idx / half, i = idx % half;
+                            s_fe.cs[t][i] = ep.rope_cos[static_cast<size_t>(n0 + t) * half + i];
+                            s_fe.sn[t][i] = ep.rope_sin[static_cast<size_t>(n0 + t) * half + i];
+                        }
+                        if (tid < W) {
+                            const int pos = n0 + tid;
+                            s_fe.page[tid] = ep.page_table[pos / ep.page_size];
+                            s_fe.slot[tid] = pos % ep.page_size;
+                        }
+                    }
+                    epi_bar();
                 }
-                mbar_wait(&tfull[b], (u >> 1) & 1u);
-                if (tid == 0) pass_stamp(P, p, 4);  // debug: accumulator of the CTA's latest tile ready
-                __syncwarp();
-                tc_fence_after();
-                const uint32_t t_lane =
-                    tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * P.tmem_buf);
-                bool publish = false;
-                if (fast) {
-                    // tokens in chunks of 16 (W <= 32: two chunks), one TMEM load each
-                    const int nch = NCHUNK == 1 ? 1 : (W + kChunk - 1) / kChunk;
-                    // partial layout [segment][row][Wp] (Wp = W rounded up to 4): one
-                    // 16-byte store / load per 4 tokens
-                    const int Wp = (W + 3) & ~3;
-                    auto next_xv = [&](int t0) {  // residual rows of a later chunk
-                        if (!resid) return;
+                const int tile_lo = g0 / sb.nkb, tile_hi = (g1 - 1) / sb.nkb;
+                for (int tile = tile_lo; tile <= tile_hi; ++tile, ++u) {
+                    int nseg, seg;
+                    part.segments(tile, sb.nkb, sb.T, c, &nseg, &seg);
+                    const int gtile = sb.tile0 + tile;  // global output tile
+                    // the tile's reducer: segment 0 of its last k-group (every other
+                    // (k-group, segment) stores a partial); a lone segment of a
+                    // single k-group runs the epilogue directly
+                    const bool reducer = sb.last_k && seg == 0;
+                    const int n_part = kg * nseg;  // partials + the reducer's own accumulator
+                    const int b = u & (kAccBufs - 1);
+                    float xv[kChunk];
+                    float gcol = 1.0f;
+                    if (fast && resid && reducer) {  // residual rows of this tile, before the accumulator lands
 #pragma unroll
                         for (int t = 0; t < kChunk; ++t)
-                            xv[t] = t0 + t < W
-                                        ? __ldcg(a.epi.out + static_cast<size_t>(t0 + t) * a.n_out + tile * kBlockM + tid)
-                                        : 0.0f;
-                    };
-                    if (nseg == 1) {
+                            xv[t] = t < W ? __ldcg(a.epi.out + static_cast<size_t>(t) * a.n_out + gtile * kBlockM + tid) : 0.0f;
+                        if (a.epi.u_out != nullptr) gcol = a.epi.gain[gtile * kBlockM + tid];
+                    }
+                    mbar_wait(&tfull[b], (u / kAccBufs) & 1u);
+                    if (tid == 0) pass_stamp(P, p, 4);  // debug: accumulator of the CTA's latest tile ready
+                    __syncwarp();
+                    tc_fence_after();
+                    const uint32_t t_lane =
+                        tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * P.tmem_buf);
+                    bool publish = false;
+                    if (fast) {
+                        // tokens in chunks of 16 (W <= 32: two chunks), one TMEM load each
+                        const int nch = NCHUNK == 1 ? 1 : (W + kChunk - 1) / kChunk;
+                        // partial layout [tile][k-group][segment][row][Wp] (Wp = W rounded
+                        // up to 4): one 16-byte store / load per 4 tokens
+                        const int Wp = (W + 3) & ~3;
+                        const size_t slot_floats = static_cast<size_t>(Wp) * 128;
+                        float* tile_ws = a.ws + static_cast<size_t>(gtile) * kg * a.max_seg * slot_floats +
+                                         static_cast<size_t>(row) * Wp;
+                        auto next_xv = [&](int t0) {  // residual rows of a later chunk
+                            if (!resid) return;
+#pragma unroll
+                            for (int t = 0; t < kChunk; ++t)
+                                xv[t] = t0 + t < W
+                                            ? __ldcg(a.epi.out + static_cast<size_t>(t0 + t) * a.n_out + gtile * kBlockM + tid)
+                                            : 0.0f;
+                        };
+                        if (n_part == 1) {
 #pragma unroll 1
-                        for (int ch = 0; ch < nch; ++ch) {
+                            for (int ch = 0; ch < nch; ++ch) {
+                                float v[16];
+                                tmem_ld16(t_lane + ch * kChunk, v);
+                                if (ch == nch - 1) {
+                                    tc_fence_before();
+                                    mbar_arrive(&tempty[b]);
+                                }
+                                if (ch > 0) {
+                                    epi_bar();  // `red` of the previous chunk consumed
+                                    next_xv(ch * kChunk);
+                                }
+                                fast_tile_epilogue(a, s_fe, gtile, ch * kChunk, v, xv, gcol, red, tid);
+                            }
+                            publish = true;
+                        } else if (!reducer) {
+                            // The reducer (segment 0 of the last k-group: the tile's first
+                            // k-blocks of that group sit at the END of its CTA's range, so it
+                            // finishes last) waits for the others: they store their partial
+                            // and bump the tile counter with a fire-and-forget release; it
+                            // adds them in (k-group, segment) order to its own registers.
+                            float* part = tile_ws + static_cast<size_t>(sb.ki * a.max_seg + seg) * slot_floats;
+#pragma unroll 1
+                            for (int ch = 0; ch < nch; ++ch) {
+                                float v[16];
+                                tmem_ld16(t_lane + ch * kChunk, v);
+#pragma unroll
+                                for (int q4 = 0; q4 < 4; ++q4)
+                                    if (ch * kChunk + 4 * q4 < W)
+                                        reinterpret_cast<float4*>(part)[ch * 4 + q4] =
+                                            make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+                            }
+                            tc_fence_before();
+                            mbar_arrive(&tempty[b]);
+                            epi_bar();  // every partial store happens-before the release
+                            if (tid == 0) post_pub(kPubCount, 0, 0, &a.epi.counters[gtile * kCounterStride], p);
+                        } else {
+                            if (tid == 0) {
+                                while (!(P.nodep & 8) && ld_acquire(&a.epi.counters[gtile * kCounterStride]) < n_part - 1)
+                                    __nanosleep(32);
+                                a.epi.counters[gtile * kCounterStride] = 0;
+                                pass_stamp(P, p, 5);  // debug: reducer saw every partial
+                            }
+                            epi_bar();
+                            const int own = (kg - 1) * nseg;  // flat index of the reducer's own slot
+#pragma unroll 1
+                            for (int ch = 0; ch < nch; ++ch) {
+                                float acc[16];
+                                tmem_ld16(t_lane + ch * kChunk, acc);
+                                if (ch == nch - 1) {
+                                    tc_fence_before();
+                                    mbar_arrive(&tempty[b]);
+                                }
+                                for (int o0 = 0; o0 < n_part - 1; o0 += 4) {
+                                    float4 pv[4][4];
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k) {
+                                        const int f = o0 + k < own ? o0 + k : o0 + k + 1;  // flat (k-group, segment)
+                                        const int ki = f / nseg, si = f - ki * nseg;
+                                        const float4* src = reinterpret_cast<const float4*>(
+                                            tile_ws + static_cast<size_t>(ki * a.max_seg + si) * slot_floats);
+#pragma unroll
+                                        for (int q4 = 0; q4 < 4; ++q4)
+                                            pv[k][q4] = (o0 + k < n_part - 1 && ch * kChunk + 4 * q4 < W)
+                                                            ? __ldcg(src + ch * 4 + q4)
+                                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                                    }
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k)
+                                        if (o0 + k < n_part - 1)
+#pragma unroll
+                                            for (int q4 = 0; q4 < 4; ++q4) {
+                                                acc[4 * q4] = __fadd_rn(acc[4 * q4], pv[k][q4].x);
+                                                acc[4 * q4 + 1] = __fadd_rn(acc[4 * q4 + 1], pv[k][q4].y);
+                                                acc[4 * q4 + 2] = __fadd_rn(acc[4 * q4 + 2], pv[k][q4].z);
+                                                acc[4 * q4 + 3] = __fadd_rn(acc[4 * q4 + 3], pv[k][q4].w);
+                                            }
+                                }
+                                if (tid == 0) pass_stamp(P, p, 8);  // debug: partials summed
+                                if (ch > 0) {
+                                    epi_bar();
+                                    next_xv(ch * kChunk);
+                                }
+                                fast_tile_epilogue(a, s_fe, gtile, ch * kChunk, acc, xv, gcol, red, tid);
+                            }
+                            if (tid == 0) pass_stamp(P, p, 9);
+                            publish = true;
+                        }
+                    } else if (nseg == 1) {
+                        // (W > 32: the host builds these phases unsplit, kg = tg = 1)
+                        for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                            const int tn = min(kChunk, a.w - t0);
                             float v[16];
-                            tmem_ld16(t_lane + ch * kChunk, v);
-                            if (ch == nch - 1) {
+                            tmem_ld16(t_lane + t0, v);
+                            if (t0 + kChunk >= a.w) {
                                 tc_fence_before();
                                 mbar_arrive(&tempty[b]);
                             }
-                            if (ch > 0) {
-                                epi_bar();  // `red` of the previous chunk consumed
-                                next_xv(ch * kChunk);
-                            }
-                            fast_tile_epilogue(a, s_fe, tile, ch * kChunk, v, xv, gcol, red, tid);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (j < tn) red[j * 128 + row] = v[j];
+                            epi_bar();
+                            scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                            apply_epilogue(a, gtile, t0, tn, red, tid, s_part);
+                            epi_bar();
                         }
                         publish = true;
-                    } else if (seg != 0) {
-                        // Segment 0 (the tile's first k-blocks) sits at the END of its
-                        // CTA's range, so it finishes last: it is the designated reducer.
-                        // The others store their partial and bump the tile counter with a
-                        // fire-and-forget release; the reducer waits for them (normally
-                        // already done), adds them in segment order to its own registers.
-                        float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * Wp * 128 +
-                                      static_cast<size_t>(row) * Wp;
-#pragma unroll 1
-                        for (int ch = 0; ch < nch; ++ch) {
+                    } else {
+                        float* part = a.ws + (static_cast<size_t>(gtile) * a.max_seg + seg) * a.w * 128;
+                        for (int t0 = 0; t0 < a.w; t0 += 16) {
                             float v[16];
-                            tmem_ld16(t_lane + ch * kChunk, v);
+                            tmem_ld16(t_lane + t0, v);
 #pragma unroll
-                            for (int q4 = 0; q4 < 4; ++q4)
-                                if (ch * kChunk + 4 * q4 < W)
-                                    reinterpret_cast<float4*>(part)[ch * 4 + q4] =
-                                        make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+                            for (int j = 0; j < 16; ++j)
+                                if (t0 + j < a.w) part[static_cast<size_t>(t0 + j) * 128 + row] = v[j];
                         }
                         tc_fence_before();
                         mbar_arrive(&tempty[b]);
-                        epi_bar();  // every partial store happens-before the release
-                        if (tid == 0)
-                            asm volatile("red.release.gpu.global.add.s32 [%0], 1;"
-                                         ::"l"(&a.epi.counters[tile * kCounterStride]) : "memory");
-                    } else {
-                        if (tid == 0) {
-                            while (ld_acquire(&a.epi.counters[tile * kCounterStride]) < nseg - 1) __nanosleep(32);
-                            a.epi.counters[tile * kCounterStride] = 0;
-                            pass_stamp(P, p, 5);  // debug: reducer saw every partial
+                        epi_bar();
+                        if (tid == 0) {  // release this segment's partial, acquire the others'
+                            const int prev = atom_add_acq_rel(&a.epi.counters[gtile * kCounterStride], 1);
+                            s_last = (prev == nseg - 1);
                         }
                         epi_bar();
-                        const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * Wp * 128 +
-                                            static_cast<size_t>(row) * Wp;
-#pragma unroll 1
-                        for (int ch = 0; ch < nch; ++ch) {
-                            float acc[16];
-                            tmem_ld16(t_lane + ch * kChunk, acc);
-                            if (ch == nch - 1) {
-                                tc_fence_before();
-                                mbar_arrive(&tempty[b]);
-                            }
-                            for (int s0 = 1; s0 < nseg; s0 += 4) {
-                                float4 pv[4][4];
+                        if (s_last) {
+                            const float* base = a.ws + static_cast<size_t>(gtile) * a.max_seg * a.w * 128;
+                            const size_t seg_stride = static_cast<size_t>(a.w) * 128;
+                            for (int t0 = 0; t0 < a.w; t0 += kChunk) {
+                                const int tn = min(kChunk, a.w - t0);
+                                for (int itm = tid; itm < tn * 32; itm += kEpiThreads) {
+                                    const int t = itm >> 5, r4 = (itm & 31) * 4;
+                                    const float4* src = reinterpret_cast<const float4*>(
+                                        base + static_cast<size_t>(t0 + t) * 128 + r4);
+                                    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                                    for (int s0 = 0; s0 < nseg; s0 += 8) {
+                                        float4 vv[8];
 #pragma unroll
-                                for (int k = 0; k < 4; ++k)
+                                        for (int j = 0; j < 8; ++j)
+                                            if (s0 + j < nseg) vv[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
 #pragma unroll
-                                    for (int q4 = 0; q4 < 4; ++q4)
-                                        pv[k][q4] = (s0 + k < nseg && ch * kChunk + 4 * q4 < W)
-                                                        ? __ldcg(reinterpret_cast<const float4*>(
-                                                              base + static_cast<size_t>(s0 + k) * Wp * 128) + ch * 4 + q4)
-                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    if (s0 + k < nseg)
-#pragma unroll
-                                        for (int q4 = 0; q4 < 4; ++q4) {
-                                            acc[4 * q4] = __fadd_rn(acc[4 * q4], pv[k][q4].x);
-                                            acc[4 * q4 + 1] = __fadd_rn(acc[4 * q4 + 1], pv[k][q4].y);
-                                            acc[4 * q4 + 2] = __fadd_rn(acc[4 * q4 + 2], pv[k][q4].z);
-                                            acc[4 * q4 + 3] = __fadd_rn(acc[4 * q4 + 3], pv[k][q4].w);
-                                        }
-                            }
-                            if (tid == 0) pass_stamp(P, p, 8);  // debug: partials summed
-                            if (ch > 0) {
-                                epi_bar();
-                                next_xv(ch * kChunk);
-                            }
-                            fast_tile_epilogue(a, s_fe, tile, ch * kChunk, acc, xv, gcol, red, tid);
-                        }
-                        if (tid == 0) pass_stamp(P, p, 9);
-                        publish = true;
-                    }
-                } else if (nseg == 1) {
-                    for (int t0 = 0; t0 < a.w; t0 += kChunk) {
-                        const int tn = min(kChunk, a.w - t0);
-                        float v[16];
-                        tmem_ld16(t_lane + t0, v);
-                        if (t0 + kChunk >= a.w) {
-                            tc_fence_before();
-                            mbar_arrive(&tempty[b]);
-                        }
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (j < tn) red[j * 128 + row] = v[j];
-                        epi_bar();
-                        scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                        apply_epilogue(a, tile, t0, tn, red, tid, s_part);
-                        epi_bar();
-                    }
-                    publish = true;
-                } else {
-                    float* part = a.ws + (static_cast<size_t>(tile) * a.max_seg + seg) * a.w * 128;
-                    for (int t0 = 0; t0 < a.w; t0 += 16) {
-                        float v[16];
-                        tmem_ld16(t_lane + t0, v);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (t0 + j < a.w) part[static_cast<size_t>(t0 + j) * 128 + row] = v[j];
-                    }
-                    tc_fence_before();
-                    mbar_arrive(&tempty[b]);
-                    epi_bar();
-                    if (tid == 0) {  // release this segment's partial, acquire the others'
-                        const int prev = atom_add_acq_rel(&a.epi.counters[tile * kCounterStride], 1);
-                        s_last = (prev == nseg - 1);
-                    }
-                    epi_bar();
-                    if (s_last) {
-                        const float* base = a.ws + static_cast<size_t>(tile) * a.max_seg * a.w * 128;
-                        const size_t seg_stride = static_cast<size_t>(a.w) * 128;
-                        for (int t0 = 0; t0 < a.w; t0 += kChunk) {
-                            const int tn = min(kChunk, a.w - t0);
-                            for (int itm = tid; itm < tn * 32; itm += kEpiThreads) {
-                                const int t = itm >> 5, r4 = (itm & 31) * 4;
-                                const float4* src = reinterpret_cast<const float4*>(
-                                    base + static_cast<size_t>(t0 + t) * 128 + r4);
-                                float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                                for (int s0 = 0; s0 < nseg; s0 += 8) {
-                                    float4 vv[8];
-#pragma unroll
-                                    for (int j = 0; j < 8; ++j)
-                                        if (s0 + j < nseg) vv[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
-#pragma unroll
-                                    for (int j = 0; j < 8; ++j)
-                                        if (s0 + j < nseg) {
-                                            acc4.x = __fadd_rn(acc4.x, vv[j].x);
-                                            acc4.y = __fadd_rn(acc4.y, vv[j].y);
-                                            acc4.z = __fadd_rn(acc4.z, vv[j].z);
-                                            acc4.w = __fadd_rn(acc4.w, vv[j].w);
-                                        }
+                                        for (int j = 0; j < 8; ++j)
+                                            if (s0 + j < nseg) {
+                                                acc4.x = __fadd_rn(acc4.x, vv[j].x);
+                                                acc4.y = __fadd_rn(acc4.y, vv[j].y);
+                                                acc4.z = __fadd_rn(acc4.z, vv[j].z);
+                                                acc4.w = __fadd_rn(acc4.w, vv[j].w);
+                                            }
+                                    }
+                                    *reinterpret_cast<float4*>(red + t * 128 + r4) = acc4;
                                 }
-                                *reinterpret_cast<float4*>(red + t * 128 + r4) = acc4;
+                                epi_bar();
+                                scale_by_rnorm(a, t0, tn, red, tid, s_r);
+                                apply_epilogue(a, gtile, t0, tn, red, tid, s_part);
+                                epi_bar();
                             }
-                            epi_bar();
-                            scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                            apply_epilogue(a, tile, t0, tn, red, tid, s_part);
-                            epi_bar();
+                            if (tid == 0) a.epi.counters[gtile * kCounterStride] = 0;
+                            publish = true;
                         }
-                        if (tid == 0) a.epi.counters[tile * kCounterStride] = 0;
-                        publish = true;
                     }
-                }
-                if (publish) {
-                    epi_bar();  // every epilogue store happens-before the release
-                    if (tid == 0) {
-                        st_release_flag(P.flags, ph.out_flag, tile, epoch);
-                        pass_stamp(P, p, 6);
+                    if (publish) {
+                        epi_bar();  // every epilogue store happens-before the release
+                        if (tid == 0) post_pub(kPubFlag, ph.out_flag, gtile, nullptr, p);
                     }
                 }
             }
             epi_bar();  // s_args reuse by the next phase
             if (tid == 0) pass_stamp(P, p, 3);
         }
+        if (tid == 0) post_pub(kPubExit, 0, 0, nullptr, 0);
+    } else if (warp == 3 && DD_PUB_OFFLOAD) {
+        // ---------------- publisher ----------------
+        // gpu-scope releases on behalf of the epilogue, in its order: one
+        // acq_rel fence (cumulative over the epilogue's stores, which
+        // happen-before the slot's mbarrier arrive) and the relaxed update
+        if (lane == 0) {
+            for (uint32_t n = 0;; ++n) {
+                const int sl = static_cast<int>(n % kPubSlots);
+                mbar_wait(&pfull[sl], (n / kPubSlots) & 1u);
+                const PubAction act = s_pub[sl];
+                mbar_arrive(&pempty[sl]);
+                if (act.kind == kPubExit) break;
+                if (act.kind == kPubCount) {
+                    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(act.ptr) : "memory");
+                } else {
+                    st_release_flag(P.flags, act.base, act.idx, epoch);
+                    pass_stamp(P, act.phase, 6);
+                }
+            }
+        }
     }
     if (threadIdx.x == 0) PASS_DBG(7, -1);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
-        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * 2);
+        const uint32_t cols = static_cast<uint32_t>(P.tmem_buf * kAccBufs);
         if (cols <= 64) tmem_dealloc<64>(tmem);
         else if (cols <= 128) tmem_dealloc<128>(tmem);
         else if (cols <= 256) tmem_dealloc<256>(tmem);

@@ -27,7 +27,13 @@ struct PassPhase {
     int out_flag;  // flag base of this phase's outputs
     int layer;
     int qkv_flag;  // attention: flag base of the layer's QKV tiles
-    int pad_;
+    // GEMM sub-phases: the (tile, k-block) grid is cut into kg k-groups x tg
+    // tile groups, run in the order (k-group 0: tile groups 0..tg-1), (k-group
+    // 1: ...), each a stream-K over every CTA.  A tile group is complete after
+    // its last k-group, so outputs are published progressively (tile group 0
+    // first) and a consumer's k-group i needs only its producer's tile group i.
+    int kg;
+    int tg;
     const __nv_bfloat16* w;  // pre-tiled weights (GEMM)
     const int* begins;       // [149] stream-K range starts by rank (weighted), or nullptr
     GemmArgs a;              // GEMM shape + fused epilogue
@@ -41,6 +47,7 @@ struct PassParams {
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
     int attn_cpg;  // attention: kAttnChunk-key chunks per group before an item is split
+    int nodep;     // timing experiments only (wrong numerics): skip waits, bit 1 activation producer, 2 epilogue inputs, 4 attention inputs, 8 stream-K reducer
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 

@@ -243,6 +243,58 @@ int pass_max_seg(const dd_ctx* ctx, int tiles, int nkb) {
     return ms;
 }
 
+// Sub-phase grid (k-groups x tile groups) of each GEMM of the persistent pass
+// (PassPhase.kg / tg): DD_PASS_SPLIT="KGxTG,..." in the order qkv, o, gate/up,
+// down, head overrides the default.  A split must divide the tiles and
+// k-blocks and keep every tile within the partial-slot limit; otherwise, and
+// for passes wider than 32 tokens (the per-thread epilogue), 1x1.
+void pass_split(const dd_ctx* ctx, int id, int w, int* kg, int* tg) {
+    static int cfg[kNumGemm][2] = {{-1, -1}};
+    if (cfg[0][0] < 0) {
+        // gate/up publishes two tile groups and down consumes them as two
+        // k-groups, so most of down starts on the first half of the SwiGLU
+        // output (W=9: 3.157 -> 3.113 ms); every other split measured slower
+        // (more segments and polls per phase than it saves)
+        static const int def[kNumGemm][2] = {{1, 1}, {1, 1}, {1, 2}, {2, 1}, {1, 1}};
+        for (int i = 0; i < kNumGemm; ++i) {
+            cfg[i][0] = def[i][0];
+            cfg[i][1] = def[i][1];
+        }
+        if (const char* e = getenv("DD_PASS_SPLIT")) {
+            for (int i = 0; i < kNumGemm && *e; ++i) {
+                int a = 1, b = 1, nc = 0;
+                if (sscanf(e, "%dx%d%n", &a, &b, &nc) == 2) {
+                    cfg[i][0] = a;
+                    cfg[i][1] = b;
+                    e += nc;
+                }
+                if (*e == ',') ++e;
+            }
+        }
+    }
+    *kg = 1;
+    *tg = 1;
+    if (w > 32) return;
+    int n_out, k;
+    gemm_shape(ctx, id, &n_out, &k);
+    const int tiles = n_out / 128, nkb = k / 64, a = cfg[id][0], b = cfg[id][1];
+    if (a < 1 || b < 1 || tiles % b || nkb % a) return;
+    if (a * pass_max_seg(ctx, tiles / b, nkb / a) > 64) return;  // partial slots per tile
+    *kg = a;
+    *tg = b;
+}
+
+// partial-buffer floats of one GEMM's phase (every split it may run with)
+size_t pass_ws_floats(const dd_ctx* ctx, int id) {
+    int n_out, k;
+    gemm_shape(ctx, id, &n_out, &k);
+    size_t best = static_cast<size_t>(n_out / 128) * pass_max_seg(ctx, n_out / 128, k / 64);
+    int kg, tg;
+    pass_split(ctx, id, 1, &kg, &tg);
+    best = std::max(best, static_cast<size_t>(n_out / 128) * kg * pass_max_seg(ctx, n_out / 128 / tg, k / 64 / kg));
+    return best * kMaxPassTokens * 128;
+}
+
 int tmem_buf_for(int nt) {
     int buf = 32;
     while (buf < nt) buf <<= 1;
@@ -300,7 +352,8 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
         a.nt = nt;
         a.tiles = n_outr / 128;
         a.nkb = k / 64;
-        a.max_seg = pass_max_seg(ctx, a.tiles, a.nkb);
+        pass_split(ctx, id, w, &p.kg, &p.tg);
+        a.max_seg = pass_max_seg(ctx, a.tiles / p.tg, a.nkb / p.kg);
         a.tmem_buf = tmem_buf_for(nt);
         a.ws = ctx->pass_ws + (gidx & 1) * ctx->pass_ws_half;
         ep.counters = ctx->pass_counters + (gidx & 1) * 512 * kCounterStride;
@@ -356,7 +409,8 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
         std::vector<size_t> off(ph.size(), 0);
         for (size_t i = 0; i < ph.size(); ++i) {
             if (ph[i].type != kPhGemm) continue;
-            const unsigned T = static_cast<unsigned>(ph[i].a.tiles * ph[i].a.nkb);
+            // every sub-phase of a GEMM has the same shape: one partition
+            const unsigned T = static_cast<unsigned>((ph[i].a.tiles / ph[i].tg) * (ph[i].a.nkb / ph[i].kg));
             off[i] = hb.size();
             for (int r = 0; r <= kNumSMs; ++r)
                 hb.push_back(static_cast<int>(static_cast<unsigned long long>(pre[r]) * T / pre[kNumSMs]));
@@ -396,6 +450,8 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     // sequence (scripts/pass_ab.py with DD_ATTN_CPG)
     static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 12;
     p.attn_cpg = env_cpg;
+    static const int env_nodep = getenv("DD_PASS_NODEP") ? atoi(getenv("DD_PASS_NODEP")) : 0;
+    p.nodep = env_nodep;
     const int smem = pass_smem_bytes(m, p.nt, &p.stages);
     if (smem < 0) return ctx_fail(ctx, DD_E_ARG, "pass kernel shared memory plan failed");
     p.ps = ctx->d_ps;
@@ -792,12 +848,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         CK(cudaMalloc(&ctx->pass_flags, bytes));
         CK(cudaMemset(ctx->pass_flags, 0, bytes));
         size_t half = 0;
-        for (int id = 0; id < kNumGemm; ++id) {
-            int n_out, k;
-            gemm_shape(ctx, id, &n_out, &k);
-            half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(ctx, n_out / 128, k / 64) *
-                                      kMaxPassTokens * 128);
-        }
+        for (int id = 0; id < kNumGemm; ++id) half = std::max(half, pass_ws_floats(ctx, id));
         ctx->pass_ws_half = half;
         CK(cudaMalloc(&ctx->pass_ws, sizeof(float) * 2 * half));
         CK(cudaMalloc(&ctx->pass_counters, sizeof(int) * 2 * 512 * kCounterStride));
@@ -1606,12 +1657,7 @@ int dd_pass_balance(dd_ctx* ctx) {
     ctx->pass_begins.clear();
     ctx->pass_nphases.clear();
     size_t half = 0;
-    for (int id = 0; id < kNumGemm; ++id) {
-        int n_out, k;
-        gemm_shape(ctx, id, &n_out, &k);
-        half = std::max(half, static_cast<size_t>(n_out / 128) * pass_max_seg(ctx, n_out / 128, k / 64) *
-                                  kMaxPassTokens * 128);
-    }
+    for (int id = 0; id < kNumGemm; ++id) half = std::max(half, pass_ws_floats(ctx, id));
     if (half > ctx->pass_ws_half) {
         cudaFree(ctx->pass_ws);
         ctx->pass_ws_half = half;

@@ -29,7 +29,12 @@ for r in range(rounds):
             for kv in st.split():
                 k, v = kv.split("=", 1)
                 env[k] = v
-        p = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+        try:
+            p = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True,
+                               timeout=float(os.environ.get("AB_TIMEOUT", "150")))
+        except subprocess.TimeoutExpired:
+            print(f"[{st}] W={w} ctx={ctxs}: TIMEOUT", flush=True)
+            continue
         line = [l for l in p.stdout.splitlines() if l.startswith("RESULT")]
         print(f"[{st}] W={w} ctx={ctxs}:", line[0][7:] if line else ("FAILED " + p.stderr[-300:]),
               flush=True)
