@@ -70,6 +70,9 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #ifndef DD_PUB_OFFLOAD
 #define DD_PUB_OFFLOAD 1
 #endif
+#ifndef DD_PASS_SLOW_EPI
+#define DD_PASS_SLOW_EPI 0  // 1: keep the staged epilogue for W > 16 * NCHUNK (DD_PASS_MAXW > 32)
+#endif
 constexpr int kAccBufs = DD_ACC_BUFS;  // TMEM accumulators: the MMA runs up to kAccBufs tile segments ahead of the epilogue
 // Publish ring: the epilogue hands every gpu-scope release (stream-K partial
 // counters, tile flags) to warp 3, so its own threads never wait for the
@@ -745,7 +748,7 @@ struct Partition {
 // NCHUNK = 16-token chunks of the register-resident epilogue: 1 (W <= 16, the
 // decode widths of every budget up to 16) or 2 (17 <= W <= 32); separate
 // instantiations keep the common one free of the second chunk's registers.
-template <int NCHUNK>
+template <int NCHUNK, int HD>
 __global__ void __launch_bounds__(kPassThreads, 1)
     pass_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_o,
                 const __grid_constant__ CUtensorMap map_a, const __grid_constant__ PassParams P) {
@@ -767,7 +770,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const int S = P.stages, nt = P.nt;
     const uint32_t b_bytes = static_cast<uint32_t>(nt) * 128u;
     const uint32_t stage_bytes = kABytes + b_bytes;
-    const int hd = P.m.head_dim;
+    constexpr int hd = HD;  // one instantiation per head_dim: the kernel's code stays within the I-cache budget
     uint8_t* kv_smem = smem + S * stage_bytes;                          // attention K/V chunk
     float* red = reinterpret_cast<float*>(kv_smem + kAttnBufs * 2 * kAttnChunk * hd * 2);  // [kChunk][128]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
@@ -1034,10 +1037,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                     int grp = item % per_head, qt = 0;
                     for (int act = active_of(0); grp >= act; act = active_of(++qt)) grp -= act;
                     if (tid == 0) PASS_DBG(6, p * 100000 + item);
-                    if (hd == 128)
-                        attn_item<128>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid, p);
-                    else
-                        attn_item<64>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid, p);
+                    attn_item<HD>(P, ph, kv_smem, &s_last, head, qt, grp, epoch, tid, p);
                 }
                 if (tid == 0) pass_stamp(P, p, 3);
                 continue;
@@ -1048,7 +1048,10 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             if (tid == 0) s_args = ph.a;
             epi_bar();
             const GemmArgs& a = s_args;
-            const bool fast = W <= NCHUNK * kChunk;
+            // W <= NCHUNK * 16 always (the host routes wider passes to the
+            // per-launch path): the per-thread register epilogue; the staged
+            // per-launch-style epilogue below is compiled out
+            constexpr bool fast = DD_PASS_SLOW_EPI == 0;
             const bool resid = a.epi.kind == kEpiResidual;
             bool consts = false;  // phase-level constants loaded (at the CTA's first sub-phase of the last k-group, before its tiles land)
             for (int sp = 0; sp < nsp; ++sp) {
@@ -1379,14 +1382,17 @@ int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
 cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
                                const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
                                cudaStream_t s) {
-    static int attr_set[kMaxDevices][2] = {};  // per device: TP ranks of one process
+    static int attr_set[kMaxDevices][4] = {};  // per device: TP ranks of one process
     const int dev = current_device_slot();
     const int two = p.nt > kChunk ? 1 : 0;
-    if (attr_set[dev][two] < smem_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(two ? pass_kernel<2> : pass_kernel<1>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    const int v = two * 2 + (p.m.head_dim == 128 ? 1 : 0);
+    void (*const fns[4])(CUtensorMap, CUtensorMap, CUtensorMap, PassParams) = {
+        pass_kernel<1, 64>, pass_kernel<1, 128>, pass_kernel<2, 64>, pass_kernel<2, 128>};
+    if (p.nt > 2 * kChunk || (p.m.head_dim != 64 && p.m.head_dim != 128)) return cudaErrorInvalidValue;
+    if (attr_set[dev][v] < smem_bytes) {
+        cudaError_t e = cudaFuncSetAttribute(fns[v], cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
         if (e != cudaSuccess) return e;
-        attr_set[dev][two] = smem_bytes;
+        attr_set[dev][v] = smem_bytes;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kNumSMs, 1, 1);
@@ -1398,8 +1404,7 @@ cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return two ? cudaLaunchKernelEx(&cfg, pass_kernel<2>, map_h, map_o, map_a, p)
-               : cudaLaunchKernelEx(&cfg, pass_kernel<1>, map_h, map_o, map_a, p);
+    return cudaLaunchKernelEx(&cfg, fns[v], map_h, map_o, map_a, p);
 }
 
 }  // namespace dd

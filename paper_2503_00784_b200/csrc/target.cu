@@ -482,10 +482,10 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
 // compute-heavier and run as one launch per GEMM / attention, whose
 // 2-CTA-per-SM GEMM keeps more tiles in flight for the epilogue-heavy wide case.
 bool use_pass_kernel(const dd_ctx* ctx, int w) {
-    // DD_PASS_MAXW (A/B knob, <= 64): the register-resident epilogue serves up to
+    // DD_PASS_MAXW (A/B knob, <= 32): the register-resident epilogue serves up to
     // 32 tokens (two 16-token chunks); wider passes take the per-launch path
     static const int max_w =
-        getenv("DD_PASS_MAXW") ? std::min(64, atoi(getenv("DD_PASS_MAXW"))) : 32;
+        getenv("DD_PASS_MAXW") ? std::min(32, atoi(getenv("DD_PASS_MAXW"))) : 32;
     return ctx->use_pass_kernel && w <= max_w;
 }
 
