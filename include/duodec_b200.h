@@ -165,7 +165,7 @@ typedef struct dd_verify_out {
     int sps_accepted;        /* sps: accepted draft length                    */
     int next_token;          /* sps: resample or bonus; vanilla: sampled token*/
     int n_draws;             /* uniforms consumed                              */
-    int pad;
+    int pad;                 /* internal: completion sequence of the result   */
     uint64_t counter_out;    /* counter + n_draws                              */
 } dd_verify_out;
 

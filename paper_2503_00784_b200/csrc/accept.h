@@ -27,7 +27,8 @@ struct AcceptParams {
     double* row_sum;       // scratch [L+1]
     int* row_argmax;       // scratch [L+1]
     unsigned int* ticket;  // zero-initialised counter (reset by the kernel)
-    dd_verify_out* out;    // device or mapped-host result
+    dd_verify_out* out;    // mapped-host result: fields, system fence, then out->pad = seq
+    int seq;               // completion sequence the host polls for (nonzero)
 };
 
 cudaError_t launch_accept(const AcceptParams& p, cudaStream_t stream);

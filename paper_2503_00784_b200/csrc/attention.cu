@@ -651,3 +651,15 @@ int launch_attention(const PassState* ps, int w, const ModelDims& m, const float
 }
 
 }  // namespace dd
+
+namespace dd {
+void preload_attention_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_cluster_kernel<128, kRanks>);
+    cudaFuncGetAttributes(&a, attn_cluster_kernel<128, 1>);
+    cudaFuncGetAttributes(&a, attn_cluster_kernel<64, kRanks>);
+    cudaFuncGetAttributes(&a, attn_cluster_kernel<64, 1>);
+    cudaFuncGetAttributes(&a, attn_prefill_kernel<128>);
+    cudaFuncGetAttributes(&a, attn_prefill_kernel<64>);
+}
+}  // namespace dd

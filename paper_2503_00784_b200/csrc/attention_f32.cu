@@ -107,3 +107,10 @@ int launch_attention_f32(const PassState* ps, int w, const ModelDims& m, const f
 }
 
 }  // namespace dd
+
+namespace dd {
+void preload_attention_f32_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, attn_f32_kernel);
+}
+}  // namespace dd

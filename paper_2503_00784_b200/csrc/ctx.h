@@ -89,7 +89,9 @@ struct dd_ctx {
     int* row_argmax = nullptr;
     unsigned* ticket = nullptr;
     dd_verify_out* d_out = nullptr;
-    dd_verify_out* h_out = nullptr;
+    dd_verify_out* h_out = nullptr;      // mapped pinned: written by the acceptance kernel
+    dd_verify_out* h_out_dev = nullptr;  // its device alias
+    int verify_seq = 0;
     float* q_rows = nullptr;
     float* h_q_stage = nullptr;
     int q_rows_valid = 0;

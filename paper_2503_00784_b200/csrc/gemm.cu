@@ -459,3 +459,10 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
 }
 
 }  // namespace dd
+
+namespace dd {
+void preload_gemm_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, gemm_sk_kernel);
+}
+}  // namespace dd

@@ -100,7 +100,7 @@ cudaError_t launch_gemm(const __nv_bfloat16* w_tiled, const CUtensorMap* map_x, 
 
 // Prefill GEMM (gemm_wide.cu): tokens on M (<= 128, one TMEM lane each),
 // 256 weight rows on N; map_x128 has 128-row boxes.  n_out % 256 == 0.
-GemmPlan plan_gemm_wide(int n_out, int k);
+GemmPlan plan_gemm_wide(int n_out, int k, int sm_avail = 148 /* kNumSMs */);
 size_t gemm_wide_ws_floats(const GemmPlan& p);
 // debug seam: per-CTA stamps of every following wide launch at buf + launch * 8 * 148
 void gemm_wide_set_trace(unsigned long long* buf);

@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kWideThreads, 1)
 #endif
 }
 
-GemmPlan plan_gemm_wide(int n_out, int k) {
+GemmPlan plan_gemm_wide(int n_out, int k, int sm_avail) {
     GemmPlan p{};
     // 128-row tiles when 256-row tiles would leave fewer than 64 of them
     // 128-row weight tiles (measured: 256-row tiles, whose fewer and larger
@@ -512,6 +512,9 @@ GemmPlan plan_gemm_wide(int n_out, int k) {
     if (env_big == -1) big = p.tiles / ((p.tiles + kNumSMs - 1) / kNumSMs);  // whole tiles per CTA
     else if (env_big > 0) big = env_big;
     p.ctas = static_cast<int>(std::min<long>(p.tiles >= 64 ? big : env_small, T));
+    // the designated reducers wait for their segments: every CTA must be able to
+    // be resident at once (sm_avail < 148 when other work may hold SMs)
+    p.ctas = std::min(p.ctas, std::max(1, sm_avail));
     int ms = 1;
     for (int t = 0; t < p.tiles; ++t) {
         const int f = gemm_dev::sk_owner(static_cast<long>(t) * p.nkb, T, p.ctas);
@@ -782,4 +785,14 @@ cudaError_t launch_gemm_prefill(const __nv_bfloat16* w_tiled, const CUtensorMap*
     return cudaLaunchKernelEx(&cfg, gemm_prefill_kernel<128>, w_tiled, *map_x128, a);
 }
 
+}  // namespace dd
+
+namespace dd {
+void preload_gemm_wide_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, gemm_wide_kernel<128>);
+    cudaFuncGetAttributes(&a, gemm_wide_kernel<256>);
+    cudaFuncGetAttributes(&a, gemm_prefill_kernel<128>);
+    cudaFuncGetAttributes(&a, gemm_prefill_kernel<256>);
+}
 }  // namespace dd

@@ -217,3 +217,17 @@ void launch_kv_compact(__nv_bfloat16* kv_pool, float* kv_f32, const int32_t* pag
 }
 
 }  // namespace dd
+
+namespace dd {
+void preload_model_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, init_matrix_kernel);
+    cudaFuncGetAttributes(&a, init_matrix_il_kernel);
+    cudaFuncGetAttributes(&a, init_head_kernel);
+    cudaFuncGetAttributes(&a, fill_f32_kernel);
+    cudaFuncGetAttributes(&a, embed_norm_kernel);
+    cudaFuncGetAttributes(&a, rmsnorm_kernel);
+    cudaFuncGetAttributes(&a, kv_compact_kernel<float>);
+    cudaFuncGetAttributes(&a, kv_compact_kernel<__nv_bfloat16>);
+}
+}  // namespace dd

@@ -1408,3 +1408,13 @@ cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_
 }
 
 }  // namespace dd
+
+namespace dd {
+void preload_pass_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, pass_kernel<1, 64>);
+    cudaFuncGetAttributes(&a, pass_kernel<1, 128>);
+    cudaFuncGetAttributes(&a, pass_kernel<2, 64>);
+    cudaFuncGetAttributes(&a, pass_kernel<2, 128>);
+}
+}  // namespace dd

@@ -7,6 +7,9 @@
 // and n_cached, so dd_score must be given exactly the tokens that are not yet
 // cached ([last committed token] ++ tail).
 #include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstddef>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -23,6 +26,18 @@
 #include "pass.h"
 
 using namespace dd;
+
+namespace dd {
+// every kernel of each translation unit, loaded at context creation
+void preload_accept_kernels();
+void preload_attention_kernels();
+void preload_attention_f32_kernels();
+void preload_gemm_kernels();
+void preload_gemm_wide_kernels();
+void preload_model_kernels();
+void preload_tp_kernels();
+void preload_pass_kernels();
+}  // namespace dd
 
 thread_local std::string g_last_error;
 
@@ -710,6 +725,27 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     ctx->fp32acc = d.precision == DD_PREC_FP32ACC;
     ctx->sm_count = prop.multiProcessorCount;
     CK(cudaSetDevice(cuda_device));
+    {
+        // Load every kernel of the library now: with lazy module loading a
+        // kernel's first launch loads its module and synchronises the device,
+        // which deadlocks tensor-parallel ranks driven from one thread (a rank
+        // blocks in the load while its own queued reduction waits for a peer
+        // whose work is not yet issued).
+        static bool loaded[kMaxDevices] = {};
+        const int slot = current_device_slot();
+        if (!loaded[slot]) {
+            preload_accept_kernels();
+            preload_attention_kernels();
+            preload_attention_f32_kernels();
+            preload_gemm_kernels();
+            preload_gemm_wide_kernels();
+            preload_model_kernels();
+            preload_tp_kernels();
+            preload_pass_kernels();
+            CK(cudaGetLastError());
+            loaded[slot] = true;
+        }
+    }
     ctx->tp_rank = tp_rank;
     ctx->tp_size = tp_size;
     ctx->vocab = d.vocab;
@@ -883,7 +919,9 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
     CK(cudaMalloc(&ctx->ticket, sizeof(unsigned)));
     CK(cudaMemset(ctx->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&ctx->d_out, sizeof(dd_verify_out)));
-    CK(cudaHostAlloc(&ctx->h_out, sizeof(dd_verify_out), cudaHostAllocDefault));
+    CK(cudaHostAlloc(&ctx->h_out, sizeof(dd_verify_out), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_out_dev), ctx->h_out, 0));
+    std::memset(ctx->h_out, 0, sizeof(dd_verify_out));
     CK(cudaMalloc(&ctx->q_rows, sizeof(float) * kMaxPassTokens * ctx->vocab));
     CK(cudaMalloc(&ctx->d_tail, sizeof(int32_t) * kMaxPassTokens));
     CK(cudaMalloc(&ctx->d_compact_dst, sizeof(int32_t) * kMaxPassTokens));
@@ -1045,8 +1083,26 @@ int dd_tp_connect_local(dd_ctx* const* ctxs, int n) {
                 return ctx_fail(ctxs[i], DD_E_CUDA, cudaGetErrorString(e));
             }
         }
+    bool shared = true;
+    for (int i = 1; i < n; ++i) shared = shared && ctxs[i]->device == ctxs[0]->device;
     for (int i = 0; i < n; ++i) {
         for (int r = 0; r < n; ++r) tp_set_peer(ctxs[i], r, static_cast<char*>(ctxs[r]->tp_xbuf));
+        ctxs[i]->tp_peers.shared = shared ? 1 : 0;
+        if (shared) {
+            // Every rank's kernels share one GPU: a rank's TP wait kernels (at most
+            // 8 CTAs, above) spin while its peers' GEMMs run, so the tokens-on-M
+            // GEMMs, whose stream-K reducers wait for segments of their own grid,
+            // are planned on 16 fewer SMs; graphs captured before are dropped.
+            dd_ctx* ctx = ctxs[i];
+            for (int id = 0; id < kNumGemm; ++id) {
+                int n_out, k;
+                gemm_shape(ctx, id, &n_out, &k);
+                if (ctx->wide_plans[id].tiles > 0) ctx->wide_plans[id] = plan_gemm_wide(n_out, k, kNumSMs - 16);
+            }
+            CK(cudaStreamSynchronize(ctx->stream));
+            for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+            ctx->graphs.clear();
+        }
         ctxs[i]->tp_connected = true;
     }
     return DD_OK;
@@ -1169,18 +1225,34 @@ static int verify_common(dd_ctx* ctx, AcceptParams& p, const dd_verify_args* arg
     p.row_sum = ctx->row_sum;
     p.row_argmax = ctx->row_argmax;
     p.ticket = ctx->ticket;
-    p.out = ctx->d_out;
+    p.out = ctx->h_out_dev;
+    ctx->verify_seq = ctx->verify_seq == INT_MAX ? 1 : ctx->verify_seq + 1;
+    p.seq = ctx->verify_seq;
     if (!p.q_onehot && p.mode != DD_MODE_VANILLA && p.L > 0) {
         if (ctx->q_rows_valid < p.L) return ctx_fail(ctx, DD_E_STATE, "q rows not uploaded");
         CK(cudaStreamWaitEvent(ctx->stream, ctx->q_ready, 0));
     }
     CK(launch_accept(p, ctx->stream));
     ctx->launches += 1;
-    CK(cudaMemcpyAsync(ctx->h_out, ctx->d_out, sizeof(dd_verify_out), cudaMemcpyDeviceToHost,
-                       ctx->stream));
     ctx->d2h_bytes += sizeof(dd_verify_out);
-    CK(cudaStreamSynchronize(ctx->stream));
-    *out = *ctx->h_out;
+    // spin on the mapped result's sequence word (the kernel writes it after a
+    // system fence); every 1024 polls ask the stream whether it failed
+    volatile const int* seqw = &ctx->h_out->pad;
+    for (unsigned spins = 1; *seqw != p.seq; ++spins) {
+        if ((spins & 1023u) == 0) {
+            const cudaError_t e = cudaStreamQuery(ctx->stream);
+            if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+            if (e == cudaSuccess && *seqw != p.seq)
+                return ctx_fail(ctx, DD_E_CUDA, "acceptance result missing after the stream drained");
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const volatile int* src = reinterpret_cast<const volatile int*>(ctx->h_out);
+    int* dst = reinterpret_cast<int*>(out);
+    for (size_t i = 0; i < sizeof(dd_verify_out) / sizeof(int); ++i) dst[i] = src[i];
     return DD_OK;
 }
 

@@ -2,6 +2,8 @@
 // are latency-bound (a [W, d] fp32 partial per rank, W <= 128): one CTA per
 // 128-column tile of the residual stream, loads of every rank's partial issued
 // back to back, no shared-memory staging.
+#include <algorithm>
+
 #include "common.cuh"
 #include "tp.h"
 
@@ -70,9 +72,11 @@ __global__ void __launch_bounds__(128) tp_reduce_residual_kernel(
     tp_barrier(P, static_cast<unsigned>(ps->epoch) * static_cast<unsigned>(ops_per_pass) +
                       static_cast<unsigned>(op) + 1u);
     __shared__ float part[4];
-    const int tile = blockIdx.x, tid = threadIdx.x, col = tile * 128 + tid;
+    const int tid = threadIdx.x;
     const int tiles = d / 128;
     const size_t off = static_cast<size_t>(op & 1) * kMaxPassTokens * d;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int col = tile * 128 + tid;
     const float g = gain[col];
     for (int t = 0; t < w; ++t) {
         const size_t i = static_cast<size_t>(t) * d + col;
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(128) tp_reduce_residual_kernel(
             ss_out[static_cast<size_t>(t) * tiles + tile] =
                 __fadd_rn(__fadd_rn(part[0], part[1]), __fadd_rn(part[2], part[3]));
         __syncthreads();
+    }
     }
 }
 
@@ -120,13 +125,23 @@ __global__ void __launch_bounds__(256) tp_gather_logits_kernel(TpPeers P, const 
 void launch_tp_reduce_residual(const TpPeers& P, const PassState* ps, int op, int ops_per_pass,
                                int d, float* x, __nv_bfloat16* u, const float* gain,
                                float* ss_out, cudaStream_t s) {
-    tp_reduce_residual_kernel<<<d / 128, 128, 0, s>>>(P, ps, op, ops_per_pass, d, x, u, gain,
-                                                      ss_out);
+    // ranks sharing one device: few spinning CTAs, so a peer's GEMM (whose
+    // stream-K reducers need all of its CTAs resident) always finds its SMs
+    const int grid = P.shared ? std::min(d / 128, 4) : d / 128;
+    tp_reduce_residual_kernel<<<grid, 128, 0, s>>>(P, ps, op, ops_per_pass, d, x, u, gain, ss_out);
 }
 
 void launch_tp_gather_logits(const TpPeers& P, const PassState* ps, int op, int ops_per_pass,
                              int vocab, float* logits, cudaStream_t s) {
-    tp_gather_logits_kernel<<<kNumSMs, 256, 0, s>>>(P, ps, op, ops_per_pass, vocab, logits);
+    tp_gather_logits_kernel<<<P.shared ? 4 : kNumSMs, 256, 0, s>>>(P, ps, op, ops_per_pass, vocab, logits);
 }
 
+}  // namespace dd
+
+namespace dd {
+void preload_tp_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, tp_reduce_residual_kernel);
+    cudaFuncGetAttributes(&a, tp_gather_logits_kernel);
+}
 }  // namespace dd

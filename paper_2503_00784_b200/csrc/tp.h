@@ -37,6 +37,7 @@ struct TpPeers {
     int* flags[kMaxTp];   // rank r's [kMaxTp][kTpFlagStride] arrival flags
     int v0[kMaxTp + 1];   // vocabulary split (multiples of 128)
     int rank, size;
+    int shared;  // every rank on one device (test harness): the waiting kernels run on few CTAs
 };
 
 // exchange-buffer layout (identical on every rank)
