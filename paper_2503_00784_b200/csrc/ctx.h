@@ -40,6 +40,7 @@ struct dd_ctx {
     int vocab = 0;      // full vocabulary (tokens, logits, acceptance)
     // tensor parallelism (tp.h); tp_size 1 = unsharded
     int tp_rank = 0, tp_size = 1;
+    int pass_ctas = 148;  // persistent pass kernel grid (148 / N when N TP ranks share one GPU)
     std::vector<int> tp_v0;        // vocabulary split, [tp_size + 1]
     void* tp_xbuf = nullptr;       // symmetric exchange buffer (flags | partials | local logits)
     dd::TpLayout tp_lay{};

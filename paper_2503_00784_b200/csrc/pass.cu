@@ -124,6 +124,63 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Tensor parallelism inside the pass (tp.h): the reducer of row-parallel tile
+// `tile` (O or down, residual phase k of the pass) publishes its reduced fp32
+// values v[16] (thread = row, 16 tokens) in slot k % 4 of its exchange buffer,
+// signals every peer's flag line (system-scope release), waits for every
+// peer's signal of the same tile and phase, and replaces v by the sum over
+// ranks in rank order 0..N-1 (bit-identical on every rank, so the replicated
+// residual stays identical).  Slot reuse: a rank rewrites slot k % 4 at phase
+// k + 4 only after it saw every peer's phase k + 2 signal, which a peer sends
+// after its phase k + 1, i.e. after finishing its phase-k reads.  A peer that
+// never signals traps after 10 s.
+__device__ void tp_exchange(const PassParams& P, int k, int tile, float* v, int tid, int epoch) {
+    const TpPeers& T = P.tp;
+    const unsigned val = static_cast<unsigned>(epoch) * static_cast<unsigned>(2 * P.m.n_layers) +
+                         static_cast<unsigned>(k) + 1u;
+    const size_t off = (static_cast<size_t>((k & (kTpPassSlots - 1)) * kTpPassTiles + tile) * 128 + tid) * 16;
+    float4* mine = reinterpret_cast<float4*>(T.pxch[T.rank] + off);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) mine[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+    epi_bar();  // every row's store happens-before the release below
+    if (tid == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int r = 0; r < T.size; ++r)
+            if (r != T.rank)
+                asm volatile("st.relaxed.sys.global.b32 [%0], %1;" ::"l"(T.pflags[r] + (T.rank * kTpPassTiles + tile) * kTpFlagStride),
+                             "r"(val) : "memory");
+    }
+    if (tid < T.size && tid != T.rank) {
+        const int* f = T.pflags[T.rank] + (tid * kTpPassTiles + tile) * kTpFlagStride;
+        const unsigned long long t0 = gtimer();
+        for (;;) {
+            int got;
+            asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(got) : "l"(f) : "memory");
+            if (static_cast<int>(static_cast<unsigned>(got) - val) >= 0) break;
+            __nanosleep(64);
+            if (gtimer() - t0 > 10000000000ull) __trap();
+        }
+    }
+    epi_bar();  // every peer's tile happens-before the loads below
+    float tot[16];
+    for (int r = 0; r < T.size; ++r) {
+        float x[16];
+        if (r == T.rank) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = v[i];
+        } else {
+            const float* src = T.pxch[r] + off;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(x[i]) : "l"(src + i) : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tot[i] = r == 0 ? x[i] : __fadd_rn(tot[i], x[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = tot[i];
+}
+
 // ---------------------------------------------------------------- attention
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -1053,6 +1110,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             // per-launch-style epilogue below is compiled out
             constexpr bool fast = DD_PASS_SLOW_EPI == 0;
             const bool resid = a.epi.kind == kEpiResidual;
+            const int tp_k = 2 * ph.layer + (ph.x_src == kXSwiglu ? 1 : 0);  // residual phase index (TP)
             bool consts = false;  // phase-level constants loaded (at the CTA's first sub-phase of the last k-group, before its tiles land)
             for (int sp = 0; sp < nsp; ++sp) {
                 const SubPhase sb = sub_of(ph, sp);
@@ -1159,6 +1217,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                     epi_bar();  // `red` of the previous chunk consumed
                                     next_xv(ch * kChunk);
                                 }
+                                if (NCHUNK == 1 && resid && P.tp.size > 1) tp_exchange(P, tp_k, gtile, v, tid, epoch);
                                 fast_tile_epilogue(a, s_fe, gtile, ch * kChunk, v, xv, gcol, red, tid);
                             }
                             publish = true;
@@ -1230,6 +1289,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                     epi_bar();
                                     next_xv(ch * kChunk);
                                 }
+                                if (NCHUNK == 1 && resid && P.tp.size > 1) tp_exchange(P, tp_k, gtile, acc, tid, epoch);
                                 fast_tile_epilogue(a, s_fe, gtile, ch * kChunk, acc, xv, gcol, red, tid);
                             }
                             if (tid == 0) pass_stamp(P, p, 9);
@@ -1381,7 +1441,7 @@ int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
 
 cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
                                const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
-                               cudaStream_t s) {
+                               int nctas, cudaStream_t s) {
     static int attr_set[kMaxDevices][4] = {};  // per device: TP ranks of one process
     const int dev = current_device_slot();
     const int two = p.nt > kChunk ? 1 : 0;
@@ -1395,7 +1455,7 @@ cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_
         attr_set[dev][v] = smem_bytes;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kNumSMs, 1, 1);
+    cfg.gridDim = dim3(nctas, 1, 1);
     cfg.blockDim = dim3(kPassThreads, 1, 1);
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;

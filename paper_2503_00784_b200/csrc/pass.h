@@ -8,6 +8,7 @@
 
 #include "gemm.h"
 #include "model.h"
+#include "tp.h"
 
 namespace dd {
 
@@ -49,6 +50,7 @@ struct PassParams {
     int attn_cpg;  // attention: kAttnChunk-key chunks per group before an item is split
     int nodep;     // timing experiments only (wrong numerics): skip waits, bit 1 activation producer, 2 epilogue inputs, 4 attention inputs, 8 stream-K reducer
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
+    TpPeers tp;               // tensor parallelism (tp.size > 1): O / down tile exchange (W <= 16)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 
     const PassState* ps;
@@ -88,6 +90,6 @@ int pass_smem_bytes(const ModelDims& m, int nt, int* stages);
 
 cudaError_t launch_pass_kernel(const CUtensorMap& map_h, const CUtensorMap& map_o,
                                const CUtensorMap& map_a, const PassParams& p, int smem_bytes,
-                               cudaStream_t s);
+                               int nctas, cudaStream_t s);
 
 }  // namespace dd

@@ -251,7 +251,7 @@ struct HostPartition {
 };
 
 int pass_max_seg(const dd_ctx* ctx, int tiles, int nkb) {
-    const HostPartition hp{&ctx->sk_prefix_h, kNumSMs};
+    const HostPartition hp{&ctx->sk_prefix_h, ctx->pass_ctas};
     const int T = tiles * nkb;
     int ms = 1;
     for (int t = 0; t < tiles; ++t) ms = std::max(ms, hp.nseg(t, nkb, T));
@@ -412,7 +412,7 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
     if (want_logits) {
         GemmEpiParams el = e;
         el.kind = kEpiStore;
-        el.out = ctx->logits;
+        el.out = ctx->tp_size > 1 ? ctx->tp_peers.lg[ctx->tp_rank] : ctx->logits;
         gemm(kGHead, ctx->head, 0, kXNormed, h_flag, el, m.n_layers);
     }
     if (static_cast<size_t>(next_flag) > ctx->pass_flag_count)
@@ -487,7 +487,15 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.attn_cnt = ctx->attn_cnt;
     p.trace = trace;
     p.rank_of_smid = ctx->rank_of_smid_d;
-    CK(launch_pass_kernel(ctx->map_h, ctx->map_o, ctx->map_a, p, smem, ctx->stream));
+    p.tp = ctx->tp_peers;
+    p.tp.size = ctx->tp_size;
+    p.tp.rank = ctx->tp_rank;
+    CK(launch_pass_kernel(ctx->map_h, ctx->map_o, ctx->map_a, p, smem, ctx->pass_ctas, ctx->stream));
+    if (ctx->tp_size > 1 && want_logits) {  // vocabulary-parallel head: assemble full rows (op 2L of the pass)
+        const int tp_ops = 2 * m.n_layers + 1;
+        launch_tp_gather_logits(ctx->tp_peers, ctx->d_ps, tp_ops - 1, tp_ops, ctx->vocab, ctx->logits, ctx->stream);
+        CK(cudaGetLastError());
+    }
     return DD_OK;
 }
 
@@ -501,12 +509,18 @@ bool use_pass_kernel(const dd_ctx* ctx, int w) {
     // 32 tokens (two 16-token chunks); wider passes take the per-launch path
     static const int max_w =
         getenv("DD_PASS_MAXW") ? std::min(32, atoi(getenv("DD_PASS_MAXW"))) : 32;
+    if (ctx->tp_size > 1) {
+        // tensor parallel: the O / down reducers exchange their tiles in the
+        // epilogue (pass.cu tp_exchange), 16-token register chunks only
+        static const bool tp_pass = !(getenv("DD_TP_PASS") && getenv("DD_TP_PASS")[0] == '0');
+        return tp_pass && ctx->use_pass_kernel && ctx->tp_connected && w <= 16 && ctx->m.d / 128 <= kTpPassTiles;
+    }
     return ctx->use_pass_kernel && w <= max_w;
 }
 
 int enqueue_pass(dd_ctx* ctx, int w, bool want_logits, int* kernels) {
     if (use_pass_kernel(ctx, w)) {
-        if (kernels) *kernels = 1;
+        if (kernels) *kernels = 1 + (ctx->tp_size > 1 && want_logits ? 1 : 0);  // + TP logits gather
         return enqueue_pass_kernel(ctx, w, want_logits);
     }
     int n = 0;
@@ -874,8 +888,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         // (fp32-accumulate mode: split activations run on the per-launch GEMM; a
         // partitioned device with fewer SMs than the persistent grid cannot
         // co-schedule its 148 CTAs)
-        ctx->use_pass_kernel = !(env && env[0] == '0') && tp_size == 1 && !ctx->fp32acc &&
-                               ctx->sm_count >= kNumSMs;
+        ctx->use_pass_kernel = !(env && env[0] == '0') && !ctx->fp32acc && ctx->sm_count >= kNumSMs;
         // embed + per layer (qkv, attention, o, gate/up, down) + head
         const size_t per_layer = m.qkv_rows() / 128 + m.n_heads * 16 + m.d / 128 + 2 * m.ffn / 128 + m.d / 128;
         const size_t n_flags = m.d / 128 + per_layer * m.n_layers + m.vocab / 128;
@@ -1027,6 +1040,8 @@ static void tp_set_peer(dd_ctx* ctx, int r, char* base) {
     P.flags[r] = reinterpret_cast<int*>(base + ctx->tp_lay.flags_off);
     P.part[r] = reinterpret_cast<float*>(base + ctx->tp_lay.part_off);
     P.lg[r] = reinterpret_cast<float*>(base + ctx->tp_lay.lg_off);
+    P.pflags[r] = reinterpret_cast<int*>(base + ctx->tp_lay.pflag_off);
+    P.pxch[r] = reinterpret_cast<float*>(base + ctx->tp_lay.pxch_off);
 }
 
 int dd_tp_export(dd_ctx* ctx, void* ipc_handle) {
@@ -1089,6 +1104,11 @@ int dd_tp_connect_local(dd_ctx* const* ctxs, int n) {
         for (int r = 0; r < n; ++r) tp_set_peer(ctxs[i], r, static_cast<char*>(ctxs[r]->tp_xbuf));
         ctxs[i]->tp_peers.shared = shared ? 1 : 0;
         if (shared) {
+            // the ranks' persistent pass kernels must be resident together
+            ctxs[i]->pass_ctas = kNumSMs / n;
+            for (auto& kv : ctxs[i]->pass_phases) cudaFree(kv.second);
+            ctxs[i]->pass_phases.clear();
+            ctxs[i]->pass_nphases.clear();
             // Every rank's kernels share one GPU: a rank's TP wait kernels (at most
             // 8 CTAs, above) spin while its peers' GEMMs run, so the tokens-on-M
             // GEMMs, whose stream-K reducers wait for segments of their own grid,

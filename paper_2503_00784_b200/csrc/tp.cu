@@ -15,7 +15,10 @@ TpLayout tp_layout(int d, int max_local_vocab) {
     L.part_off = 4096;
     L.part_stride = static_cast<size_t>(kMaxPassTokens) * d;
     L.lg_off = L.part_off + sizeof(float) * 2 * L.part_stride;
-    L.bytes = L.lg_off + sizeof(float) * static_cast<size_t>(kMaxPassTokens) * max_local_vocab;
+    L.pflag_off = L.lg_off + sizeof(float) * static_cast<size_t>(kMaxPassTokens) * max_local_vocab;
+    L.pflag_off = (L.pflag_off + 4095) & ~static_cast<size_t>(4095);
+    L.pxch_off = L.pflag_off + sizeof(int) * static_cast<size_t>(kMaxTp) * kTpPassTiles * kTpFlagStride;
+    L.bytes = L.pxch_off + sizeof(float) * static_cast<size_t>(kTpPassSlots) * kTpPassTiles * 128 * 16;
     L.bytes = (L.bytes + 4095) & ~static_cast<size_t>(4095);
     return L;
 }

@@ -30,19 +30,27 @@ namespace dd {
 
 constexpr int kMaxTp = 8;
 constexpr int kTpFlagStride = 32;  // ints: one 128-byte line per source rank
+// Persistent pass kernel under TP (pass.cu tp_exchange): the O / down
+// reducers exchange their reduced fp32 tile [128 rows][16 tokens] with the
+// peers' reducers of the same tile, through 4 rotating slots per tile and one
+// flag line per (source rank, tile).
+constexpr int kTpPassTiles = 64;  // d_model <= 8192
+constexpr int kTpPassSlots = 4;
 
 struct TpPeers {
     float* part[kMaxTp];  // rank r's [2][kMaxPassTokens][d] fp32 partials
     float* lg[kMaxTp];    // rank r's [kMaxPassTokens][v0[r+1] - v0[r]] local logits
     int* flags[kMaxTp];   // rank r's [kMaxTp][kTpFlagStride] arrival flags
     int v0[kMaxTp + 1];   // vocabulary split (multiples of 128)
+    int* pflags[kMaxTp];  // rank r's [kMaxTp][kTpPassTiles][kTpFlagStride] pass-kernel tile flags
+    float* pxch[kMaxTp];  // rank r's [kTpPassSlots][kTpPassTiles][128][16] reduced tiles
     int rank, size;
     int shared;  // every rank on one device (test harness): the waiting kernels run on few CTAs
 };
 
 // exchange-buffer layout (identical on every rank)
 struct TpLayout {
-    size_t flags_off, part_off, lg_off, bytes;
+    size_t flags_off, part_off, lg_off, pflag_off, pxch_off, bytes;
     size_t part_stride;  // floats per partial buffer
 };
 TpLayout tp_layout(int d, int max_local_vocab);

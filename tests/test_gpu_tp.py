@@ -139,6 +139,25 @@ def test_tp_engine_duo_equals_vanilla(group):
     assert out["sps"] == out["vanilla"]
 
 
+def test_tp_decode_runs_on_pass_kernel(group):
+    """Decode passes of a TP group (W <= 16) run the persistent pass kernel with
+    the O / down tile exchange in its epilogue: per extra decode iteration the
+    engine launches, per rank, the pass kernel and the vocabulary gather, plus
+    the acceptance kernel - not one launch per GEMM / attention / reduction."""
+    from paper_2503_00784_b200 import EngineConfig, run_generation
+    ranks, _ = group
+    prompt = np.random.default_rng(9).integers(0, TP_SHAPE["vocab"], 24).tolist()
+    runs = {}
+    for n in (8, 16):
+        cfg = EngineConfig(mode="vanilla", budget=2, max_sequences=1, max_new_tokens=n, greedy=True)
+        res = run_generation(ranks, None, prompt, cfg)
+        runs[n] = (res.gpu_launches, len(res.iterations))
+    d_launch, d_iter = runs[16][0] - runs[8][0], runs[16][1] - runs[8][1]
+    n = len(ranks)
+    assert d_iter > 0 and d_launch <= 3 * n * d_iter, (runs, "launches per decode iteration")
+    assert d_launch >= 2 * n * d_iter, runs
+
+
 def test_tp_two_processes_ipc(tmp_path):
     """Two rank processes connected through CUDA IPC handles exchanged over
     gloo (the one-process-per-GPU deployment), here sharing one GPU."""
