@@ -70,6 +70,9 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #ifndef DD_PUB_OFFLOAD
 #define DD_PUB_OFFLOAD 1
 #endif
+#ifndef DD_ATTN_AHEAD
+#define DD_ATTN_AHEAD 4  // attention chunks staged ahead (4: every buffer before the loop, refilled after use; 3: one buffer kept free)
+#endif
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
 #endif
@@ -309,7 +312,8 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
             prefetch_l2(P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot), run * HD * 2);
         }
     }
-    while (issued < min(n_mine, kAttnBufs - 1) && (grp + issued * active + 1) * kAttnChunk <= n0) issue();
+    constexpr int kAhead = DD_ATTN_AHEAD;  // chunks in flight before the loop (the loop refills a consumed buffer)
+    while (issued < min(n_mine, kAhead) && (grp + issued * active + 1) * kAttnChunk <= n0) issue();
     // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
     if (tid < 3) {  // q, k and v tiles polled in parallel
         const int row = tid == 0 ? head * HD : tid == 1 ? qd + kvh * HD : qd + md.kv_dim() + kvh * HD;
@@ -317,7 +321,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     }
     epi_bar();
     if (tid == 0) pass_stamp(P, pidx, 1);  // debug: QKV flags seen
-    while (issued < min(n_mine, kAttnBufs - 1)) issue();  // in flight while Q is loaded
+    while (issued < min(n_mine, kAhead)) issue();  // in flight while Q is loaded
 
     const int pos_g = n0 + qt * 16 + g, pos_g8 = pos_g + 8;
     const bool v_g = qt * 16 + g < W, v_g8 = qt * 16 + g + 8 < W;
@@ -353,7 +357,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     for (int i = 0, chunk = grp; chunk < n_chunks; ++i, chunk += active) {
         const int kb = chunk * kAttnChunk;
         const int b = i % kAttnBufs;
-        if (issued < n_mine) issue();  // into the buffer chunk i - 1 released
+        if (kAhead < kAttnBufs && issued < n_mine) issue();  // into the buffer chunk i - 1 released
         // chunk i landed: at most (issued - 1 - i) younger groups pending
         switch (issued - 1 - i) {
             case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
@@ -447,6 +451,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
             }
         }
         epi_bar();  // buffer b is refilled by the stage issued in the next iteration
+        if (kAhead == kAttnBufs && issued < n_mine) issue();  // into buffer b, just consumed
     }
 #pragma unroll
     for (int off = 1; off <= 2; off <<= 1) {
