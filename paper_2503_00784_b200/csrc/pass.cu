@@ -71,7 +71,10 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #define DD_PUB_OFFLOAD 1
 #endif
 #ifndef DD_ATTN_AHEAD
-#define DD_ATTN_AHEAD 4  // attention chunks staged ahead (4: every buffer before the loop, refilled after use; 3: one buffer kept free)
+#define DD_ATTN_AHEAD 0  // attention chunks staged ahead (0: every buffer before the loop, each refilled after use; else that many, one buffer kept free)
+#endif
+#ifndef DD_PASS_STAGE_CAP
+#define DD_PASS_STAGE_CAP 9
 #endif
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
@@ -235,6 +238,7 @@ __device__ __forceinline__ int attn_groups(int n_chunks, int cpg) {
 template <int HD>
 __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_smem, int* s_bcast,
                           int head, int qt, int grp, int epoch, int tid, int pidx) {
+    constexpr int kAttnBufs = attn_bufs(HD);
     constexpr int NCH = HD / 32;
     constexpr int CHK = HD / 8;
     constexpr int DW = HD / 4;
@@ -312,7 +316,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
             prefetch_l2(P.kv_pool + kv_offset(md, P.page_size, page, ph.layer, 1, kvh, slot), run * HD * 2);
         }
     }
-    constexpr int kAhead = DD_ATTN_AHEAD;  // chunks in flight before the loop (the loop refills a consumed buffer)
+    constexpr int kAhead = DD_ATTN_AHEAD > 0 ? DD_ATTN_AHEAD : kAttnBufs;  // chunks staged before the loop
     while (issued < min(n_mine, kAhead) && (grp + issued * active + 1) * kAttnChunk <= n0) issue();
     // inputs: this head's q rows and its kv head's k and v rows of the QKV GEMM
     if (tid < 3) {  // q, k and v tiles polled in parallel
@@ -665,7 +669,8 @@ struct FastEpi {
 };
 // FastEpi lives in the attention K/V staging area (the epilogue warps run GEMM
 // epilogues and attention items one after the other, never both at once)
-static_assert(sizeof(FastEpi) <= kAttnBufs * 2 * kAttnChunk * 64 * 2, "FastEpi exceeds the K/V staging area");
+static_assert(sizeof(FastEpi) <= attn_bufs(64) * 2 * kAttnChunk * 64 * 2 &&
+                  sizeof(FastEpi) <= attn_bufs(128) * 2 * kAttnChunk * 128 * 2, "FastEpi exceeds the K/V staging area");
 
 // Tokens [t0, t0 + 16) of the pass (W <= 32 runs two chunks).
 __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, int tile, int t0, float* v,
@@ -846,7 +851,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     const uint32_t stage_bytes = kABytes + b_bytes;
     constexpr int hd = HD;  // one instantiation per head_dim: the kernel's code stays within the I-cache budget
     uint8_t* kv_smem = smem + S * stage_bytes;                          // attention K/V chunk
-    float* red = reinterpret_cast<float*>(kv_smem + kAttnBufs * 2 * kAttnChunk * hd * 2);  // [kChunk][128]
+    float* red = reinterpret_cast<float*>(kv_smem + attn_bufs(hd) * 2 * kAttnChunk * hd * 2);  // [kChunk][128]
     uint64_t* full = reinterpret_cast<uint64_t*>(red + kChunk * 128);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -1446,9 +1451,9 @@ size_t pass_attn_cnt_ints(const ModelDims& m) { return static_cast<size_t>(m.n_h
 
 int pass_smem_bytes(const ModelDims& m, int nt, int* stages) {
     const int stage_bytes = static_cast<int>(kABytes) + nt * 128;
-    const int fixed = 1024 /* align */ + kAttnBufs * 2 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
+    const int fixed = 1024 /* align */ + attn_bufs(m.head_dim) * 2 * kAttnChunk * m.head_dim * 2 + kChunk * 128 * 4 + 64 * 8 + 64;
     const int budget = 225 * 1024 - 2048 /* static shared */;
-    static const int cap = getenv("DD_PASS_STAGES") ? atoi(getenv("DD_PASS_STAGES")) : 8;
+    static const int cap = getenv("DD_PASS_STAGES") ? atoi(getenv("DD_PASS_STAGES")) : DD_PASS_STAGE_CAP;
     int s = (budget - fixed) / stage_bytes;
     s = s > cap ? cap : s;
     if (s < 2) return -1;

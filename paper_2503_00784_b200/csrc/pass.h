@@ -75,8 +75,14 @@ struct PassParams {
 
 constexpr int kPassThreads = 256;
 constexpr int kAttnChunk = 32;    // keys staged per attention step
-constexpr int kAttnBufs = 4;      // K/V chunk buffers (up to 3 chunks in flight)
-static_assert(kAttnBufs == 4, "attn_item's cp.async wait ladder assumes 4 buffers");
+#ifndef DD_ATTN_BUFS_128
+#define DD_ATTN_BUFS_128 3
+#endif
+// K/V chunk buffers of a decode attention item (all staged ahead, each refilled
+// after use).  head_dim 128 keeps 3 (16 KiB each): the smem they free buys the
+// weight ring a ninth stage (W=9: 3.006 -> 2.983 ms, 2K context -0.02 ms).
+__host__ __device__ constexpr int attn_bufs(int hd) { return hd == 128 ? DD_ATTN_BUFS_128 : 4; }
+static_assert(DD_ATTN_BUFS_128 >= 2 && DD_ATTN_BUFS_128 <= 4, "attn_item's cp.async wait ladder handles 2..4 buffers");
 constexpr int kAttnGroups = 4;    // chunk groups per (head, query tile)
 constexpr int kCounterStride = 32;  // ints: one 128-byte line per stream-K tile counter
 constexpr int kFlagStride = 32;   // ints: one 128-byte line per flag replica
