@@ -79,9 +79,6 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
 #endif
-#ifndef DD_PASS_SLOW_EPI
-#define DD_PASS_SLOW_EPI 0  // 1: keep the staged epilogue for W > 16 * NCHUNK (DD_PASS_MAXW > 32)
-#endif
 constexpr int kAccBufs = DD_ACC_BUFS;  // TMEM accumulators: the MMA runs up to kAccBufs tile segments ahead of the epilogue
 // Publish ring: the epilogue hands every gpu-scope release (stream-K partial
 // counters, tile flags) to warp 3, so its own threads never wait for the
@@ -861,7 +858,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + kPubSlots);
     __shared__ PubAction s_pub[kPubSlots];
     __shared__ int s_last;
-    __shared__ float s_r[kChunk];
     __shared__ float s_part[4 * 32];
     __shared__ GemmArgs s_args;
     FastEpi& s_fe = *reinterpret_cast<FastEpi*>(kv_smem);  // aliases the attention staging area
@@ -1128,9 +1124,8 @@ __global__ void __launch_bounds__(kPassThreads, 1)
             epi_bar();
             const GemmArgs& a = s_args;
             // W <= NCHUNK * 16 always (the host routes wider passes to the
-            // per-launch path): the per-thread register epilogue; the staged
-            // per-launch-style epilogue below is compiled out
-            constexpr bool fast = DD_PASS_SLOW_EPI == 0;
+            // per-launch path): one output row per thread, tokens in registers
+            constexpr bool fast = true;
             const bool resid = a.epi.kind == kEpiResidual;
             const int tp_k = 2 * ph.layer + (ph.x_src == kXSwiglu ? 1 : 0);  // residual phase index (TP)
             bool consts = false;  // phase-level constants loaded (at the CTA's first sub-phase of the last k-group, before its tiles land)
@@ -1315,76 +1310,6 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                 fast_tile_epilogue(a, s_fe, gtile, ch * kChunk, acc, xv, gcol, red, tid);
                             }
                             if (tid == 0) pass_stamp(P, p, 9);
-                            publish = true;
-                        }
-                    } else if (nseg == 1) {
-                        // (W > 32: the host builds these phases unsplit, kg = tg = 1)
-                        for (int t0 = 0; t0 < a.w; t0 += kChunk) {
-                            const int tn = min(kChunk, a.w - t0);
-                            float v[16];
-                            tmem_ld16(t_lane + t0, v);
-                            if (t0 + kChunk >= a.w) {
-                                tc_fence_before();
-                                mbar_arrive(&tempty[b]);
-                            }
-#pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (j < tn) red[j * 128 + row] = v[j];
-                            epi_bar();
-                            scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                            apply_epilogue(a, gtile, t0, tn, red, tid, s_part);
-                            epi_bar();
-                        }
-                        publish = true;
-                    } else {
-                        float* part = a.ws + (static_cast<size_t>(gtile) * a.max_seg + seg) * a.w * 128;
-                        for (int t0 = 0; t0 < a.w; t0 += 16) {
-                            float v[16];
-                            tmem_ld16(t_lane + t0, v);
-#pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                if (t0 + j < a.w) part[static_cast<size_t>(t0 + j) * 128 + row] = v[j];
-                        }
-                        tc_fence_before();
-                        mbar_arrive(&tempty[b]);
-                        epi_bar();
-                        if (tid == 0) {  // release this segment's partial, acquire the others'
-                            const int prev = atom_add_acq_rel(&a.epi.counters[gtile * kCounterStride], 1);
-                            s_last = (prev == nseg - 1);
-                        }
-                        epi_bar();
-                        if (s_last) {
-                            const float* base = a.ws + static_cast<size_t>(gtile) * a.max_seg * a.w * 128;
-                            const size_t seg_stride = static_cast<size_t>(a.w) * 128;
-                            for (int t0 = 0; t0 < a.w; t0 += kChunk) {
-                                const int tn = min(kChunk, a.w - t0);
-                                for (int itm = tid; itm < tn * 32; itm += kEpiThreads) {
-                                    const int t = itm >> 5, r4 = (itm & 31) * 4;
-                                    const float4* src = reinterpret_cast<const float4*>(
-                                        base + static_cast<size_t>(t0 + t) * 128 + r4);
-                                    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
-                                    for (int s0 = 0; s0 < nseg; s0 += 8) {
-                                        float4 vv[8];
-#pragma unroll
-                                        for (int j = 0; j < 8; ++j)
-                                            if (s0 + j < nseg) vv[j] = __ldcg(src + (s0 + j) * (seg_stride / 4));
-#pragma unroll
-                                        for (int j = 0; j < 8; ++j)
-                                            if (s0 + j < nseg) {
-                                                acc4.x = __fadd_rn(acc4.x, vv[j].x);
-                                                acc4.y = __fadd_rn(acc4.y, vv[j].y);
-                                                acc4.z = __fadd_rn(acc4.z, vv[j].z);
-                                                acc4.w = __fadd_rn(acc4.w, vv[j].w);
-                                            }
-                                    }
-                                    *reinterpret_cast<float4*>(red + t * 128 + r4) = acc4;
-                                }
-                                epi_bar();
-                                scale_by_rnorm(a, t0, tn, red, tid, s_r);
-                                apply_epilogue(a, gtile, t0, tn, red, tid, s_part);
-                                epi_bar();
-                            }
-                            if (tid == 0) a.epi.counters[gtile * kCounterStride] = 0;
                             publish = true;
                         }
                     }
