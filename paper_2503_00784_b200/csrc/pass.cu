@@ -225,10 +225,12 @@ __device__ __forceinline__ int v_chunk(int key, int ch) {
 // warp w accumulates O for its quarter of the head dims (mma.sync m16n8k16).
 // Groups merge through global partials; the last-arriving group combines them
 // in group order and publishes the (head, tile) flag.
-// Chunk groups of a (head, query tile) item: up to `cpg` chunks run in one
-// group before the item is split (each extra group costs a partial round trip
-// and the last arriver's combine).
-__device__ __forceinline__ int attn_groups(int n_chunks, int cpg) {
+// Chunk groups of a (head, query tile) item: an item of at most `single`
+// chunks runs as one group (each extra group costs a partial round trip and
+// the last arriver's combine); longer ones split into groups of `cpg` chunks,
+// at most kAttnGroups.
+__device__ __forceinline__ int attn_groups(int n_chunks, int cpg, int single) {
+    if (n_chunks <= single) return 1;
     return min(kAttnGroups, max(1, (n_chunks + cpg - 1) / cpg));
 }
 
@@ -246,7 +248,7 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
     const int t_hi = min(W, (qt + 1) * 16);
     const int kmax = n0 + t_hi - 1;
     const int n_chunks = kmax / kAttnChunk + 1;
-    const int active = attn_groups(n_chunks, P.attn_cpg);
+    const int active = attn_groups(n_chunks, P.attn_cpg, P.attn_single);
     const int warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, c = lane & 3;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
@@ -1102,7 +1104,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 // order), CTA c taking items c, c + nctas, ...
                 const int n0 = P.ps->n_cached;
                 auto active_of = [&](int qt) {
-                    return attn_groups((n0 + min(W, (qt + 1) * 16) - 1) / kAttnChunk + 1, P.attn_cpg);
+                    return attn_groups((n0 + min(W, (qt + 1) * 16) - 1) / kAttnChunk + 1, P.attn_cpg, P.attn_single);
                 };
                 int per_head = 0;
                 for (int qt = 0; qt < qtiles; ++qt) per_head += active_of(qt);

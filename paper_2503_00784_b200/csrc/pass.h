@@ -47,7 +47,8 @@ struct PassParams {
     int nt;
     int tmem_buf;
     int prefetch;  // L2 prefetch distance (k-blocks) beyond the shared-memory ring
-    int attn_cpg;  // attention: kAttnChunk-key chunks per group before an item is split
+    int attn_cpg;     // attention: kAttnChunk-key chunks per group of a split item
+    int attn_single;  // attention: items of at most this many chunks are not split
     int nodep;     // timing experiments only (wrong numerics): skip waits, bit 1 activation producer, 2 epilogue inputs, 4 attention inputs, 8 stream-K reducer
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
     TpPeers tp;               // tensor parallelism (tp.size > 1): O / down tile exchange (W <= 16)

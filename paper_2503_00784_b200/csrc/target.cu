@@ -460,11 +460,14 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.tmem_buf = tmem_buf_for(p.nt);
     static const int env_pf = getenv("DD_PASS_PREFETCH") ? atoi(getenv("DD_PASS_PREFETCH")) : 4;
     p.prefetch = env_pf;
-    // up to 12 chunks (384 keys) per attention group: below that the groups'
-    // partial round trip and combine cost more than running the chunks in
-    // sequence (scripts/pass_ab.py with DD_ATTN_CPG)
-    static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 12;
+    // attention items of up to 10 chunks (320 keys) run unsplit (the groups'
+    // partial round trip and combine cost more than running them in sequence);
+    // longer ones split into groups of 4 chunks, at most 4 groups (W=9: 512
+    // keys 3.28 -> 3.23 ms, 1024 keys 3.42 -> 3.37 ms)
+    static const int env_cpg = getenv("DD_ATTN_CPG") ? atoi(getenv("DD_ATTN_CPG")) : 4;
+    static const int env_single = getenv("DD_ATTN_SINGLE") ? atoi(getenv("DD_ATTN_SINGLE")) : 10;
     p.attn_cpg = env_cpg;
+    p.attn_single = env_single;
     static const int env_nodep = getenv("DD_PASS_NODEP") ? atoi(getenv("DD_PASS_NODEP")) : 0;
     p.nodep = env_nodep;
     const int smem = pass_smem_bytes(m, p.nt, &p.stages);
