@@ -808,9 +808,11 @@ int CpuLlama::distribution(const float* lg, double temperature, bool greedy, flo
             bv = bestv[t];
             bi = besti[t];
         }
-    if (greedy) {
-        std::memset(q, 0, sizeof(float) * V_);
-        q[bi] = 1.0f;
+    if (greedy) {  // one-hot at the argmax (q == nullptr: argmax only)
+        if (q != nullptr) {
+            std::memset(q, 0, sizeof(float) * V_);
+            q[bi] = 1.0f;
+        }
         return bi;
     }
     const double inv_t = 1.0 / temperature;

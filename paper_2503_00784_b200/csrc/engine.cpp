@@ -115,8 +115,10 @@ Bundle draft_dynamic(DraftModel& dm, const std::vector<int32_t>& context, int bu
     const auto t0 = Clock::now();
     const int V = dm.V;
     Bundle b;
-    std::vector<float> first(V), probe(V);
-    const int top = dm.dist(context, first.data());
+    // greedy: the distributions are one-hot at the argmax, so only the argmax is
+    // computed (no V-wide q rows to fill: p_top = probe[a2] = 1)
+    std::vector<float> first(dm.greedy ? 0 : V), probe(dm.greedy ? 0 : V);
+    const int top = dm.dist(context, dm.greedy ? nullptr : first.data());
     const int s_cap = std::min(max_sequences, budget);
     std::vector<int32_t> ranks(std::min(V, s_cap + 1));
     if (dm.greedy) {
@@ -124,11 +126,11 @@ Bundle draft_dynamic(DraftModel& dm, const std::vector<int32_t>& context, int bu
     } else {
         dm.m->top_k(first.data(), static_cast<int>(ranks.size()), ranks.data());
     }
-    const double p_top = first[top];
+    const double p_top = dm.greedy ? 1.0 : first[top];
     std::vector<int32_t> pctx = context;
     pctx.push_back(top);
-    const int a2 = dm.dist(pctx, probe.data());
-    b.threshold = p_top * static_cast<double>(probe[a2]);
+    const int a2 = dm.dist(pctx, dm.greedy ? nullptr : probe.data());
+    b.threshold = p_top * (dm.greedy ? 1.0 : static_cast<double>(probe[a2]));
     b.forwards = 2;
     std::vector<int32_t> firsts{top};
     if (!dm.greedy) {
@@ -139,7 +141,7 @@ Bundle draft_dynamic(DraftModel& dm, const std::vector<int32_t>& context, int bu
     }
     const int s = static_cast<int>(firsts.size());
     const int base = budget / s, rem = budget - base * s;
-    std::vector<float> d(V);
+    std::vector<float> d(dm.greedy ? 0 : V);
     for (int i = 0; i < s; ++i) {
         const int len = base + (i == 0 ? rem : 0);
         DraftSeq seq;
@@ -155,7 +157,7 @@ Bundle draft_dynamic(DraftModel& dm, const std::vector<int32_t>& context, int bu
                 am = a2;
                 dp = probe.data();
             } else {
-                am = dm.dist(ctx, d.data());
+                am = dm.dist(ctx, dm.greedy ? nullptr : d.data());
                 ++b.forwards;
                 dp = d.data();
             }
