@@ -391,7 +391,8 @@ float rmsnorm_bf(const float* x, int d, float eps, uint16_t* h) {
 }  // namespace
 
 // ------------------------------------------------------------------ pool
-SpinPool::SpinPool(int n_threads, const std::vector<int>& cpus) : n_(std::max(1, n_threads)) {
+SpinPool::SpinPool(int n_threads, const std::vector<int>& cpus)
+    : n_(std::max(1, n_threads)), done_(new Done[std::max(1, n_threads)]) {
     // workers 1..n-1 are pinned to cpus[1..]; the calling thread (tid 0, the
     // engine's draft worker) pins itself to cpus[0]
     for (int i = 1; i < n_; ++i) {
@@ -430,7 +431,7 @@ void SpinPool::worker(int tid) {
         seen = gen_.load(std::memory_order_acquire);
         if (stop_.load(std::memory_order_acquire)) return;
         (*job_)(tid, n_);
-        done_.fetch_add(1, std::memory_order_acq_rel);
+        done_[tid].gen.store(seen, std::memory_order_release);
     }
 }
 
@@ -440,11 +441,11 @@ void SpinPool::run(const std::function<void(int, int)>& fn) {
         return;
     }
     job_ = &fn;
-    done_.store(0, std::memory_order_relaxed);
-    gen_.fetch_add(1, std::memory_order_acq_rel);
+    const uint64_t g = gen_.fetch_add(1, std::memory_order_acq_rel) + 1;
     if (sleepers_.load(std::memory_order_acquire) > 0) gen_.notify_all();
     fn(0, n_);
-    while (done_.load(std::memory_order_acquire) != n_ - 1) _mm_pause();
+    for (int t = 1; t < n_; ++t)
+        while (done_[t].gen.load(std::memory_order_acquire) != g) _mm_pause();
 }
 
 // ------------------------------------------------------------------ model

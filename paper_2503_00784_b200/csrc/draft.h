@@ -7,6 +7,7 @@
 #include <functional>
 #include <string>
 #include <thread>
+#include <memory>
 #include <vector>
 
 #include "../../include/duodec_b200.h"
@@ -27,7 +28,13 @@ class SpinPool {
     int n_;
     std::vector<std::thread> th_;
     std::atomic<uint64_t> gen_{0};
-    std::atomic<int> done_{0};
+    // per-worker completion word (the job generation it finished), one cache
+    // line each: the caller polls them instead of every worker incrementing
+    // one contended counter
+    struct alignas(64) Done {
+        std::atomic<uint64_t> gen{0};
+    };
+    std::unique_ptr<Done[]> done_;
     std::atomic<int> sleepers_{0};
     std::atomic<bool> stop_{false};
     const std::function<void(int, int)>* job_ = nullptr;
