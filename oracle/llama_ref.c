@@ -348,8 +348,11 @@ void orc_llama_set_quant(orc_llama* m, int on) {
         orc_layer* Ly = &m->layers[l];
         Ly->qqkv = quantize_rows(Ly->qkv, qd + 2 * kvd, m->d);
         Ly->qo = quantize_rows(Ly->o, m->d, qd);
-        Ly->qgu = quantize_rows(Ly->gu, 2 * m->F, m->d);
-        Ly->qdn = quantize_rows(Ly->dn, m->d, m->F);
+        /* the draft's gate/up and down are 4-bit (draft.cpp) unless DD_DRAFT_FFN_BITS=8 */
+        const char* fb = getenv("DD_DRAFT_FFN_BITS");
+        const int f4 = !(fb && atoi(fb) == 8) && m->d % 128 == 0 && m->F % 128 == 0;
+        Ly->qgu = quantize_rows_levels(Ly->gu, 2 * m->F, m->d, f4 ? 7 : 127);
+        Ly->qdn = quantize_rows_levels(Ly->dn, m->d, m->F, f4 ? 7 : 127);
     }
     /* the draft's LM head is 4-bit (draft.cpp quantize4) when d is a multiple of 128 */
     const char* hb = getenv("DD_DRAFT_HEAD_BITS");

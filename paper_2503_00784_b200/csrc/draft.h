@@ -68,6 +68,8 @@ struct Q4Mat {
 
 struct DraftLayer {
     QMat qkv, o, gu, dn;  // row-major [out][in]
+    Q4Mat gu4, dn4;       // nibble copies of gu / dn (DD_DRAFT_FFN_BITS=4)
+    bool w4 = false;
 };
 
 // Llama forward on host cores with a KV cache that follows the draft
