@@ -346,8 +346,10 @@ void orc_llama_set_quant(orc_llama* m, int on) {
     const int qd = m->H * m->hd, kvd = m->Hkv * m->hd;
     for (int l = 0; l < m->L; ++l) {
         orc_layer* Ly = &m->layers[l];
-        Ly->qqkv = quantize_rows(Ly->qkv, qd + 2 * kvd, m->d);
-        Ly->qo = quantize_rows(Ly->o, m->d, qd);
+        const char* ab = getenv("DD_DRAFT_ATTN_BITS");
+        const int a4 = ab && atoi(ab) == 4 && m->d % 128 == 0 && qd % 128 == 0;
+        Ly->qqkv = quantize_rows_levels(Ly->qkv, qd + 2 * kvd, m->d, a4 ? 7 : 127);
+        Ly->qo = quantize_rows_levels(Ly->o, m->d, qd, a4 ? 7 : 127);
         /* the draft's gate/up and down are 4-bit (draft.cpp) unless DD_DRAFT_FFN_BITS=8 */
         const char* fb = getenv("DD_DRAFT_FFN_BITS");
         const int f4 = !(fb && atoi(fb) == 8) && m->d % 128 == 0 && m->F % 128 == 0;

@@ -519,8 +519,15 @@ CpuLlama::CpuLlama(const dd_model_desc& d, uint64_t weight_seed, const dd_plant_
         gen(*pool_, gu, 0, F_ * D, derive(weight_seed, tensor_id(l, 4)), amp_proj);
         gen(*pool_, gu, F_ * D, F_ * D, derive(weight_seed, tensor_id(l, 5)), amp_proj);
         gen(*pool_, dn, 0, D * F_, derive(weight_seed, tensor_id(l, 6)), amp_out);
-        Ly.qkv = quantize(qkv, qd + 2 * kvd, d_, *pool_);
-        Ly.o = quantize(o, d_, qd, *pool_);
+        // DD_DRAFT_ATTN_BITS=4: QKV and O 4-bit as well (same scheme as the FFN below)
+        static const bool attn4 = getenv("DD_DRAFT_ATTN_BITS") && atoi(getenv("DD_DRAFT_ATTN_BITS")) == 4;
+        Ly.a4 = attn4 && d_ % 128 == 0 && qd % 128 == 0;
+        Ly.qkv = quantize(qkv, qd + 2 * kvd, d_, *pool_, Ly.a4 ? 7 : 127);
+        Ly.o = quantize(o, d_, qd, *pool_, Ly.a4 ? 7 : 127);
+        if (Ly.a4) {
+            Ly.qkv4 = pack4(Ly.qkv, *pool_);
+            Ly.o4 = pack4(Ly.o, *pool_);
+        }
         // gate/up and down quantised to 7 levels (4-bit) and streamed as nibbles by
         // decode - 2/3 of the layer bytes, so a drafted token reads 24 instead of 31 MB
         // (c 16.1 -> 20.8 on the B200 host, tokens per iteration unchanged, config 2
@@ -759,7 +766,8 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd_)));
     for (int l = 0; l < L_; ++l) {
         const DraftLayer& Ly = layers_[l];
-        matmul(*pool_, Ly.qkv, hb_.data(), w, qkv_.data(), xq_, xs_);
+        if (Ly.a4 && w == 1) matmul4(*pool_, Ly.qkv4, hb_.data(), qkv_.data(), xq_, xs_);
+        else matmul(*pool_, Ly.qkv, hb_.data(), w, qkv_.data(), xq_, xs_);
         per_token([&](int t) {
             float* r = &qkv_[static_cast<size_t>(t) * rows];
             for (int i = 0; i < rows; ++i) r[i] *= rn[t];
@@ -794,7 +802,8 @@ void CpuLlama::forward(const int32_t* toks, int w, float* logits_last) {
                            max_seq_, scale, sc, &ob_[t * qd + head * hd_]);
             }
         });
-        matmul(*pool_, Ly.o, ob_.data(), w, y_.data(), xq_, xs_);
+        if (Ly.a4 && w == 1) matmul4(*pool_, Ly.o4, ob_.data(), y_.data(), xq_, xs_);
+        else matmul(*pool_, Ly.o, ob_.data(), w, y_.data(), xq_, xs_);
         per_token([&](int t) {
             for (int i = 0; i < d_; ++i) x_[t * d_ + i] += y_[t * d_ + i];
             rn[t] = rmsnorm_bf(&x_[t * d_], d_, eps_, &hb_[t * d_]);

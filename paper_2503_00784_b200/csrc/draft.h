@@ -70,6 +70,8 @@ struct DraftLayer {
     QMat qkv, o, gu, dn;  // row-major [out][in]
     Q4Mat gu4, dn4;       // nibble copies of gu / dn (DD_DRAFT_FFN_BITS=4)
     bool w4 = false;
+    Q4Mat qkv4, o4;       // nibble copies of qkv / o (DD_DRAFT_ATTN_BITS=4)
+    bool a4 = false;
 };
 
 // Llama forward on host cores with a KV cache that follows the draft
