@@ -76,6 +76,9 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #ifndef DD_PASS_STAGE_CAP
 #define DD_PASS_STAGE_CAP 9
 #endif
+#ifndef DD_ATTN_ONEBAR
+#define DD_ATTN_ONEBAR 1  // attention chunk loop: one CTA barrier per chunk (refill after the next chunk's barrier)
+#endif
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
 #endif
@@ -369,6 +372,11 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
             default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
         }
         epi_bar();
+#if DD_ATTN_ONEBAR
+        // every warp is past iteration i - 1: its buffer takes the next chunk
+        // (one CTA barrier per chunk instead of two)
+        if (kAhead == kAttnBufs && i > 0 && issued < n_mine) issue();
+#endif
         if (tid == 0 && i == 0) pass_stamp(P, pidx, 2);  // debug: first chunk staged
         __nv_bfloat16(*ks)[HD] = ks_of(b);
         __nv_bfloat16(*vs)[HD] = vs_of(b);
@@ -453,9 +461,14 @@ __device__ void attn_item(const PassParams& P, const PassPhase& ph, uint8_t* kv_
                 mma_bf16(acc[e], pa[kst], b0, b1);
             }
         }
+#if !DD_ATTN_ONEBAR
         epi_bar();  // buffer b is refilled by the stage issued in the next iteration
         if (kAhead == kAttnBufs && issued < n_mine) issue();  // into buffer b, just consumed
+#endif
     }
+#if DD_ATTN_ONEBAR
+    epi_bar();  // every warp done with the staging buffers (the next item restages them)
+#endif
 #pragma unroll
     for (int off = 1; off <= 2; off <<= 1) {
         l_g += __shfl_xor_sync(0xffffffffu, l_g, off);
