@@ -107,6 +107,8 @@ struct dd_ctx {
     size_t pass_flag_count = 0;
     int* sk_prefix_d = nullptr;      // weighted stream-K partition by SM rank (or null)
     int* rank_of_smid_d = nullptr;
+    int* attn_rank_d = nullptr;  // [pass_ctas] attention item order (pass.cu), rebuilt with the phase tables
+    int attn_rank_ctas = 0;
     std::vector<int> sk_prefix_h;
     std::vector<int*> pass_begins;   // device begin tables of the phase tables
     float* pass_ws = nullptr;        // 2 x stream-K partials (alternating GEMM phases)

@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                 int per_head = 0;
                 for (int qt = 0; qt < qtiles; ++qt) per_head += active_of(qt);
                 const int items = P.m.n_heads * per_head;
-                for (int item = c; item < items; item += nctas) {
+                for (int item = P.attn_rank ? P.attn_rank[c] : c; item < items; item += nctas) {
                     const int head = item / per_head;
                     int grp = item % per_head, qt = 0;
                     for (int act = active_of(0); grp >= act; act = active_of(++qt)) grp -= act;

@@ -51,6 +51,7 @@ struct PassParams {
     int attn_single;  // attention: items of at most this many chunks are not split
     int nodep;     // timing experiments only (wrong numerics): skip waits, bit 1 activation producer, 2 epilogue inputs, 4 attention inputs, 8 stream-K reducer
     const int* rank_of_smid;  // [1024] partition rank of each SM, or nullptr (rank = blockIdx)
+    const int* attn_rank;     // [nctas] position of each partition rank in the attention item order, or nullptr
     TpPeers tp;               // tensor parallelism (tp.size > 1): O / down tile exchange (W <= 16)
     unsigned long long* trace;  // debug: [CTA][phase][12] globaltimer stamps, or nullptr
 

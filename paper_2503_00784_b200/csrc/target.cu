@@ -437,6 +437,32 @@ int build_pass_phases(dd_ctx* ctx, int w, bool want_logits, const PassPhase** ou
         for (size_t i = 0; i < ph.size(); ++i)
             if (ph[i].type == kPhGemm) ph[i].begins = db + off[i];
     }
+    {
+        // Attention items go first to the CTAs with no QKV reducer duty (their
+        // QKV range holds no tile start, so their epilogue only stores a partial
+        // and is free first); the reducers follow.  Same order on every pass.
+        static const bool order = !(getenv("DD_ATTN_ORDER") && getenv("DD_ATTN_ORDER")[0] == '0');
+        const int P = ctx->pass_ctas;
+        int kg = 1, tg = 1;
+        pass_split(ctx, kGQkv, w, &kg, &tg);
+        if (order && kg == 1 && tg == 1 && ctx->attn_rank_ctas != P) {
+            int n_out, k;
+            gemm_shape(ctx, kGQkv, &n_out, &k);
+            const int nkb = k / 64, T = (n_out / 128) * nkb;
+            const HostPartition hp{&ctx->sk_prefix_h, P};
+            std::vector<int> red(P), rank(P);
+            int n_free = 0;
+            for (int r = 0; r < P; ++r) {
+                const int g0 = hp.begin(r, T), g1 = hp.begin(r + 1, T);
+                red[r] = (g0 + nkb - 1) / nkb * nkb < g1 ? 1 : 0;
+                n_free += 1 - red[r];
+            }
+            for (int r = 0, f = 0, b = 0; r < P; ++r) rank[r] = red[r] ? n_free + b++ : f++;
+            if (!ctx->attn_rank_d) CK(cudaMalloc(&ctx->attn_rank_d, sizeof(int) * kNumSMs));
+            CK(cudaMemcpy(ctx->attn_rank_d, rank.data(), sizeof(int) * P, cudaMemcpyHostToDevice));
+            ctx->attn_rank_ctas = P;
+        }
+    }
     PassPhase* d = nullptr;
     CK(cudaMalloc(&d, sizeof(PassPhase) * ph.size()));
     CK(cudaMemcpy(d, ph.data(), sizeof(PassPhase) * ph.size(), cudaMemcpyHostToDevice));
@@ -490,6 +516,11 @@ int enqueue_pass_kernel(dd_ctx* ctx, int w, bool want_logits, unsigned long long
     p.attn_cnt = ctx->attn_cnt;
     p.trace = trace;
     p.rank_of_smid = ctx->rank_of_smid_d;
+    {
+        int kg = 1, tg = 1;
+        pass_split(ctx, kGQkv, w, &kg, &tg);
+        p.attn_rank = kg == 1 && tg == 1 && ctx->attn_rank_ctas == ctx->pass_ctas ? ctx->attn_rank_d : nullptr;
+    }
     p.tp = ctx->tp_peers;
     p.tp.size = ctx->tp_size;
     p.tp.rank = ctx->tp_rank;
@@ -956,6 +987,7 @@ void dd_ctx_destroy(dd_ctx* ctx) {
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : ctx->pass_phases) cudaFree(kv.second);
     for (int* b : ctx->pass_begins) cudaFree(b);
+    if (ctx->attn_rank_d) cudaFree(ctx->attn_rank_d);
     for (auto& L : ctx->layers) {
         cudaFree(L.qkv);
         cudaFree(L.o);
@@ -1750,6 +1782,7 @@ int dd_pass_balance(dd_ctx* ctx) {
     ctx->pass_phases.clear();
     for (int* b : ctx->pass_begins) cudaFree(b);
     ctx->pass_begins.clear();
+    ctx->attn_rank_ctas = 0;
     ctx->pass_nphases.clear();
     size_t half = 0;
     for (int id = 0; id < kNumGemm; ++id) half = std::max(half, pass_ws_floats(ctx, id));
