@@ -79,6 +79,10 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #ifndef DD_ATTN_ONEBAR
 #define DD_ATTN_ONEBAR 1  // attention chunk loop: one CTA barrier per chunk (refill after the next chunk's barrier)
 #endif
+#ifndef DD_SUM_BATCH
+#define DD_SUM_BATCH 6  // measured: 4 / 5 / 6 / 7 / 8 -> W=9 2.969 / 2.980 / 2.940 / 2.980 / 2.994 ms
+#endif
+constexpr int kSumBatch = DD_SUM_BATCH;  // stream-K partials loaded per round by a reducer thread
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
 #endif
@@ -1291,10 +1295,11 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                     tc_fence_before();
                                     mbar_arrive(&tempty[b]);
                                 }
-                                for (int o0 = 0; o0 < n_part - 1; o0 += 4) {
-                                    float4 pv[4][4];
+                                // partials in batches of kSumBatch loads in flight per thread
+                                for (int o0 = 0; o0 < n_part - 1; o0 += kSumBatch) {
+                                    float4 pv[kSumBatch][4];
 #pragma unroll
-                                    for (int k = 0; k < 4; ++k) {
+                                    for (int k = 0; k < kSumBatch; ++k) {
                                         const int f = o0 + k < own ? o0 + k : o0 + k + 1;  // flat (k-group, segment)
                                         const int ki = f / nseg, si = f - ki * nseg;
                                         const float4* src = reinterpret_cast<const float4*>(
@@ -1306,7 +1311,7 @@ __global__ void __launch_bounds__(kPassThreads, 1)
                                                             : make_float4(0.f, 0.f, 0.f, 0.f);
                                     }
 #pragma unroll
-                                    for (int k = 0; k < 4; ++k)
+                                    for (int k = 0; k < kSumBatch; ++k)
                                         if (o0 + k < n_part - 1)
 #pragma unroll
                                             for (int q4 = 0; q4 < 4; ++q4) {
