@@ -83,6 +83,9 @@ constexpr int kEpiBase = 128;  // first epilogue thread (warp 4)
 #define DD_SUM_BATCH 6  // measured: 4 / 5 / 6 / 7 / 8 -> W=9 2.969 / 2.980 / 2.940 / 2.980 / 2.994 ms
 #endif
 constexpr int kSumBatch = DD_SUM_BATCH;  // stream-K partials loaded per round by a reducer thread
+#ifndef DD_SS_UNROLL
+#define DD_SS_UNROLL 1  // residual epilogue: the tile's sum of squares with its 16 shared loads in flight
+#endif
 #ifndef DD_ACQ_POLL
 #define DD_ACQ_POLL 1  // activation producer: per-flag acquire loads instead of a full fence after the polls (W=9 3.12 -> 3.02 ms); 0: fence
 #endif
@@ -726,8 +729,17 @@ __device__ void fast_tile_epilogue(const GemmArgs& a, const FastEpi& fe, int til
             float sq = 0.0f;
             if (t < W) {
                 const float* rr = red + t * 128 + j * 16;
+#if DD_SS_UNROLL
+                // 16 independent shared loads in flight, then the adds in row order
+                float rv[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) rv[k] = rr[k];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) sq = __fadd_rn(sq, rv[k]);
+#else
 #pragma unroll 1
                 for (int k = 0; k < 16; ++k) sq = __fadd_rn(sq, rr[k]);
+#endif
             }
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1) sq = __fadd_rn(sq, __shfl_xor_sync(0xffffffffu, sq, o));
