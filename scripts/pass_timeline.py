@@ -19,12 +19,16 @@ n = C.c_int()
 rc = lib.dd_debug_pass_timeline(t.h, w, buf, C.c_size_t(cap), C.byref(n))
 assert rc == 0, lib.dd_last_error(t.h)
 a = np.frombuffer(buf, dtype=np.uint64)[: 148 * n.value * 12].reshape(148, n.value, 12).astype(np.float64)
+if len(sys.argv) > 3:
+    np.save(sys.argv[3] + ".raw.npy", a[:, :, 10])
 t0 = a[:, :, 0][a[:, :, 0] > 0].min()
 a = np.where(a > 0, (a - t0) / 1e3, np.nan)
+if len(sys.argv) > 3:
+    np.save(sys.argv[3], a)
 names = ["embed"] + [x for l in range(32) for x in (f"qkv{l}", f"attn{l}", f"o{l}", f"gu{l}", f"dn{l}")] + ["head"]
 print("phase      wstart(min/max)   inputs(min/max)    mma_done(min/max)   epi_done(min/max)  -  -  publish  enter-poll  wend")
 for p in range(n.value):
-    if p < 6 or p > 11:
+    if not (p <= 1 or 6 <= p <= 11 or p >= n.value - 2):
         continue
     r = a[:, p, :]
     def mm(k):
