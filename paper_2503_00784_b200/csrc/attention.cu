@@ -372,9 +372,10 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
 // dims, so the K / V chunks staged in shared memory (cp.async, double-buffered,
 // the same swizzles as above) are shared by 64 queries and no warp repeats
 // another's work.  Causal: a chunk past a warp's last query is skipped, the
-// CTA stops at its last query's key.  Heavier (later) query tiles launch first.
+// CTA stops at its last query's key.  Heavier (later) query tiles of every head
+// launch before any lighter one.
 template <int HD>
-__global__ void __launch_bounds__(kAttnCtaThreads)
+__global__ void __launch_bounds__(kAttnCtaThreads, 3)
     attn_prefill_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
                         const __nv_bfloat16* __restrict__ kv_pool, const int32_t* __restrict__ page_table,
                         int page_size, int layer, float scale_log2, __nv_bfloat16* __restrict__ o) {
@@ -392,7 +393,9 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
     pdl_launch_();
     const int n0 = ps->n_cached, W = ps->w;
     const int qtiles = (W + 63) / 64;
-    const int qt = qtiles - 1 - static_cast<int>(blockIdx.x), head = blockIdx.y;
+    // heads fastest, heaviest query tiles first: the launch order is globally
+    // longest-first, so the last wave holds only the short early tiles
+    const int qt = qtiles - 1 - static_cast<int>(blockIdx.y), head = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int g = lane >> 2, c = lane & 3;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
@@ -407,16 +410,22 @@ __global__ void __launch_bounds__(kAttnCtaThreads)
         __nv_bfloat16(*kd)[HD] = ks(b);
         __nv_bfloat16(*vd)[HD] = vs(b);
         const int kb = chunk * kKeys;
-        for (int idx = tid; idx < kKeys * CHK; idx += kAttnCtaThreads) {
-            const int kk = idx / CHK, ch = idx % CHK;
-            const int key = kb + kk;
-            const bool ok = key <= kmax;
-            const int kc = ok ? key : 0;
-            const int page = page_table[kc / page_size], slot = kc % page_size;
-            cp_async16(&kd[kk][k_chunk(kk, ch) * 8],
-                       kv_pool + kv_offset(md, page_size, page, layer, 0, kvh, slot) + ch * 8, ok ? 16u : 0u);
-            cp_async16(&vd[kk][v_chunk<HD>(kk, ch) * 8],
-                       kv_pool + kv_offset(md, page_size, page, layer, 1, kvh, slot) + ch * 8, ok ? 16u : 0u);
+        // one page-table read and one row address per key (2 threads per key,
+        // half of its 16-byte chunks each); V row = K row + one kv plane
+        constexpr int kTpk = kAttnCtaThreads / kKeys;
+        const int kk = tid / kTpk, ch0 = (tid % kTpk) * (CHK / kTpk);
+        const int key = kb + kk;
+        const bool ok = key <= kmax;
+        const int kc = ok ? key : 0;
+        const __nv_bfloat16* krow =
+            kv_pool + kv_offset(md, page_size, page_table[kc / page_size], layer, 0, kvh, kc % page_size);
+        const __nv_bfloat16* vrow = krow + static_cast<size_t>(md.n_kv_heads) * page_size * HD;
+        const uint32_t nb = ok ? 16u : 0u;
+#pragma unroll
+        for (int i = 0; i < CHK / kTpk; ++i) {
+            const int ch = ch0 + i;
+            cp_async16(&kd[kk][k_chunk(kk, ch) * 8], krow + ch * 8, nb);
+            cp_async16(&vd[kk][v_chunk<HD>(kk, ch) * 8], vrow + ch * 8, nb);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -581,7 +590,7 @@ int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, con
     const float scale_log2 =
         static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(m.head_dim)));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((w + 63) / 64, m.n_heads, 1);
+    cfg.gridDim = dim3(m.n_heads, (w + 63) / 64, 1);
     cfg.blockDim = dim3(kAttnCtaThreads, 1, 1);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
