@@ -584,6 +584,252 @@ __global__ void __launch_bounds__(kAttnCtaThreads, 3)
     }
 }
 
+// Prefill attention on tcgen05 (head_dim 128, long prompts): CTA = (head,
+// 128-query tile), thread = query row = TMEM lane.  Per 128-key block:
+//   S = Q K^T   one elected thread, 8 MMAs 128x128x16 (A = Q, B = K, both
+//               K-major SW128 in shared memory), S in TMEM columns [0, 128);
+//   softmax     each thread reads its S row (tcgen05.ld), masks keys past its
+//               position, updates the running base / sum (fp32, exp2 domain)
+//               and writes P = bf16(exp2(s - base))
+//               as the K-major SW128 A operand of the PV product;
+//   O += P V    8 MMAs 128x128x16 with V read MN-major (the [key][dim] rows the
+//               KV cache holds), O accumulated in TMEM columns [128, 256); a
+//               row's O is rescaled in TMEM only when its exp2 base moves.
+// K/V blocks are staged with cp.async (one page-table read per key and
+// thread), double-buffered so block j+1 loads under block j.  Same roundings
+// as the mma.sync kernel (q, P and K/V bf16, fp32 accumulate); different
+// fp32 summation order.
+namespace {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+constexpr int kTcKeys = 128;
+constexpr uint32_t kTcHalf = 128 * 128;  // one 64-dim (or 64-key) SW128 half: 128 rows x 128 B
+__host__ __device__ constexpr uint32_t idesc_bf16_mn(int M, int N, int b_mn) {
+    return idesc_bf16_f32(M, N) | (static_cast<uint32_t>(b_mn) << 16);
+}
+__device__ __forceinline__ uint64_t sw128_desc_lbo(uint32_t addr, uint32_t lbo) {
+    return (sw128_kmajor_desc(addr) & ~(static_cast<uint64_t>(0x3FFF) << 16)) |
+           (static_cast<uint64_t>(lbo >> 4) << 16);
+}
+// byte offset of 16-byte chunk `ch` (0..15, 8 bf16 each) of row `r` in a
+// [2 halves][128 rows][128 B] SW128 tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int ch) {
+    return static_cast<uint32_t>((ch >> 3) * kTcHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128, 1)
+    attn_prefill_tc_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
+                           const __nv_bfloat16* __restrict__ kv_pool, const int32_t* __restrict__ page_table,
+                           int page_size, int layer, float scale_log2, __nv_bfloat16* __restrict__ o) {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
+    constexpr int HD = 128;
+    extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(attn_smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+    uint8_t* sQ = sm;                       // 32 KiB
+    uint8_t* sKV = sQ + 2 * kTcHalf;        // [2 buffers][K 32 KiB | V 32 KiB]
+    uint8_t* sP = sKV + 8 * kTcHalf;        // 32 KiB
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * kTcHalf);  // [0] S done, [1] PV done
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tmem_alloc<256>(tslot);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    pdl_wait_();
+    pdl_launch_();
+    const int n0 = ps->n_cached, W = ps->w;
+    const int qt = static_cast<int>(gridDim.y) - 1 - static_cast<int>(blockIdx.y), head = blockIdx.x;
+    const int kvh = head / (md.n_heads / md.n_kv_heads);
+    const int qd = md.q_dim();
+    const int row = 128 * qt + tid;  // this thread's query row in the pass
+    const int pos = n0 + row;
+    const int kmax = n0 + min(W, 128 * (qt + 1)) - 1;  // last key of the CTA
+    const int n_blk = kmax / kTcKeys + 1;
+    const size_t plane = static_cast<size_t>(md.n_kv_heads) * page_size * HD;
+
+    auto stage = [&](int blk, int b) {  // thread = key
+        uint8_t* sk = sKV + b * 4 * kTcHalf;
+        uint8_t* sv = sk + 2 * kTcHalf;
+        const int key = blk * kTcKeys + tid;
+        const bool ok = key <= kmax;
+        const int kc = ok ? key : 0;
+        const __nv_bfloat16* krow =
+            kv_pool + kv_offset(md, page_size, page_table[kc / page_size], layer, 0, kvh, kc % page_size);
+        const __nv_bfloat16* vrow = krow + plane;
+        const uint32_t nb = ok ? 16u : 0u;
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+            cp_async16(sk + sw128_off(tid, ch), krow + ch * 8, nb);
+            cp_async16(sv + sw128_off(tid, ch), vrow + ch * 8, nb);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    stage(0, 0);
+    {  // Q row (fp32 -> bf16), zero past the pass
+        const float* src = q + static_cast<size_t>(row) * qd + head * HD;
+#pragma unroll 4
+        for (int ch = 0; ch < 16; ++ch) {
+            uint4 u = make_uint4(0u, 0u, 0u, 0u);
+            if (row < W) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(src + ch * 8));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(src + ch * 8 + 4));
+                u = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
+            }
+            *reinterpret_cast<uint4*>(sQ + sw128_off(tid, ch)) = u;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t tS = tmem + lane_off, tO = tmem + 128 + lane_off;
+    constexpr uint32_t kIdS = idesc_bf16_mn(128, 128, 0), kIdO = idesc_bf16_mn(128, 128, 1);
+
+    // O accumulates in TMEM across blocks.  The exp2 base of a row moves only
+    // when its block max exceeds the base by more than 8 (P <= 2^8 in bf16 is
+    // exact in range), and then the row's O and sum are rescaled in place.
+    float m_base = -INFINITY, l_run = 0.f;
+
+    for (int blk = 0; blk < n_blk; ++blk) {
+        const int b = blk & 1;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();  // K/V of blk (and the PV MMA of blk - 1) complete everywhere
+        tc_fence_after();
+        if (blk + 1 < n_blk) stage(blk + 1, b ^ 1);
+        const uint8_t* sk = sKV + b * 4 * kTcHalf;
+        const uint8_t* sv = sk + 2 * kTcHalf;
+        if (tid == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = (ks >> 2) * kTcHalf;
+                umma_bf16(tmem, sw128_kmajor_desc(smem_u32(sQ + off)) + 2 * (ks & 3),
+                          sw128_kmajor_desc(smem_u32(sk + off)) + 2 * (ks & 3), kIdS, ks ? 1u : 0u);
+            }
+            umma_commit(&bar[0]);
+        }
+        __syncwarp();
+        mbar_wait(&bar[0], static_cast<uint32_t>(blk & 1));
+        tc_fence_after();
+        const int kb = blk * kTcKeys;
+        // pass 1: row max of the masked, scaled scores
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < kTcKeys; c0 += 64) {
+            uint32_t r[4][16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + c0 + 16 * i, r[i]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (kb + c0 + 16 * i + j <= pos) mx = fmaxf(mx, __uint_as_float(r[i][j]) * scale_log2);
+        }
+        const bool move = mx > m_base + 8.0f;  // false while both are -inf
+        float corr = 1.0f;
+        if (move) {
+            corr = fast_exp2(m_base - mx);  // 0 on the first live block
+            m_base = mx;
+            l_run *= corr;
+        }
+        if (blk > 0 && __any_sync(0xffffffffu, move)) {  // warp-collective rescale of O rows
+#pragma unroll
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                uint32_t r[2][16];
+                tmem_ld16_async(tO + c0, r[0]);
+                tmem_ld16_async(tO + c0 + 16, r[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) r[i][j] = __float_as_uint(__uint_as_float(r[i][j]) * corr);
+                tmem_st16(tO + c0, r[0]);
+                tmem_st16(tO + c0 + 16, r[1]);
+            }
+            tmem_wait_st();
+        }
+        const float base = m_base == -INFINITY ? 0.f : m_base;
+        // pass 2: P = exp2(s - base) as bf16 into the SW128 A tile, row sums in fp32
+#pragma unroll
+        for (int c0 = 0; c0 < kTcKeys; c0 += 64) {
+            uint32_t r[4][16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + c0 + 16 * i, r[i]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                uint32_t pk[8];
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const int key = kb + c0 + 16 * i + j;
+                    const float p0 = key <= pos ? fast_exp2(__uint_as_float(r[i][j]) * scale_log2 - base) : 0.f;
+                    const float p1 =
+                        key + 1 <= pos ? fast_exp2(__uint_as_float(r[i][j + 1]) * scale_log2 - base) : 0.f;
+                    l_run += p0 + p1;
+                    pk[j >> 1] = pack_bf16(p0, p1);
+                }
+                const int ch = (c0 + 16 * i) >> 3;  // 16-byte chunk of the key row
+                *reinterpret_cast<uint4*>(sP + sw128_off(tid, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(sP + sw128_off(tid, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc_fence_before();
+        __syncthreads();  // P and the O rescale complete, S reads done
+        tc_fence_after();
+        if (tid == 0) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)  // 16 keys per step
+                umma_bf16(tmem + 128, sw128_kmajor_desc(smem_u32(sP + (ks >> 2) * kTcHalf)) + 2 * (ks & 3),
+                          sw128_desc_lbo(smem_u32(sv + ks * 16 * 128), kTcHalf), kIdO,
+                          (blk > 0 || ks > 0) ? 1u : 0u);
+            umma_commit(&bar[1]);
+        }
+        __syncwarp();
+        mbar_wait(&bar[1], static_cast<uint32_t>(blk & 1));
+        tc_fence_after();
+    }
+    {
+        const float il = 1.0f / l_run;
+        __nv_bfloat16* og = o + static_cast<size_t>(row) * qd + head * HD;
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t r[2][16];
+            tmem_ld16_async(tO + c0, r[0]);
+            tmem_ld16_async(tO + c0 + 16, r[1]);
+            tmem_wait_ld();
+            if (row < W)
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int j = 0; j < 16; j += 8) {
+                        const float* f = reinterpret_cast<const float*>(&r[i][j]);
+                        *reinterpret_cast<uint4*>(og + c0 + 16 * i + j) =
+                            make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
+                                       pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
+                    }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<256>(tmem);
+#endif
+}
+
 int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, const float* q,
                              const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                              int layer, __nv_bfloat16* o, cudaStream_t s) {
@@ -610,7 +856,19 @@ int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, con
         return cudaLaunchKernelEx(&cfg, kernel, ps, m, q, kv_pool, page_table, page_size, layer, scale_log2, o);
     };
     cudaError_t e;
-    if (m.head_dim == 128) e = go(attn_prefill_kernel<128>, 128, a128);
+    static const bool tc = !(getenv("DD_ATTN_PREFILL_TC") && atoi(getenv("DD_ATTN_PREFILL_TC")) == 0);
+    static bool atc[kMaxDevices] = {};
+    if (m.head_dim == 128 && tc && m.n_heads % m.n_kv_heads == 0) {
+        cfg.gridDim = dim3(m.n_heads, (w + 127) / 128, 1);
+        const int smem = static_cast<int>(12 * kTcHalf + 1024 + 64);
+        cfg.dynamicSmemBytes = smem;
+        if (!atc[dev]) {
+            cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            atc[dev] = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, ps, m, q, kv_pool, page_table, page_size, layer,
+                               scale_log2, o);
+    } else if (m.head_dim == 128) e = go(attn_prefill_kernel<128>, 128, a128);
     else if (m.head_dim == 64) e = go(attn_prefill_kernel<64>, 64, a64);
     else return -1;
     return e == cudaSuccess ? 0 : -2;
@@ -670,5 +928,6 @@ void preload_attention_kernels() {
     cudaFuncGetAttributes(&a, attn_cluster_kernel<64, 1>);
     cudaFuncGetAttributes(&a, attn_prefill_kernel<128>);
     cudaFuncGetAttributes(&a, attn_prefill_kernel<64>);
+    cudaFuncGetAttributes(&a, attn_prefill_tc_kernel);
 }
 }  // namespace dd
