@@ -585,7 +585,9 @@ __global__ void __launch_bounds__(kAttnCtaThreads, 3)
 }
 
 // Prefill attention on tcgen05 (head_dim 128, long prompts): CTA = (head,
-// 128-query tile), thread = query row = TMEM lane.  Per 128-key block:
+// 128-query tile), two threads per query row (TMEM lane), one per 64-key half
+// of S and 64-dim half of O (8 warps: one warp per scheduler is latency-bound).
+// Per 128-key block:
 //   S = Q K^T   one elected thread, 8 MMAs 128x128x16 (A = Q, B = K, both
 //               K-major SW128 in shared memory), S in TMEM columns [0, 128);
 //   softmax     each thread reads its S row (tcgen05.ld), masks keys past its
@@ -610,6 +612,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 constexpr int kTcKeys = 128;
+constexpr int kTcThreads = 256;  // 2 threads per query row (key / dim halves)
 constexpr uint32_t kTcHalf = 128 * 128;  // one 64-dim (or 64-key) SW128 half: 128 rows x 128 B
 __host__ __device__ constexpr uint32_t idesc_bf16_mn(int M, int N, int b_mn) {
     return idesc_bf16_f32(M, N) | (static_cast<uint32_t>(b_mn) << 16);
@@ -625,21 +628,26 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int ch) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
     attn_prefill_tc_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
                            const __nv_bfloat16* __restrict__ kv_pool, const int32_t* __restrict__ page_table,
                            int page_size, int layer, float scale_log2, __nv_bfloat16* __restrict__ o) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     constexpr int HD = 128;
     extern __shared__ __align__(128) uint8_t attn_smem_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(attn_smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+    // 1024-byte alignment by pointer arithmetic on the __shared__ array (an
+    // integer round trip would turn the exchange accesses into generic LD/ST)
+    uint8_t* sm = attn_smem_raw + ((1024u - (smem_u32(attn_smem_raw) & 1023u)) & 1023u);
     uint8_t* sQ = sm;                       // 32 KiB
     uint8_t* sKV = sQ + 2 * kTcHalf;        // [2 buffers][K 32 KiB | V 32 KiB]
     uint8_t* sP = sKV + 8 * kTcHalf;        // 32 KiB
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * kTcHalf);  // [0] S done, [1] PV done
+    float* xch = reinterpret_cast<float*>(sP + 2 * kTcHalf);  // [2 halves][128 rows] max / sum exchange
+    uint64_t* bar = reinterpret_cast<uint64_t*>(xch + 2 * 128);  // [0] S done, [1] PV done
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // thread = (query row r, key / dim half h): warps 0-3 take columns [0, 64)
+    // of S and O, warps 4-7 columns [64, 128) of the same TMEM lanes
+    const int h = warp >> 2, r = (warp & 3) * 32 + lane;
     if (warp == 0) tmem_alloc<256>(tslot);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -652,49 +660,57 @@ __global__ void __launch_bounds__(128, 1)
     const int qt = static_cast<int>(gridDim.y) - 1 - static_cast<int>(blockIdx.y), head = blockIdx.x;
     const int kvh = head / (md.n_heads / md.n_kv_heads);
     const int qd = md.q_dim();
-    const int row = 128 * qt + tid;  // this thread's query row in the pass
+    const int row = 128 * qt + r;  // this thread's query row in the pass
     const int pos = n0 + row;
     const int kmax = n0 + min(W, 128 * (qt + 1)) - 1;  // last key of the CTA
     const int n_blk = kmax / kTcKeys + 1;
     const size_t plane = static_cast<size_t>(md.n_kv_heads) * page_size * HD;
 
-    auto stage = [&](int blk, int b) {  // thread = key
+    // staging: thread = (key r, 8 of its 16 chunks); page-table entry read one
+    // block ahead, so staging never waits on it
+    auto page_of = [&](int blk) {
+        const int key = min(blk * kTcKeys + r, kmax);
+        return __ldg(page_table + key / page_size);
+    };
+    auto stage = [&](int blk, int b, int page) {
         uint8_t* sk = sKV + b * 4 * kTcHalf;
         uint8_t* sv = sk + 2 * kTcHalf;
-        const int key = blk * kTcKeys + tid;
+        const int key = blk * kTcKeys + r;
         const bool ok = key <= kmax;
-        const int kc = ok ? key : 0;
-        const __nv_bfloat16* krow =
-            kv_pool + kv_offset(md, page_size, page_table[kc / page_size], layer, 0, kvh, kc % page_size);
+        const int kc = ok ? key : kmax;
+        const __nv_bfloat16* krow = kv_pool + kv_offset(md, page_size, page, layer, 0, kvh, kc % page_size);
         const __nv_bfloat16* vrow = krow + plane;
         const uint32_t nb = ok ? 16u : 0u;
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
-            cp_async16(sk + sw128_off(tid, ch), krow + ch * 8, nb);
-            cp_async16(sv + sw128_off(tid, ch), vrow + ch * 8, nb);
+        for (int i = 0; i < 8; ++i) {
+            const int ch = 8 * h + i;
+            cp_async16(sk + sw128_off(r, ch), krow + ch * 8, nb);
+            cp_async16(sv + sw128_off(r, ch), vrow + ch * 8, nb);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    stage(0, 0);
-    {  // Q row (fp32 -> bf16), zero past the pass
+    stage(0, 0, page_of(0));
+    int page_next = n_blk > 1 ? page_of(1) : 0;
+    {  // Q row (fp32 -> bf16) half, zero past the pass
         const float* src = q + static_cast<size_t>(row) * qd + head * HD;
 #pragma unroll 4
-        for (int ch = 0; ch < 16; ++ch) {
+        for (int i = 0; i < 8; ++i) {
+            const int ch = 8 * h + i;
             uint4 u = make_uint4(0u, 0u, 0u, 0u);
             if (row < W) {
                 const float4 a = __ldg(reinterpret_cast<const float4*>(src + ch * 8));
                 const float4 b = __ldg(reinterpret_cast<const float4*>(src + ch * 8 + 4));
                 u = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w));
             }
-            *reinterpret_cast<uint4*>(sQ + sw128_off(tid, ch)) = u;
+            *reinterpret_cast<uint4*>(sQ + sw128_off(r, ch)) = u;
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tO = tmem + 128 + lane_off;
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 64 * h, tO = tmem + 128 + lane_off + 64 * h;
     constexpr uint32_t kIdS = idesc_bf16_mn(128, 128, 0), kIdO = idesc_bf16_mn(128, 128, 1);
 
     // O accumulates in TMEM across blocks.  The exp2 base of a row moves only
@@ -709,7 +725,6 @@ __global__ void __launch_bounds__(128, 1)
         tc_fence_before();
         __syncthreads();  // K/V of blk (and the PV MMA of blk - 1) complete everywhere
         tc_fence_after();
-        if (blk + 1 < n_blk) stage(blk + 1, b ^ 1);
         const uint8_t* sk = sKV + b * 4 * kTcHalf;
         const uint8_t* sv = sk + 2 * kTcHalf;
         if (tid == 0) {
@@ -721,24 +736,30 @@ __global__ void __launch_bounds__(128, 1)
             }
             umma_commit(&bar[0]);
         }
+        if (blk + 1 < n_blk) {  // next block's K/V load under this block's MMAs and softmax
+            stage(blk + 1, b ^ 1, page_next);
+            if (blk + 2 < n_blk) page_next = page_of(blk + 2);
+        }
         __syncwarp();
         mbar_wait(&bar[0], static_cast<uint32_t>(blk & 1));
         tc_fence_after();
-        const int kb = blk * kTcKeys;
-        // pass 1: row max of the masked, scaled scores
+        const int kb = blk * kTcKeys + 64 * h;  // first key of this thread's half
+        // pass 1: max of the masked, scaled scores over the half, then the row's
         float mx = -INFINITY;
+        {
+            uint32_t rr[4][16];
 #pragma unroll
-        for (int c0 = 0; c0 < kTcKeys; c0 += 64) {
-            uint32_t r[4][16];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + c0 + 16 * i, r[i]);
+            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + 16 * i, rr[i]);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 16; ++j)
-                    if (kb + c0 + 16 * i + j <= pos) mx = fmaxf(mx, __uint_as_float(r[i][j]) * scale_log2);
+                    if (kb + 16 * i + j <= pos) mx = fmaxf(mx, __uint_as_float(rr[i][j]) * scale_log2);
         }
+        xch[h * 128 + r] = mx;
+        __syncthreads();
+        mx = fmaxf(xch[r], xch[128 + r]);
         const bool move = mx > m_base + 8.0f;  // false while both are -inf
         float corr = 1.0f;
         if (move) {
@@ -746,45 +767,44 @@ __global__ void __launch_bounds__(128, 1)
             m_base = mx;
             l_run *= corr;
         }
-        if (blk > 0 && __any_sync(0xffffffffu, move)) {  // warp-collective rescale of O rows
+        if (blk > 0 && __any_sync(0xffffffffu, move)) {  // warp-collective rescale of this half of O
 #pragma unroll
-            for (int c0 = 0; c0 < HD; c0 += 32) {
-                uint32_t r[2][16];
-                tmem_ld16_async(tO + c0, r[0]);
-                tmem_ld16_async(tO + c0 + 16, r[1]);
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                uint32_t rr[2][16];
+                tmem_ld16_async(tO + c0, rr[0]);
+                tmem_ld16_async(tO + c0 + 16, rr[1]);
                 tmem_wait_ld();
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) r[i][j] = __float_as_uint(__uint_as_float(r[i][j]) * corr);
-                tmem_st16(tO + c0, r[0]);
-                tmem_st16(tO + c0 + 16, r[1]);
+                    for (int j = 0; j < 16; ++j) rr[i][j] = __float_as_uint(__uint_as_float(rr[i][j]) * corr);
+                tmem_st16(tO + c0, rr[0]);
+                tmem_st16(tO + c0 + 16, rr[1]);
             }
             tmem_wait_st();
         }
         const float base = m_base == -INFINITY ? 0.f : m_base;
-        // pass 2: P = exp2(s - base) as bf16 into the SW128 A tile, row sums in fp32
+        // pass 2: P = exp2(s - base) as bf16 into the SW128 A tile, half sums in fp32
+        {
+            uint32_t rr[4][16];
 #pragma unroll
-        for (int c0 = 0; c0 < kTcKeys; c0 += 64) {
-            uint32_t r[4][16];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + c0 + 16 * i, r[i]);
+            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + 16 * i, rr[i]);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 uint32_t pk[8];
 #pragma unroll
                 for (int j = 0; j < 16; j += 2) {
-                    const int key = kb + c0 + 16 * i + j;
-                    const float p0 = key <= pos ? fast_exp2(__uint_as_float(r[i][j]) * scale_log2 - base) : 0.f;
+                    const int key = kb + 16 * i + j;
+                    const float p0 = key <= pos ? fast_exp2(__uint_as_float(rr[i][j]) * scale_log2 - base) : 0.f;
                     const float p1 =
-                        key + 1 <= pos ? fast_exp2(__uint_as_float(r[i][j + 1]) * scale_log2 - base) : 0.f;
+                        key + 1 <= pos ? fast_exp2(__uint_as_float(rr[i][j + 1]) * scale_log2 - base) : 0.f;
                     l_run += p0 + p1;
                     pk[j >> 1] = pack_bf16(p0, p1);
                 }
-                const int ch = (c0 + 16 * i) >> 3;  // 16-byte chunk of the key row
-                *reinterpret_cast<uint4*>(sP + sw128_off(tid, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                *reinterpret_cast<uint4*>(sP + sw128_off(tid, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                const int ch = 8 * h + 2 * i;  // 16-byte chunk of the key row
+                *reinterpret_cast<uint4*>(sP + sw128_off(r, ch)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(sP + sw128_off(r, ch + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -803,21 +823,23 @@ __global__ void __launch_bounds__(128, 1)
         mbar_wait(&bar[1], static_cast<uint32_t>(blk & 1));
         tc_fence_after();
     }
+    xch[h * 128 + r] = l_run;  // the last exchange read happened before two barriers
+    __syncthreads();
     {
-        const float il = 1.0f / l_run;
-        __nv_bfloat16* og = o + static_cast<size_t>(row) * qd + head * HD;
+        const float il = 1.0f / (xch[r] + xch[128 + r]);
+        __nv_bfloat16* og = o + static_cast<size_t>(row) * qd + head * HD + 64 * h;
 #pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-            uint32_t r[2][16];
-            tmem_ld16_async(tO + c0, r[0]);
-            tmem_ld16_async(tO + c0 + 16, r[1]);
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+            uint32_t rr[2][16];
+            tmem_ld16_async(tO + c0, rr[0]);
+            tmem_ld16_async(tO + c0 + 16, rr[1]);
             tmem_wait_ld();
             if (row < W)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int j = 0; j < 16; j += 8) {
-                        const float* f = reinterpret_cast<const float*>(&r[i][j]);
+                        const float* f = reinterpret_cast<const float*>(&rr[i][j]);
                         *reinterpret_cast<uint4*>(og + c0 + 16 * i + j) =
                             make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
                                        pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
@@ -860,7 +882,8 @@ int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, con
     static bool atc[kMaxDevices] = {};
     if (m.head_dim == 128 && tc && m.n_heads % m.n_kv_heads == 0) {
         cfg.gridDim = dim3(m.n_heads, (w + 127) / 128, 1);
-        const int smem = static_cast<int>(12 * kTcHalf + 1024 + 64);
+        const int smem = static_cast<int>(12 * kTcHalf + 1024 + 2 * 128 * 4 + 64);
+        cfg.blockDim = dim3(kTcThreads, 1, 1);
         cfg.dynamicSmemBytes = smem;
         if (!atc[dev]) {
             cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
