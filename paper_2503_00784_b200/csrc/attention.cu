@@ -630,7 +630,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int ch) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     attn_prefill_tc_kernel(const PassState* ps, ModelDims md, const float* __restrict__ q,
-                           const __nv_bfloat16* __restrict__ kv_pool, const int32_t* __restrict__ page_table,
+                           const __grid_constant__ CUtensorMap map_kv, const int32_t* __restrict__ page_table,
                            int page_size, int layer, float scale_log2, __nv_bfloat16* __restrict__ o) {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 1000
     constexpr int HD = 128;
@@ -642,16 +642,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint8_t* sKV = sQ + 2 * kTcHalf;        // [2 buffers][K 32 KiB | V 32 KiB]
     uint8_t* sP = sKV + 8 * kTcHalf;        // 32 KiB
     float* xch = reinterpret_cast<float*>(sP + 2 * kTcHalf);  // [2 halves][128 rows] max / sum exchange
-    uint64_t* bar = reinterpret_cast<uint64_t*>(xch + 2 * 128);  // [0] S done, [1] PV done
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(xch + 2 * 128);  // [0] S done, [1] PV done, [2 + b] K/V buffer b full
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // thread = (query row r, key / dim half h): warps 0-3 take columns [0, 64)
     // of S and O, warps 4-7 columns [64, 128) of the same TMEM lanes
     const int h = warp >> 2, r = (warp & 3) * 32 + lane;
     if (warp == 0) tmem_alloc<256>(tslot);
+    // V rows past the last key are read by the PV product with P = 0, so the
+    // buffers must never hold non-finite bytes: zero them before any TMA
+    for (int i = tid; i < 2 * 4 * static_cast<int>(kTcHalf) / 16; i += kTcThreads) {
+        const int buf = i / (4 * kTcHalf / 16), off = i % (4 * kTcHalf / 16);
+        reinterpret_cast<uint4*>(sm + 2 * kTcHalf + buf * 4 * kTcHalf)[off] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        tma_prefetch_desc(&map_kv);
+        for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
         fence_barrier_init();
     }
     pdl_wait_();
@@ -664,33 +671,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int pos = n0 + row;
     const int kmax = n0 + min(W, 128 * (qt + 1)) - 1;  // last key of the CTA
     const int n_blk = kmax / kTcKeys + 1;
-    const size_t plane = static_cast<size_t>(md.n_kv_heads) * page_size * HD;
 
-    // staging: thread = (key r, 8 of its 16 chunks); page-table entry read one
-    // block ahead, so staging never waits on it
-    auto page_of = [&](int blk) {
-        const int key = min(blk * kTcKeys + r, kmax);
-        return __ldg(page_table + key / page_size);
-    };
-    auto stage = [&](int blk, int b, int page) {
+    // staging (thread 0): per page of the block holding a key <= kmax, four
+    // TMA boxes (K / V x 64-dim halves) of page_size rows land as SW128 rows
+    // of the K-major (K) and MN-major (V) operand tiles; pages past kmax keep
+    // the buffer's earlier (finite) rows, masked to P = 0
+    const uint64_t pol = policy_evict_normal();
+    auto stage = [&](int blk, int b) {
         uint8_t* sk = sKV + b * 4 * kTcHalf;
         uint8_t* sv = sk + 2 * kTcHalf;
-        const int key = blk * kTcKeys + r;
-        const bool ok = key <= kmax;
-        const int kc = ok ? key : kmax;
-        const __nv_bfloat16* krow = kv_pool + kv_offset(md, page_size, page, layer, 0, kvh, kc % page_size);
-        const __nv_bfloat16* vrow = krow + plane;
-        const uint32_t nb = ok ? 16u : 0u;
+        const int kb0 = blk * kTcKeys;
+        const int n_pg = min(kTcKeys, kmax - kb0 + page_size) / page_size;  // pages with a live key
+        mbar_arrive_expect_tx(&bar[2 + b], static_cast<uint32_t>(n_pg * page_size * 128 * 4));
+        for (int pg = 0; pg < n_pg; ++pg) {
+            const int key = kb0 + pg * page_size;
+            const int page = page_table[key / page_size];
+            const int rk = static_cast<int>(kv_offset(md, page_size, page, layer, 0, kvh, 0) / HD);
+            const int rv = static_cast<int>(kv_offset(md, page_size, page, layer, 1, kvh, 0) / HD);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int ch = 8 * h + i;
-            cp_async16(sk + sw128_off(r, ch), krow + ch * 8, nb);
-            cp_async16(sv + sw128_off(r, ch), vrow + ch * 8, nb);
+            for (int hh = 0; hh < 2; ++hh) {
+                tma_load_2d(sk + hh * kTcHalf + pg * page_size * 128, &map_kv, &bar[2 + b], 64 * hh, rk, pol);
+                tma_load_2d(sv + hh * kTcHalf + pg * page_size * 128, &map_kv, &bar[2 + b], 64 * hh, rv, pol);
+            }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    stage(0, 0, page_of(0));
-    int page_next = n_blk > 1 ? page_of(1) : 0;
+    __syncthreads();  // barriers initialised, buffers zeroed
+    if (tid == 0) stage(0, 0);
     {  // Q row (fp32 -> bf16) half, zero past the pass
         const float* src = q + static_cast<size_t>(row) * qd + head * HD;
 #pragma unroll 4
@@ -720,10 +726,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     for (int blk = 0; blk < n_blk; ++blk) {
         const int b = blk & 1;
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_wait(&bar[2 + b], static_cast<uint32_t>((blk >> 1) & 1));  // K/V of blk landed
         tc_fence_before();
-        __syncthreads();  // K/V of blk (and the PV MMA of blk - 1) complete everywhere
+        __syncthreads();  // (and every thread is past block blk - 1)
         tc_fence_after();
         const uint8_t* sk = sKV + b * 4 * kTcHalf;
         const uint8_t* sv = sk + 2 * kTcHalf;
@@ -736,10 +741,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             umma_commit(&bar[0]);
         }
-        if (blk + 1 < n_blk) {  // next block's K/V load under this block's MMAs and softmax
-            stage(blk + 1, b ^ 1, page_next);
-            if (blk + 2 < n_blk) page_next = page_of(blk + 2);
-        }
+        if (tid == 0 && blk + 1 < n_blk) stage(blk + 1, b ^ 1);  // loads under this block's MMAs and softmax
         __syncwarp();
         mbar_wait(&bar[0], static_cast<uint32_t>(blk & 1));
         tc_fence_after();
@@ -854,7 +856,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, const float* q,
                              const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                             int layer, __nv_bfloat16* o, cudaStream_t s) {
+                             int layer, __nv_bfloat16* o, cudaStream_t s, const CUtensorMap* map_kv) {
     const float scale_log2 =
         static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(m.head_dim)));
     cudaLaunchConfig_t cfg = {};
@@ -880,16 +882,16 @@ int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, con
     cudaError_t e;
     static const bool tc = !(getenv("DD_ATTN_PREFILL_TC") && atoi(getenv("DD_ATTN_PREFILL_TC")) == 0);
     static bool atc[kMaxDevices] = {};
-    if (m.head_dim == 128 && tc && m.n_heads % m.n_kv_heads == 0) {
+    if (m.head_dim == 128 && tc && map_kv != nullptr && m.n_heads % m.n_kv_heads == 0) {
         cfg.gridDim = dim3(m.n_heads, (w + 127) / 128, 1);
-        const int smem = static_cast<int>(12 * kTcHalf + 1024 + 2 * 128 * 4 + 64);
+        const int smem = static_cast<int>(12 * kTcHalf + 1024 + 2 * 128 * 4 + 64 + 32);
         cfg.blockDim = dim3(kTcThreads, 1, 1);
         cfg.dynamicSmemBytes = smem;
         if (!atc[dev]) {
             cudaFuncSetAttribute(attn_prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             atc[dev] = true;
         }
-        e = cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, ps, m, q, kv_pool, page_table, page_size, layer,
+        e = cudaLaunchKernelEx(&cfg, attn_prefill_tc_kernel, ps, m, q, *map_kv, page_table, page_size, layer,
                                scale_log2, o);
     } else if (m.head_dim == 128) e = go(attn_prefill_kernel<128>, 128, a128);
     else if (m.head_dim == 64) e = go(attn_prefill_kernel<64>, 64, a64);

@@ -66,6 +66,8 @@ struct dd_ctx {
     float* logits = nullptr;        // [256, vocab]
     CUtensorMap map_h, map_o, map_a;
     CUtensorMap map_h128, map_o128, map_a128;  // 128-row boxes (prefill GEMM)
+    CUtensorMap map_kv;  // KV pool rows (head_dim 128), page_size-row boxes (prefill attention)
+    bool has_map_kv = false;
     // fp32-accumulate mode (DD_PREC_FP32ACC): lo halves of the GEMM inputs and
     // an fp32 KV pool; every pass runs the per-launch path
     bool fp32acc = false;

@@ -2,6 +2,7 @@
 // kernels of one verification pass (see model.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -72,10 +73,12 @@ int launch_attention_f32(const PassState* ps, int w, const ModelDims& m, const f
 int launch_attention(const PassState* ps, int w, const ModelDims& m, const float* q,
                      const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
                      int layer, __nv_bfloat16* o, cudaStream_t s, int ranks = 8);
-// Long-prompt prefill attention (64-query tiles, one warp per 16 queries).
+// Long-prompt prefill attention (head_dim 128: tcgen05, 128-query tiles, K/V
+// pages staged by TMA through `map_kv` = the pool as [rows of head_dim] bf16
+// with (64-dim x page_size) SW128 boxes; otherwise mma.sync, 64-query tiles).
 int launch_attention_prefill(const PassState* ps, int w, const ModelDims& m, const float* q,
                              const __nv_bfloat16* kv_pool, const int32_t* page_table, int page_size,
-                             int layer, __nv_bfloat16* o, cudaStream_t s);
+                             int layer, __nv_bfloat16* o, cudaStream_t s, const CUtensorMap* map_kv);
 void launch_rmsnorm(int w, const float* x, int d, const float* gain, float eps, __nv_bfloat16* h,
                     cudaStream_t s);
 void launch_init_matrix_interleaved(__nv_bfloat16* dst, uint64_t rows, uint64_t cols,

@@ -613,7 +613,7 @@ int enqueue_prefill_big(dd_ctx* ctx, int w) {
         eq.layer = l;
         CK(gemm(kGQkv, L.qkv, &ctx->map_h128, eq));
         if (launch_attention_prefill(ctx->d_ps, w, m, ctx->q, ctx->kv_pool, ctx->page_table, ctx->page_size,
-                                     l, ctx->o, s))
+                                     l, ctx->o, s, ctx->has_map_kv ? &ctx->map_kv : nullptr))
             return ctx_fail(ctx, DD_E_CUDA, "attention launch failed");
         GemmEpiParams er = e;
         er.kind = kEpiResidual;
@@ -908,6 +908,17 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
                             ctx->page_size * m.head_dim;
     CK(cudaMalloc(&ctx->kv_pool, sizeof(__nv_bfloat16) * (ctx->fp32acc ? 1 : kv_elems)));
     if (ctx->fp32acc) CK(cudaMalloc(&ctx->kv_f32, sizeof(float) * kv_elems));
+    if (!ctx->fp32acc) {
+        // finite everywhere: whole-page TMA staging reads rows past the last
+        // key, which reach the PV product with P = 0
+        CK(cudaMemset(ctx->kv_pool, 0, sizeof(__nv_bfloat16) * kv_elems));
+        if (m.head_dim == 128 && ctx->page_size <= 128 && 128 % ctx->page_size == 0) {
+            if (make_tmap_bf16(&ctx->map_kv, ctx->kv_pool, kv_elems / 128, 128,
+                               static_cast<uint32_t>(ctx->page_size)))
+                return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed (KV pool)");
+            ctx->has_map_kv = true;
+        }
+    }
     std::vector<int32_t> pt(ctx->n_pages);
     for (int i = 0; i < ctx->n_pages; ++i) pt[i] = i;
     CK(cudaMalloc(&ctx->page_table, sizeof(int32_t) * ctx->n_pages));
