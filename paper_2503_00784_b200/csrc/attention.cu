@@ -672,31 +672,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int kmax = n0 + min(W, 128 * (qt + 1)) - 1;  // last key of the CTA
     const int n_blk = kmax / kTcKeys + 1;
 
-    // staging (thread 0): per page of the block holding a key <= kmax, four
-    // TMA boxes (K / V x 64-dim halves) of page_size rows land as SW128 rows
-    // of the K-major (K) and MN-major (V) operand tiles; pages past kmax keep
-    // the buffer's earlier (finite) rows, masked to P = 0
+    // staging (warp 0, lane = (page, K / V, 64-dim half)): per page of the
+    // block holding a key <= kmax one TMA box of page_size rows lands as SW128
+    // rows of the K-major (K) or MN-major (V) operand tile; pages past kmax
+    // keep the buffer's earlier (finite) rows, masked to P = 0.  Page-table
+    // entries are read one block ahead, so issuing never waits on them.
     const uint64_t pol = policy_evict_normal();
-    auto stage = [&](int blk, int b) {
-        uint8_t* sk = sKV + b * 4 * kTcHalf;
-        uint8_t* sv = sk + 2 * kTcHalf;
+    const int st_pg = lane >> 2, st_kv = (lane >> 1) & 1, st_h = lane & 1;
+    auto page_of = [&](int blk) {
+        const int key = min(blk * kTcKeys + st_pg * page_size, kmax);
+        return __ldg(page_table + key / page_size);
+    };
+    auto stage = [&](int blk, int b, int page) {
         const int kb0 = blk * kTcKeys;
         const int n_pg = min(kTcKeys, kmax - kb0 + page_size) / page_size;  // pages with a live key
-        mbar_arrive_expect_tx(&bar[2 + b], static_cast<uint32_t>(n_pg * page_size * 128 * 4));
-        for (int pg = 0; pg < n_pg; ++pg) {
-            const int key = kb0 + pg * page_size;
-            const int page = page_table[key / page_size];
-            const int rk = static_cast<int>(kv_offset(md, page_size, page, layer, 0, kvh, 0) / HD);
-            const int rv = static_cast<int>(kv_offset(md, page_size, page, layer, 1, kvh, 0) / HD);
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                tma_load_2d(sk + hh * kTcHalf + pg * page_size * 128, &map_kv, &bar[2 + b], 64 * hh, rk, pol);
-                tma_load_2d(sv + hh * kTcHalf + pg * page_size * 128, &map_kv, &bar[2 + b], 64 * hh, rv, pol);
-            }
+        if (lane == 0) mbar_arrive_expect_tx(&bar[2 + b], static_cast<uint32_t>(n_pg * page_size * 128 * 4));
+        __syncwarp();
+        if (st_pg < n_pg) {
+            const int row = static_cast<int>(kv_offset(md, page_size, page, layer, st_kv, kvh, 0) / HD);
+            tma_load_2d(sKV + b * 4 * kTcHalf + (2 * st_kv + st_h) * kTcHalf + st_pg * page_size * 128, &map_kv,
+                        &bar[2 + b], 64 * st_h, row, pol);
         }
     };
     __syncthreads();  // barriers initialised, buffers zeroed
-    if (tid == 0) stage(0, 0);
+    int page_next = 0;
+    if (warp == 0) {
+        stage(0, 0, page_of(0));
+        if (n_blk > 1) page_next = page_of(1);
+    }
     {  // Q row (fp32 -> bf16) half, zero past the pass
         const float* src = q + static_cast<size_t>(row) * qd + head * HD;
 #pragma unroll 4
@@ -741,7 +744,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             umma_commit(&bar[0]);
         }
-        if (tid == 0 && blk + 1 < n_blk) stage(blk + 1, b ^ 1);  // loads under this block's MMAs and softmax
+        if (warp == 0 && blk + 1 < n_blk) {  // next block's K/V under this block's MMAs and softmax
+            stage(blk + 1, b ^ 1, page_next);
+            if (blk + 2 < n_blk) page_next = page_of(blk + 2);
+        }
         __syncwarp();
         mbar_wait(&bar[0], static_cast<uint32_t>(blk & 1));
         tc_fence_after();

@@ -912,7 +912,7 @@ int dd_ctx_create_tp(const dd_model_desc* desc, int cuda_device, int tp_rank, in
         // finite everywhere: whole-page TMA staging reads rows past the last
         // key, which reach the PV product with P = 0
         CK(cudaMemset(ctx->kv_pool, 0, sizeof(__nv_bfloat16) * kv_elems));
-        if (m.head_dim == 128 && ctx->page_size <= 128 && 128 % ctx->page_size == 0) {
+        if (m.head_dim == 128 && ctx->page_size >= 16 && ctx->page_size <= 128 && 128 % ctx->page_size == 0) {
             if (make_tmap_bf16(&ctx->map_kv, ctx->kv_pool, kv_elems / 128, 128,
                                static_cast<uint32_t>(ctx->page_size)))
                 return ctx_fail(ctx, DD_E_CUDA, "cuTensorMapEncodeTiled failed (KV pool)");
