@@ -766,7 +766,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if (kb + 16 * i + j <= pos) mx = fmaxf(mx, __uint_as_float(rr[i][j]) * scale_log2);
         }
         xch[h * 128 + r] = mx;
-        __syncthreads();
+        // only warps w and w + 4 share rows: a 64-thread named barrier per pair
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + (warp & 3)) : "memory");
         mx = fmaxf(xch[r], xch[128 + r]);
         const bool move = mx > m_base + 8.0f;  // false while both are -inf
         float corr = 1.0f;
