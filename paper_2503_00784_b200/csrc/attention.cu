@@ -754,8 +754,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int kb = blk * kTcKeys + 64 * h;  // first key of this thread's half
         // pass 1: max of the masked, scaled scores over the half, then the row's
         float mx = -INFINITY;
+        uint32_t srow[4][16];  // this thread's 64 scores, kept for pass 2
         {
-            uint32_t rr[4][16];
+            uint32_t (&rr)[4][16] = srow;
 #pragma unroll
             for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + 16 * i, rr[i]);
             tmem_wait_ld();
@@ -795,10 +796,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const float base = m_base == -INFINITY ? 0.f : m_base;
         // pass 2: P = exp2(s - base) as bf16 into the SW128 A tile, half sums in fp32
         {
-            uint32_t rr[4][16];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) tmem_ld16_async(tS + 16 * i, rr[i]);
-            tmem_wait_ld();
+            const uint32_t (&rr)[4][16] = srow;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 uint32_t pk[8];
